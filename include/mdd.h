@@ -1,0 +1,215 @@
+/*
+ * mdd.h — C-ABI of libmdd.so, the B200-native (sm_100a) hot path behind the
+ * reference package's Python API (maxwelldd, /root/reference/pkg/src/maxwelldd).
+ *
+ * The reference is pure Python; its "FFI" for this path is the set of Python
+ * functions listed against each entry point below.  The Python host layer in
+ * paper_1711_03789_b200/ binds these symbols with ctypes (paper_1711_03789_b200/
+ * _lib.py) and keeps the reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - complex128 is `mdd_complex` (two doubles, layout-identical to numpy
+ *     complex128 and CUDA double2);
+ *   - host pointers are caller-owned and only touched during the call;
+ *   - device objects live behind opaque handles owned by the library;
+ *   - every int-returning call returns an MDD_* code; on failure
+ *     mdd_last_error() holds a thread-local message (reference exception text
+ *     conventions: "subdomain {ell}: ...", "coarse space: ...").
+ *   - there is no CPU fallback: a call needing a GPU fails with MDD_ECUDA when
+ *     none is present.
+ */
+#ifndef MDD_H
+#define MDD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } mdd_complex;
+
+typedef struct mdd_ctx mdd_ctx;     /* one device + stream + scratch            */
+typedef struct mdd_csr mdd_csr;     /* device CSR (int32 indptr/indices)        */
+typedef struct mdd_space mdd_space; /* device mesh + edge space + CSR pattern   */
+typedef struct mdd_prec mdd_prec;   /* factorised Schwarz preconditioner        */
+
+enum {
+  MDD_OK = 0,
+  MDD_EINVAL = 1,    /* -> ValueError                                        */
+  MDD_ESINGULAR = 2, /* -> linalg.SingularMatrixError (reference linalg.py:33) */
+  MDD_ECAP = 3,      /* -> linalg.SizeCapError (reference linalg.py:37)        */
+  MDD_ECUDA = 4,     /* CUDA runtime failure / no device                        */
+  MDD_ENCCL = 5,
+  MDD_ENOMEM = 6,
+  MDD_EDECOMP = 7    /* -> decomp.DecompositionError (reference decomp.py:41)  */
+};
+
+/* ------------------------------------------------------------------ misc */
+const char* mdd_last_error(void);
+int mdd_version(void);
+int mdd_device_count(int* n);
+
+/* ---------------------------------------------------------------- context */
+int mdd_ctx_create(int device, mdd_ctx** out);
+void mdd_ctx_destroy(mdd_ctx* ctx);
+int mdd_ctx_synchronize(mdd_ctx* ctx);
+/* number of this library's kernels launched on the context so far */
+int64_t mdd_ctx_kernel_launches(const mdd_ctx* ctx);
+/* device-time of the last mdd_gmres phases (ms): [assembly-free] spmv, precond, arnoldi */
+int mdd_ctx_timers(const mdd_ctx* ctx, double* out6);
+int mdd_ctx_set_timing(mdd_ctx* ctx, int enable);
+
+/* ------------------------------------------------------------ CSR matrices
+ * Replaces scipy.sparse CSR storage + linalg.spmv (reference linalg.py:41-45)
+ * and the `a_mv = op @ v` of krylov._as_callable (reference krylov.py:58-61). */
+int mdd_csr_from_host(mdd_ctx* ctx, int64_t nrow, int64_t ncol, int64_t nnz,
+                      const int32_t* indptr, const int32_t* indices,
+                      const void* values, int is_complex, mdd_csr** out);
+int mdd_csr_info(const mdd_csr* A, int64_t* nrow, int64_t* ncol, int64_t* nnz,
+                 int* is_complex);
+int mdd_csr_to_host(const mdd_csr* A, int32_t* indptr, int32_t* indices, void* values);
+void mdd_csr_destroy(mdd_csr* A);
+/* y = A x with host vectors (complex; a real A acts on complex x) */
+int mdd_spmv(mdd_ctx* ctx, const mdd_csr* A, const mdd_complex* x, mdd_complex* y);
+/* timed device-resident SpMV loop for benchmarks: `reps` launches on device
+ * buffers, returns the average kernel time (ms) measured with CUDA events.   */
+int mdd_spmv_bench(mdd_ctx* ctx, const mdd_csr* A, int reps, double* ms_per_call);
+
+/* ------------------------------------------------------- space + assembly
+ * mdd_space_create uploads the mesh of reference mesh.build_cube_mesh
+ * (mesh.py:126-213) and the DOF map of fem.build_edge_space (fem.py:71-80)
+ * and builds the CSR pattern of fem._assemble_csr (fem.py:214-230). */
+int mdd_space_create(mdd_ctx* ctx, int32_t cells_per_axis,
+                     int64_t nv, const double* vertices,
+                     int64_t nt, const int64_t* tets, const int64_t* tet_edges,
+                     const int64_t* tet_edge_signs,
+                     int64_t ne, const int64_t* edge_to_dof, int64_t ndof,
+                     mdd_space** out);
+void mdd_space_destroy(mdd_space* sp);
+int mdd_space_nnz(const mdd_space* sp, int64_t* nnz);
+
+/* Coefficients (reference fem.py:83-123). Arrays are per tet or NULL (then the
+ * scalar eps0/mu0/sigma0 applies to all tets). */
+typedef struct {
+  double k, xi;
+  const double* eps;
+  const double* mu;
+  const double* sigma;
+  double eps0, mu0, sigma0;
+  int homogeneous; /* Coefficients.homogeneous (fem.py:111-120) */
+} mdd_coeffs;
+
+/* fem.assemble (fem.py:233-279): A (complex), S, M, Dk (real) on the space's
+ * pattern; impedance != 0 adds -i*sign(xi)*k*Mb over the nbf boundary faces
+ * (sorted vertex triples) and returns Mb (fem.py:258-263, 319-353).  Any
+ * output pointer may be NULL. */
+int mdd_assemble(mdd_space* sp, const mdd_coeffs* co, int impedance,
+                 int64_t nbf, const int64_t* bfaces,
+                 mdd_csr** A, mdd_csr** S, mdd_csr** M, mdd_csr** Dk, mdd_csr** Mb);
+/* fem.assemble_rhs (fem.py:373-390): fvals are the source values at the
+ * 4-point rule's points, layout (4, nt, 3) complex; rhs is host (ndof). */
+int mdd_assemble_rhs(mdd_space* sp, const mdd_complex* fvals, mdd_complex* rhs);
+/* Same, with the source F = amp * exp(-alpha*|x-c|^2) * dir evaluated on the
+ * device (fem.gaussian_source, fem.py:360-364, is amp=-1, alpha=400,
+ * c=(.5,.5,.5), dir=(1,1,1)). */
+int mdd_assemble_rhs_gaussian(mdd_space* sp, const double* center, double alpha,
+                              double amp, const double* dir, mdd_complex* rhs);
+/* fem.element_matrices / fem._element_matrices_batch (fem.py:177-207):
+ * coords (nt,4,3), signs (nt,6) as doubles; outputs (nt,6,6), (nt,6,6), (nt). */
+int mdd_element_matrices(mdd_ctx* ctx, int64_t nt, const double* coords,
+                         const double* signs, double* s_el, double* m_el, double* vol);
+
+/* ------------------------------------------------------ preconditioner
+ * precond.PreconditionerState.__init__ / setup (precond.py:280-323, 380-387)
+ * and PreconditionerState.apply (precond.py:347-375).
+ *
+ * Subdomain local problems are factorised by a batched multifrontal
+ * elimination over a geometric nested-dissection ordering (replaces the
+ * DenseLU/zgetrf of linalg.py:73-107); the coarse block R0 A R0^T is formed by
+ * an element-wise Galerkin kernel and factorised the same way. */
+typedef struct {
+  int family;      /* 0 as, 1 ras, 2 impras   (precond.py:172)               */
+  int levels;      /* 1 or 2                                                 */
+  int correction;  /* 0 additive, 1 hybrid, 2 adef1 (precond.py:173)         */
+  int64_t lu_cap;  /* SizeCapError threshold on a local block, <=0: none     */
+  int leaf_size;   /* nested-dissection leaf size (0 -> default)             */
+  /* fine level */
+  const mdd_csr* A_prec;  /* assembled at xi_prec (precond.py:285-287)       */
+  const mdd_csr* A_corr;  /* matrix inside hybrid/adef1 (precond.py:289)     */
+  int32_t nsub;
+  const int64_t* sub_ptr;   /* nsub+1 offsets into sub_dofs                  */
+  const int64_t* sub_dofs;  /* sorted global DOF sets I_l (decomp.py:140-191) */
+  const double* sub_pou;    /* aligned weights (decomp.py:194-205) or NULL   */
+  const int32_t* dof_xyz;   /* (ndof,3) edge midpoints in half-cell units    */
+  /* impras: local matrices assembled on the submesh (precond.py:212-269)    */
+  const mdd_space* space;   /* fine space (for impras local assembly)        */
+  const mdd_coeffs* prec_coeffs;
+  const int64_t* sub_tet_ptr; /* nsub+1 offsets into sub_tets (impras)        */
+  const int64_t* sub_tets;    /* per-subdomain tet lists (decomp.elements)    */
+  const int64_t* sub_bface_ptr; /* nsub+1 offsets (impras boundary faces)     */
+  const int64_t* sub_bfaces;    /* (.,3) sorted vertex triples                */
+  /* coarse level (levels == 2) */
+  const mdd_csr* R0;          /* (ncs x ndof) real, decomp.py:212-297        */
+  const mdd_space* coarse_space;
+  const int64_t* tet_map;     /* fine tet -> coarse tet (mesh.py:231-263)    */
+  const int32_t* coarse_dof_xyz; /* (ncs,3) half-cell units of the coarse mesh */
+  int64_t nbf_global;         /* global impedance faces (bc=impedance) or 0  */
+  const int64_t* bfaces_global;
+} mdd_prec_desc;
+
+/* On MDD_ESINGULAR/MDD_ECAP, *failed_ctx is the subdomain id, or -1 for the
+ * coarse space. */
+int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* desc, mdd_prec** out,
+                    int32_t* failed_ctx);
+/* PreconditionerState.variant (precond.py:325-343): a view sharing factors. */
+int mdd_prec_variant(const mdd_prec* base, int family, int levels, int correction,
+                     const mdd_csr* A_corr, mdd_prec** out);
+void mdd_prec_destroy(mdd_prec* P);
+int mdd_prec_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
+/* PreconditionerState.coarse_solve (precond.py:357-358): R0^T A0^{-1} R0 v */
+int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
+/* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
+ *              levels, sum_local_dofs, coarse_n] */
+int mdd_prec_stats(const mdd_prec* P, double* out8);
+/* refactorise in place (same pattern) from new A_prec values: the numeric part
+ * of setup, used by the benchmark's timed step */
+int mdd_prec_refactor(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* prec_coeffs);
+
+/* ------------------------------------------------------------------ GMRES
+ * krylov.gmres (krylov.py:64-209): unrestarted GMRES, MGS + one
+ * reorthogonalisation pass, complex Givens rotations, right/left
+ * preconditioning, optional Hermitian positive definite weight D. */
+typedef int (*mdd_host_op)(void* user, int64_t n, const mdd_complex* in, mdd_complex* out);
+
+typedef struct {
+  double tol;
+  int32_t maxit;
+  int32_t side;          /* 0 right, 1 left                                   */
+  int32_t check_drift;   /* 1: compute the orthogonality drift (krylov.py:152) */
+  int32_t keep_basis;
+} mdd_gmres_cfg;
+
+typedef struct {
+  /* operator: exactly one of A / a_fn */
+  const mdd_csr* A;
+  mdd_host_op a_fn; void* a_user;
+  /* preconditioner: P, m_fn or neither */
+  mdd_prec* P;
+  mdd_host_op m_fn; void* m_user;
+  const mdd_csr* Mcsr;   /* preconditioner given as a matrix */
+  /* weight: D (CSR) or NULL */
+  const mdd_csr* D;
+} mdd_gmres_ops;
+
+int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n,
+              const mdd_complex* b, const mdd_complex* x0 /* NULL = zero */,
+              const mdd_gmres_cfg* cfg,
+              mdd_complex* x, double* history /* maxit+1 */,
+              double* drift /* maxit+1, NULL ok */, mdd_complex* basis /* (maxit+1)*n or NULL */,
+              int32_t* iterations, int32_t* converged, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDD_H */

@@ -1,0 +1,252 @@
+"""ctypes binding of libmdd.so (the C-ABI declared in include/mdd.h).
+
+The shared library is built in-tree (``python -m paper_1711_03789_b200.build``)
+and is the only compute path: there is no CPU fallback.  Importing this
+module on a machine without the library raises immediately; creating a
+context without a GPU raises ``RuntimeError`` from ``mdd_ctx_create``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmdd.so")
+
+MDD_OK, MDD_EINVAL, MDD_ESINGULAR, MDD_ECAP, MDD_ECUDA, MDD_ENCCL, MDD_ENOMEM, MDD_EDECOMP = range(8)
+
+
+class mdd_complex(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+class mdd_coeffs(C.Structure):
+    _fields_ = [
+        ("k", C.c_double),
+        ("xi", C.c_double),
+        ("eps", C.POINTER(C.c_double)),
+        ("mu", C.POINTER(C.c_double)),
+        ("sigma", C.POINTER(C.c_double)),
+        ("eps0", C.c_double),
+        ("mu0", C.c_double),
+        ("sigma0", C.c_double),
+        ("homogeneous", C.c_int),
+    ]
+
+
+class mdd_prec_desc(C.Structure):
+    _fields_ = [
+        ("family", C.c_int),
+        ("levels", C.c_int),
+        ("correction", C.c_int),
+        ("lu_cap", C.c_int64),
+        ("leaf_size", C.c_int),
+        ("A_prec", C.c_void_p),
+        ("A_corr", C.c_void_p),
+        ("nsub", C.c_int32),
+        ("sub_ptr", C.POINTER(C.c_int64)),
+        ("sub_dofs", C.POINTER(C.c_int64)),
+        ("sub_pou", C.POINTER(C.c_double)),
+        ("dof_xyz", C.POINTER(C.c_int32)),
+        ("space", C.c_void_p),
+        ("prec_coeffs", C.POINTER(mdd_coeffs)),
+        ("sub_tet_ptr", C.POINTER(C.c_int64)),
+        ("sub_tets", C.POINTER(C.c_int64)),
+        ("sub_bface_ptr", C.POINTER(C.c_int64)),
+        ("sub_bfaces", C.POINTER(C.c_int64)),
+        ("R0", C.c_void_p),
+        ("coarse_space", C.c_void_p),
+        ("tet_map", C.POINTER(C.c_int64)),
+        ("coarse_dof_xyz", C.POINTER(C.c_int32)),
+        ("nbf_global", C.c_int64),
+        ("bfaces_global", C.POINTER(C.c_int64)),
+    ]
+
+
+HOST_OP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(mdd_complex), C.POINTER(mdd_complex))
+
+
+class mdd_gmres_cfg(C.Structure):
+    _fields_ = [
+        ("tol", C.c_double),
+        ("maxit", C.c_int32),
+        ("side", C.c_int32),
+        ("check_drift", C.c_int32),
+        ("keep_basis", C.c_int32),
+    ]
+
+
+class mdd_gmres_ops(C.Structure):
+    _fields_ = [
+        ("A", C.c_void_p),
+        ("a_fn", HOST_OP),
+        ("a_user", C.c_void_p),
+        ("P", C.c_void_p),
+        ("m_fn", HOST_OP),
+        ("m_user", C.c_void_p),
+        ("Mcsr", C.c_void_p),
+        ("D", C.c_void_p),
+    ]
+
+
+_P = C.c_void_p
+_PP = C.POINTER(C.c_void_p)
+_i64 = C.c_int64
+_i32 = C.c_int32
+_pd = C.POINTER(C.c_double)
+_pz = C.POINTER(mdd_complex)
+_pi64 = C.POINTER(C.c_int64)
+_pi32 = C.POINTER(C.c_int32)
+
+# name -> (restype, argtypes); mirrors include/mdd.h one-to-one
+SIGNATURES = {
+    "mdd_last_error": (C.c_char_p, []),
+    "mdd_version": (C.c_int, []),
+    "mdd_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "mdd_ctx_create": (C.c_int, [C.c_int, _PP]),
+    "mdd_ctx_destroy": (None, [_P]),
+    "mdd_ctx_synchronize": (C.c_int, [_P]),
+    "mdd_ctx_kernel_launches": (C.c_int64, [_P]),
+    "mdd_ctx_timers": (C.c_int, [_P, _pd]),
+    "mdd_ctx_set_timing": (C.c_int, [_P, C.c_int]),
+    "mdd_csr_from_host": (C.c_int, [_P, _i64, _i64, _i64, _pi32, _pi32, C.c_void_p, C.c_int, _PP]),
+    "mdd_csr_info": (C.c_int, [_P, _pi64, _pi64, _pi64, C.POINTER(C.c_int)]),
+    "mdd_csr_to_host": (C.c_int, [_P, _pi32, _pi32, C.c_void_p]),
+    "mdd_csr_destroy": (None, [_P]),
+    "mdd_spmv": (C.c_int, [_P, _P, _pz, _pz]),
+    "mdd_spmv_bench": (C.c_int, [_P, _P, C.c_int, _pd]),
+    "mdd_space_create": (
+        C.c_int,
+        [_P, _i32, _i64, _pd, _i64, _pi64, _pi64, _pi64, _i64, _pi64, _i64, _PP],
+    ),
+    "mdd_space_destroy": (None, [_P]),
+    "mdd_space_nnz": (C.c_int, [_P, _pi64]),
+    "mdd_assemble": (
+        C.c_int,
+        [_P, C.POINTER(mdd_coeffs), C.c_int, _i64, _pi64, _PP, _PP, _PP, _PP, _PP],
+    ),
+    "mdd_assemble_rhs": (C.c_int, [_P, _pz, _pz]),
+    "mdd_assemble_rhs_gaussian": (C.c_int, [_P, _pd, C.c_double, C.c_double, _pd, _pz]),
+    "mdd_element_matrices": (C.c_int, [_P, _i64, _pd, _pd, _pd, _pd, _pd]),
+    "mdd_prec_create": (C.c_int, [_P, C.POINTER(mdd_prec_desc), _PP, _pi32]),
+    "mdd_prec_variant": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _PP]),
+    "mdd_prec_destroy": (None, [_P]),
+    "mdd_prec_apply": (C.c_int, [_P, _pz, _pz]),
+    "mdd_prec_coarse_apply": (C.c_int, [_P, _pz, _pz]),
+    "mdd_prec_stats": (C.c_int, [_P, _pd]),
+    "mdd_prec_refactor": (C.c_int, [_P, _P, C.POINTER(mdd_coeffs)]),
+    "mdd_gmres": (
+        C.c_int,
+        [
+            _P,
+            C.POINTER(mdd_gmres_ops),
+            _i64,
+            _pz,
+            _pz,
+            C.POINTER(mdd_gmres_cfg),
+            _pz,
+            _pd,
+            _pd,
+            _pz,
+            _pi32,
+            _pi32,
+            _pd,
+        ],
+    ),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python paper_1711_03789_b200/build.py` "
+            "(the package has no CPU fallback)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class MddError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def check(rc: int):
+    if rc != MDD_OK:
+        msg = lib.mdd_last_error().decode("utf-8", "replace")
+        raise MddError(rc, msg)
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def zptr(a: np.ndarray):
+    assert a.dtype == np.complex128 and a.flags.c_contiguous
+    return a.ctypes.data_as(_pz)
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One CUDA device + stream (opaque ``mdd_ctx``)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.mdd_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def synchronize(self):
+        check(lib.mdd_ctx_synchronize(self.handle))
+
+    def kernel_launches(self) -> int:
+        return int(lib.mdd_ctx_kernel_launches(self.handle))
+
+    def set_timing(self, on: bool):
+        check(lib.mdd_ctx_set_timing(self.handle, 1 if on else 0))
+
+    def timers(self):
+        out = (C.c_double * 6)()
+        check(lib.mdd_ctx_timers(self.handle, out))
+        return list(out)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            lib.mdd_ctx_destroy(h)
+            self.handle = None
+
+
+_ctx = None
+_ctx_lock = threading.Lock()
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib.mdd_device_count(C.byref(n)))
+    return n.value
+
+
+def get_context() -> Context:
+    """Process-wide default context on ``LOCAL_RANK`` (or device 0)."""
+    global _ctx
+    with _ctx_lock:
+        if _ctx is None:
+            _ctx = Context(int(os.environ.get("MDD_DEVICE", os.environ.get("LOCAL_RANK", "0"))))
+        return _ctx
+
+
+def exported_symbols():
+    return list(SIGNATURES)

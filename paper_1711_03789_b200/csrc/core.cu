@@ -1,0 +1,300 @@
+// Context, CSR storage, complex128 CSR SpMV and small vector kernels.
+//
+// SpMV replaces `a_mv = op @ v` (reference krylov.py:58-61, 95-97) and
+// linalg.spmv (reference linalg.py:41-45).  HBM-bound: 16 B value + 4 B column
+// per nonzero; a group of TPR lanes owns one row so the row's values and
+// columns are read as contiguous 16 B / 4 B segments; the group reduces with
+// shuffles (fixed order, so reruns are bitwise identical).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "mdd_internal.h"
+#include "mdd_kernels.cuh"
+
+namespace mdd {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+std::shared_ptr<mdd_pattern> make_pattern(int64_t nrow, int64_t ncol,
+                                          std::vector<int32_t>&& rowptr,
+                                          std::vector<int32_t>&& cols, cudaStream_t s) {
+  auto p = std::make_shared<mdd_pattern>();
+  p->nrow = nrow;
+  p->ncol = ncol;
+  p->nnz = (int64_t)cols.size();
+  p->h_rowptr = std::move(rowptr);
+  p->h_cols = std::move(cols);
+  p->rowptr.upload(p->h_rowptr, s);
+  p->cols.upload(p->h_cols, s);
+  return p;
+}
+
+// ------------------------------------------------------------------ SpMV
+template <bool CPLX, int TPR>
+__global__ void __launch_bounds__(256) k_spmv(int64_t nrow, const int32_t* __restrict__ rowptr,
+                                              const int32_t* __restrict__ cols,
+                                              const double* __restrict__ vals,
+                                              const double2* __restrict__ x,
+                                              double2* __restrict__ y, double2 alpha,
+                                              double2 beta, const double2* __restrict__ z) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / TPR;
+  const int lane = threadIdx.x % TPR;
+  if (row >= nrow) return;  // TPR divides 32: whole groups exit together
+  const int b = rowptr[row], e = rowptr[row + 1];
+  double re = 0.0, im = 0.0;
+  for (int j = b + lane; j < e; j += TPR) {
+    const double2 xv = x[cols[j]];
+    if (CPLX) {
+      const double2 a = reinterpret_cast<const double2*>(vals)[j];
+      re += a.x * xv.x - a.y * xv.y;
+      im += a.x * xv.y + a.y * xv.x;
+    } else {
+      const double a = vals[j];
+      re += a * xv.x;
+      im += a * xv.y;
+    }
+  }
+#pragma unroll
+  for (int off = TPR / 2; off > 0; off >>= 1) {
+    re += __shfl_down_sync(0xffffffffu, re, off, TPR);
+    im += __shfl_down_sync(0xffffffffu, im, off, TPR);
+  }
+  if (lane == 0) {
+    double2 r = make_double2(alpha.x * re - alpha.y * im, alpha.x * im + alpha.y * re);
+    if (z) {
+      const double2 zz = z[row];
+      r.x += beta.x * zz.x - beta.y * zz.y;
+      r.y += beta.x * zz.y + beta.y * zz.x;
+    }
+    y[row] = r;
+  }
+}
+
+template <int TPR>
+static void launch_spmv_t(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y,
+                          double2 alpha, double2 beta, const double2* z, cudaStream_t s) {
+  const int64_t threads = A->nrow() * TPR;
+  const int bs = 256;
+  const int64_t grid = (threads + bs - 1) / bs;
+  if (grid == 0) return;
+  if (A->is_complex)
+    k_spmv<true, TPR><<<(unsigned)grid, bs, 0, s>>>(A->nrow(), A->pat->rowptr.p, A->pat->cols.p,
+                                                   A->vals.p, x, y, alpha, beta, z);
+  else
+    k_spmv<false, TPR><<<(unsigned)grid, bs, 0, s>>>(A->nrow(), A->pat->rowptr.p, A->pat->cols.p,
+                                                    A->vals.p, x, y, alpha, beta, z);
+  CK_LAUNCH(ctx);
+}
+
+void spmv_dev_axpby(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y,
+                    double2 alpha, double2 beta, const double2* z, cudaStream_t s) {
+  const double avg = A->nrow() ? (double)A->nnz() / (double)A->nrow() : 0.0;
+  if (avg > 48)
+    launch_spmv_t<32>(ctx, A, x, y, alpha, beta, z, s);
+  else if (avg > 12)
+    launch_spmv_t<8>(ctx, A, x, y, alpha, beta, z, s);
+  else
+    launch_spmv_t<4>(ctx, A, x, y, alpha, beta, z, s);
+}
+
+void spmv_dev(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y, cudaStream_t s) {
+  spmv_dev_axpby(ctx, A, x, y, make_double2(1.0, 0.0), make_double2(0.0, 0.0), nullptr, s);
+}
+
+// ---------------------------------------------------------- vector kernels
+__global__ void k_vec_sub(const double2* a, const double2* b, double2* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 u = a[i], v = b[i];
+    out[i] = make_double2(u.x - v.x, u.y - v.y);
+  }
+}
+__global__ void k_vec_add(const double2* a, const double2* b, double2* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 u = a[i], v = b[i];
+    out[i] = make_double2(u.x + v.x, u.y + v.y);
+  }
+}
+static unsigned grid_for(int64_t n, int bs, int nsm) {
+  int64_t g = (n + bs - 1) / bs;
+  const int64_t cap = (int64_t)nsm * 16;
+  if (g > cap) g = cap;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+void vec_sub(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int64_t n,
+             cudaStream_t s) {
+  k_vec_sub<<<grid_for(n, 256, ctx->nsm), 256, 0, s>>>(a, b, out, n);
+  CK_LAUNCH(ctx);
+}
+void vec_add(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int64_t n,
+             cudaStream_t s) {
+  k_vec_add<<<grid_for(n, 256, ctx->nsm), 256, 0, s>>>(a, b, out, n);
+  CK_LAUNCH(ctx);
+}
+}  // namespace mdd
+
+using namespace mdd;
+
+void* mdd_ctx::pinned_buf(size_t bytes) {
+  if (bytes > pinned_bytes) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    size_t nb = bytes < (1u << 20) ? (1u << 20) : bytes;
+    CK(cudaMallocHost(&pinned, nb));
+    pinned_bytes = nb;
+  }
+  return pinned;
+}
+
+extern "C" {
+
+const char* mdd_last_error(void) { return g_last_error.c_str(); }
+int mdd_version(void) { return 1; }
+
+int mdd_device_count(int* n) {
+  MDD_API_BEGIN
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *n = c;
+  MDD_API_END
+}
+
+int mdd_ctx_create(int device, mdd_ctx** out) {
+  MDD_API_BEGIN
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(MDD_ECUDA, "no CUDA device available: libmdd has no CPU fallback");
+  }
+  if (device < 0 || device >= count) fail(MDD_EINVAL, "device index out of range");
+  CK(cudaSetDevice(device));
+  auto c = new mdd_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  c->nsm = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  *out = c;
+  MDD_API_END
+}
+
+void mdd_ctx_destroy(mdd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int mdd_ctx_synchronize(mdd_ctx* ctx) {
+  MDD_API_BEGIN
+  CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+int64_t mdd_ctx_kernel_launches(const mdd_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int mdd_ctx_timers(const mdd_ctx* ctx, double* out6) {
+  MDD_API_BEGIN
+  for (int i = 0; i < 6; ++i) out6[i] = ctx->timers[i];
+  MDD_API_END
+}
+
+int mdd_ctx_set_timing(mdd_ctx* ctx, int enable) {
+  MDD_API_BEGIN
+  ctx->timing = enable != 0;
+  MDD_API_END
+}
+
+int mdd_csr_from_host(mdd_ctx* ctx, int64_t nrow, int64_t ncol, int64_t nnz,
+                      const int32_t* indptr, const int32_t* indices, const void* values,
+                      int is_complex, mdd_csr** out) {
+  MDD_API_BEGIN
+  if (nrow < 0 || ncol < 0 || nnz < 0) fail(MDD_EINVAL, "negative CSR dimensions");
+  if (nnz > INT32_MAX) fail(MDD_EINVAL, "CSR with more than 2^31 nonzeros");
+  CK(cudaSetDevice(ctx->device));
+  std::vector<int32_t> rp(indptr, indptr + nrow + 1);
+  std::vector<int32_t> cl(indices, indices + nnz);
+  if (rp[0] != 0 || rp[nrow] != nnz) fail(MDD_EINVAL, "inconsistent CSR indptr");
+  auto A = new mdd_csr();
+  A->ctx = ctx;
+  A->pat = make_pattern(nrow, ncol, std::move(rp), std::move(cl), ctx->stream);
+  A->is_complex = is_complex != 0;
+  const size_t nv = (size_t)nnz * (A->is_complex ? 2 : 1);
+  A->vals.upload(reinterpret_cast<const double*>(values), nv, ctx->stream);
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = A;
+  MDD_API_END
+}
+
+int mdd_csr_info(const mdd_csr* A, int64_t* nrow, int64_t* ncol, int64_t* nnz, int* is_complex) {
+  MDD_API_BEGIN
+  *nrow = A->nrow();
+  *ncol = A->ncol();
+  *nnz = A->nnz();
+  *is_complex = A->is_complex ? 1 : 0;
+  MDD_API_END
+}
+
+int mdd_csr_to_host(const mdd_csr* A, int32_t* indptr, int32_t* indices, void* values) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(A->ctx->device));
+  if (indptr) memcpy(indptr, A->pat->h_rowptr.data(), sizeof(int32_t) * (A->nrow() + 1));
+  if (indices) memcpy(indices, A->pat->h_cols.data(), sizeof(int32_t) * A->nnz());
+  if (values) {
+    A->vals.download(reinterpret_cast<double*>(values),
+                     (size_t)A->nnz() * (A->is_complex ? 2 : 1), A->ctx->stream);
+    CK(cudaStreamSynchronize(A->ctx->stream));
+  }
+  MDD_API_END
+}
+
+void mdd_csr_destroy(mdd_csr* A) {
+  if (!A) return;
+  cudaSetDevice(A->ctx->device);
+  delete A;
+}
+
+int mdd_spmv(mdd_ctx* ctx, const mdd_csr* A, const mdd_complex* x, mdd_complex* y) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  DevBuf<double2> dx(A->ncol()), dy(A->nrow());
+  dx.upload(reinterpret_cast<const double2*>(x), A->ncol(), ctx->stream);
+  spmv_dev(ctx, A, dx.p, dy.p, ctx->stream);
+  dy.download(reinterpret_cast<double2*>(y), A->nrow(), ctx->stream);
+  CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+int mdd_spmv_bench(mdd_ctx* ctx, const mdd_csr* A, int reps, double* ms_per_call) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  DevBuf<double2> dx(A->ncol()), dy(A->nrow());
+  CK(cudaMemsetAsync(dx.p, 0, sizeof(double2) * dx.n, ctx->stream));
+  for (int i = 0; i < 3; ++i) spmv_dev(ctx, A, dx.p, dy.p, ctx->stream);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  for (int i = 0; i < reps; ++i) spmv_dev(ctx, A, dx.p, dy.p, ctx->stream);
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_per_call = reps > 0 ? ms / reps : 0.0;
+  MDD_API_END
+}
+
+}  // extern "C"

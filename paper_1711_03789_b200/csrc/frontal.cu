@@ -1,0 +1,639 @@
+// Batched multifrontal factorisation (block Gauss-Jordan sweeps) and
+// forward/backward solves.  See frontal.h for the algebra.
+//
+// Replaces linalg.DenseLU (zgetrf, reference linalg.py:73-101) and
+// DenseLU.solve (zgetrs, linalg.py:103-107) as used per subdomain and for
+// the coarse block in precond.PreconditionerState (precond.py:296-322,
+// 347-358).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "frontal.h"
+#include "mdd_kernels.cuh"
+
+namespace mdd {
+
+// ------------------------------------------------------------ kernels
+// warp per (node,row): F[row][:] = sum_children S_child[g(row)][g(:)]
+__global__ void __launch_bounds__(256) k_front_init(const int2* __restrict__ tasks, int64_t ntask,
+                                                    const NodeDev* __restrict__ nodes,
+                                                    const int32_t* __restrict__ children,
+                                                    const int32_t* __restrict__ gmap,
+                                                    double2* __restrict__ fronts) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ntask) return;
+  const int2 tk = tasks[w];
+  const NodeDev nd = nodes[tk.x];
+  const int r = tk.y, m = nd.m;
+  double2* row = fronts + nd.front_off + (int64_t)r * m;
+  for (int q = lane; q < m; q += 32) row[q] = make_double2(0.0, 0.0);
+  for (int ci = 0; ci < nd.nch; ++ci) {
+    const NodeDev ch = nodes[children[nd.child_off + ci]];
+    const int32_t* g = gmap + nd.gmap_off + (int64_t)ci * m;
+    const int gr = g[r];
+    if (gr < 0) continue;
+    const double2* S = fronts + ch.front_off + (int64_t)(ch.np + gr) * ch.m + ch.np;
+    for (int q = lane; q < m; q += 32) {
+      const int gq = g[q];
+      if (gq >= 0) row[q] = cadd(row[q], S[gq]);
+    }
+  }
+}
+
+__global__ void k_front_scatter(int64_t n, const int64_t* __restrict__ pos,
+                                const int32_t* __restrict__ src, const double2* __restrict__ vals,
+                                double2* __restrict__ fronts) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos[e];
+    fronts[p] = cadd(fronts[p], vals[src[e]]);
+  }
+}
+
+// In-place Gauss-Jordan inverse of the kb x kb pivot block (no pivoting),
+// padded with the identity to 32x32; tracks pivot magnitudes.
+__global__ void __launch_bounds__(1024) k_invert(const NodeDev* __restrict__ nodes,
+                                                 const int32_t* __restrict__ act, int step,
+                                                 const double2* __restrict__ fronts,
+                                                 double2* __restrict__ pbuf,
+                                                 double* __restrict__ pivstat) {
+  __shared__ double2 P[kPB][kPB + 1];
+  const int node = act[blockIdx.x];
+  const NodeDev nd = nodes[node];
+  const int K0 = step * kPB;
+  const int kb = min(kPB, nd.np - K0);
+  const int i = threadIdx.x >> 5, j = threadIdx.x & 31;
+  const double2* T = fronts + nd.front_off;
+  P[i][j] = (i < kb && j < kb) ? T[(int64_t)(K0 + i) * nd.m + K0 + j]
+                               : make_double2(i == j ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  double pmin = INFINITY, pmax = 0.0;
+  for (int p = 0; p < kb; ++p) {
+    const double2 piv = P[p][p];
+    const double2 aip = P[i][p];
+    __syncthreads();
+    if (i == p) P[p][j] = cdiv(j == p ? make_double2(1.0, 0.0) : P[p][j], piv);
+    __syncthreads();
+    if (i != p) {
+      const double2 base = (j == p) ? make_double2(0.0, 0.0) : P[i][j];
+      P[i][j] = csub(base, cmul(aip, P[p][j]));
+    }
+    const double a = hypot(piv.x, piv.y);
+    pmin = fmin(pmin, isfinite(a) ? a : 0.0);
+    pmax = fmax(pmax, isfinite(a) ? a : INFINITY);
+    __syncthreads();
+  }
+  pbuf[(int64_t)blockIdx.x * kPB * kPB + i * kPB + j] = P[i][j];
+  if (threadIdx.x == 0) {
+    pivstat[2 * node] = fmin(pivstat[2 * node], pmin);
+    pivstat[2 * node + 1] = fmax(pivstat[2 * node + 1], pmax);
+  }
+}
+
+// Row panel F[K][c] <- P F[K][c] (c outside K), F[K][K] <- -P, and the copy
+// W[r][:] = old F[r][K] (r outside K) used by the trailing update.
+__global__ void __launch_bounds__(kPanelCols) k_panel(const int2* __restrict__ tasks,
+                                                      const NodeDev* __restrict__ nodes,
+                                                      const int32_t* __restrict__ act,
+                                                      const int64_t* __restrict__ woff, int step,
+                                                      double2* __restrict__ fronts,
+                                                      const double2* __restrict__ pbuf,
+                                                      double2* __restrict__ wbuf) {
+  __shared__ double2 P[kPB][kPB + 1];
+  const int2 tk = tasks[blockIdx.x];
+  const int ai = tk.x, chunk = tk.y;
+  const NodeDev nd = nodes[act[ai]];
+  const int m = nd.m;
+  const int K0 = step * kPB;
+  const int kb = min(kPB, nd.np - K0);
+  for (int t = threadIdx.x; t < kPB * kPB; t += blockDim.x)
+    P[t / kPB][t % kPB] = pbuf[(int64_t)ai * kPB * kPB + t];
+  __syncthreads();
+  double2* T = fronts + nd.front_off;
+  const int c = chunk * kPanelCols + threadIdx.x;
+  if (c < m) {
+    if (c >= K0 && c < K0 + kb) {
+      for (int r = 0; r < kb; ++r) T[(int64_t)(K0 + r) * m + c] = cneg(P[r][c - K0]);
+    } else {
+      double2 x[kPB];
+#pragma unroll
+      for (int l = 0; l < kPB; ++l)
+        x[l] = l < kb ? T[(int64_t)(K0 + l) * m + c] : make_double2(0.0, 0.0);
+      for (int r = 0; r < kb; ++r) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int l = 0; l < kPB; ++l) acc = cfma(P[r][l], x[l], acc);
+        T[(int64_t)(K0 + r) * m + c] = acc;
+      }
+    }
+  }
+  // W copy: rows [chunk*128, chunk*128+128)
+  double2* W = wbuf + woff[ai];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int rr = wid; rr < kPanelCols; rr += kPanelCols / 32) {
+    const int r = chunk * kPanelCols + rr;
+    if (r >= m) break;
+    const bool inK = r >= K0 && r < K0 + kb;
+    W[(int64_t)r * kPB + lane] =
+        (inK || lane >= kb) ? make_double2(0.0, 0.0) : T[(int64_t)r * m + K0 + lane];
+  }
+}
+
+// Trailing update of one 64x64 tile:  F[r][c] = (c in K ? 0 : F[r][c]) - W[r][:] F[K][c]
+__global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
+                                                const NodeDev* __restrict__ nodes,
+                                                const int32_t* __restrict__ act,
+                                                const int64_t* __restrict__ woff, int step,
+                                                double2* __restrict__ fronts,
+                                                const double2* __restrict__ wbuf) {
+  extern __shared__ double2 sm[];
+  double2(*Ws)[kPB + 1] = reinterpret_cast<double2(*)[kPB + 1]>(sm);
+  double2(*Ks)[kTile + 1] = reinterpret_cast<double2(*)[kTile + 1]>(sm + kTile * (kPB + 1));
+  const int4 tk = tasks[blockIdx.x];
+  const int ai = tk.x;
+  const NodeDev nd = nodes[act[ai]];
+  const int m = nd.m;
+  const int K0 = step * kPB;
+  const int kb = min(kPB, nd.np - K0);
+  const int r0 = tk.y * kTile, c0 = tk.z * kTile;
+  const double2* W = wbuf + woff[ai];
+  double2* T = fronts + nd.front_off;
+  for (int t = threadIdx.x; t < kTile * kPB; t += blockDim.x) {
+    const int rr = t / kPB, l = t % kPB;
+    const int r = r0 + rr;
+    Ws[rr][l] = r < m ? W[(int64_t)r * kPB + l] : make_double2(0.0, 0.0);
+  }
+  for (int t = threadIdx.x; t < kTile * kPB; t += blockDim.x) {
+    const int l = t / kTile, cc = t % kTile;
+    const int c = c0 + cc;
+    Ks[l][cc] = (l < kb && c < m) ? T[(int64_t)(K0 + l) * m + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  double2 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+#pragma unroll 4
+  for (int l = 0; l < kPB; ++l) {
+    double2 wv[4], kv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) wv[a] = Ws[ty + 16 * a][l];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) kv[b] = Ks[l][tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = cfma(wv[a], kv[b], acc[a][b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = r0 + ty + 16 * a;
+    if (r >= m || (r >= K0 && r < K0 + kb)) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = c0 + tx + 16 * b;
+      if (c >= m) continue;
+      double2* p = T + (int64_t)r * m + c;
+      const double2 old = (c >= K0 && c < K0 + kb) ? make_double2(0.0, 0.0) : *p;
+      *p = csub(old, acc[a][b]);
+    }
+  }
+}
+
+__global__ void k_pivinit(double* p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    p[2 * i] = INFINITY;
+    p[2 * i + 1] = 0.0;
+  }
+}
+
+// forward: fp = b_P + children contributions ; uvec = (children contributions)_U - F_UP fp
+__global__ void __launch_bounds__(256) k_fwd(const int2* __restrict__ tasks,
+                                             const NodeDev* __restrict__ nodes,
+                                             const int32_t* __restrict__ children,
+                                             const int32_t* __restrict__ gmap,
+                                             const double2* __restrict__ fronts,
+                                             const double2* __restrict__ bloc,
+                                             double2* __restrict__ fpst, double2* __restrict__ uvec) {
+  extern __shared__ double2 fp[];
+  const int2 tk = tasks[blockIdx.x];
+  const NodeDev nd = nodes[tk.x];
+  const int r0 = tk.y;
+  const int np = nd.np, m = nd.m;
+  const int64_t base = (int64_t)nd.mat_off + nd.pivb;
+  for (int q = threadIdx.x; q < np; q += blockDim.x) {
+    double2 f = bloc[base + q];
+    for (int ci = 0; ci < nd.nch; ++ci) {
+      const int g = gmap[nd.gmap_off + (int64_t)ci * m + q];
+      if (g >= 0) f = cadd(f, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
+    }
+    fp[q] = f;
+    if (r0 == 0) fpst[base + q] = f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int rr = wid; rr < kSolveRows; rr += blockDim.x >> 5) {
+    const int u = r0 + rr;
+    if (u >= nd.nu) break;
+    const double2* row = fronts + nd.front_off + (int64_t)(np + u) * m;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = lane; q < np; q += 32) acc = cfma(row[q], fp[q], acc);
+    acc = warp_sum2(acc);
+    if (lane == 0) {
+      double2 fu = make_double2(0.0, 0.0);
+      for (int ci = 0; ci < nd.nch; ++ci) {
+        const int g = gmap[nd.gmap_off + (int64_t)ci * m + np + u];
+        if (g >= 0) fu = cadd(fu, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
+      }
+      uvec[nd.uvec_off + u] = csub(fu, acc);
+    }
+  }
+}
+
+// backward: x_P = -(F_PP fp + F_PU x_U)
+__global__ void __launch_bounds__(256) k_bwd(const int2* __restrict__ tasks,
+                                             const NodeDev* __restrict__ nodes,
+                                             const int32_t* __restrict__ upd,
+                                             const double2* __restrict__ fronts,
+                                             const double2* __restrict__ fpst,
+                                             double2* __restrict__ xloc) {
+  extern __shared__ double2 z[];
+  const int2 tk = tasks[blockIdx.x];
+  const NodeDev nd = nodes[tk.x];
+  const int r0 = tk.y;
+  const int np = nd.np, m = nd.m;
+  const int64_t base = (int64_t)nd.mat_off + nd.pivb;
+  for (int q = threadIdx.x; q < m; q += blockDim.x)
+    z[q] = q < np ? fpst[base + q] : xloc[(int64_t)nd.mat_off + upd[nd.upd_off + q - np]];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int rr = wid; rr < kSolveRows; rr += blockDim.x >> 5) {
+    const int i = r0 + rr;
+    if (i >= np) break;
+    const double2* row = fronts + nd.front_off + (int64_t)i * m;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = lane; q < m; q += 32) acc = cfma(row[q], z[q], acc);
+    acc = warp_sum2(acc);
+    if (lane == 0) xloc[base + i] = cneg(acc);
+  }
+}
+
+// ------------------------------------------------------------- host plan
+template <typename F>
+static void par_for(int64_t n, F&& f) {
+  const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n <= 1 || nth == 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::atomic<int64_t> next{0};
+  std::exception_ptr err;
+  std::mutex mu;
+  for (unsigned t = 0; t < std::min<int64_t>(nth, n); ++t)
+    th.emplace_back([&] {
+      try {
+        for (int64_t i = next++; i < n; i = next++) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
+
+void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) {
+  ctx = c;
+  cudaStream_t s = ctx->stream;
+  nmat = (int32_t)mats.size();
+  std::vector<SymOut> sym(nmat);
+  par_for(nmat, [&](int64_t i) {
+    SymIn in;
+    in.n = mats[i].n;
+    in.rowptr = mats[i].rowptr.data();
+    in.cols = mats[i].cols.data();
+    in.xyz = mats[i].xyz.data();
+    nd_analyze(in, leaf, sym[i]);
+  });
+  mat_n.resize(nmat);
+  mat_off.resize(nmat);
+  perm.resize(nmat);
+  int64_t off = 0;
+  std::vector<int32_t> node_base(nmat);
+  int64_t nn = 0;
+  nlevels = 0;
+  for (int i = 0; i < nmat; ++i) {
+    mat_n[i] = mats[i].n;
+    if (off > INT32_MAX) fail(MDD_EINVAL, "local vector space exceeds 2^31");
+    mat_off[i] = (int32_t)off;
+    off += mats[i].n;
+    node_base[i] = (int32_t)nn;
+    nn += (int64_t)sym[i].nodes.size();
+    nlevels = std::max(nlevels, sym[i].nlevels);
+    perm[i] = sym[i].perm;
+  }
+  nloc = off;
+  nnodes = (int32_t)nn;
+  h_nodes.resize(nn);
+  std::vector<int32_t> h_children, h_gmap_sizes;
+  int64_t gm_total = 0, upd_total = 0;
+  front_total = 0;
+  uvec_total = 0;
+  factor_flops = 0;
+  factor_entries = 0;
+  max_np = 0;
+  max_m = 0;
+  std::vector<int32_t> node_level(nn);
+  for (int i = 0; i < nmat; ++i)
+    for (size_t k = 0; k < sym[i].nodes.size(); ++k) {
+      const SymNode& sn = sym[i].nodes[k];
+      const int64_t g = node_base[i] + (int64_t)k;
+      NodeDev& nd = h_nodes[g];
+      nd.np = sn.np;
+      nd.nu = (int32_t)sn.upd.size();
+      nd.m = nd.np + nd.nu;
+      nd.pivb = sn.piv_begin;
+      nd.mat_off = mat_off[i];
+      nd.mat = i;
+      nd.front_off = front_total;
+      front_total += (int64_t)nd.m * nd.m;
+      nd.uvec_off = uvec_total;
+      uvec_total += nd.nu;
+      nd.upd_off = upd_total;
+      upd_total += nd.nu;
+      nd.nch = (int32_t)sn.children.size();
+      nd.child_off = (int32_t)h_children.size();
+      for (int32_t ch : sn.children) h_children.push_back(node_base[i] + ch);
+      nd.gmap_off = gm_total;
+      gm_total += (int64_t)nd.nch * nd.m;
+      node_level[g] = sn.level;
+      max_np = std::max(max_np, nd.np);
+      max_m = std::max(max_m, nd.m);
+      factor_flops += 8.0 * nd.np * (double)nd.m * nd.m;
+      factor_entries += (double)nd.m * nd.m - (double)nd.nu * nd.nu;
+    }
+  std::vector<int32_t> h_upd(upd_total), h_gmap(gm_total, -1);
+  // upd lists + gather maps
+  par_for(nmat, [&](int64_t i) {
+    const SymOut& so = sym[i];
+    for (size_t k = 0; k < so.nodes.size(); ++k) {
+      const SymNode& sn = so.nodes[k];
+      const NodeDev& nd = h_nodes[node_base[i] + k];
+      std::copy(sn.upd.begin(), sn.upd.end(), h_upd.begin() + nd.upd_off);
+      const int32_t pend = sn.piv_begin + sn.np;
+      for (size_t ci = 0; ci < sn.children.size(); ++ci) {
+        const SymNode& ch = so.nodes[sn.children[ci]];
+        int32_t* g = h_gmap.data() + nd.gmap_off + (int64_t)ci * nd.m;
+        for (size_t a = 0; a < ch.upd.size(); ++a) {
+          const int32_t j = ch.upd[a];
+          int32_t pos;
+          if (j < pend) {
+            if (j < sn.piv_begin) throw std::runtime_error("multifrontal: child update outside parent");
+            pos = j - sn.piv_begin;
+          } else {
+            auto it = std::lower_bound(sn.upd.begin(), sn.upd.end(), j);
+            if (it == sn.upd.end() || *it != j)
+              throw std::runtime_error("multifrontal: child update not in parent front");
+            pos = sn.np + (int32_t)(it - sn.upd.begin());
+          }
+          g[pos] = (int32_t)a;
+        }
+      }
+    }
+  });
+  // original entries -> (level, pos, src)
+  std::vector<std::vector<int64_t>> epos(nlevels);
+  std::vector<std::vector<int32_t>> esrc(nlevels);
+  {
+    std::vector<std::vector<std::vector<int64_t>>> tpos(nmat);
+    std::vector<std::vector<std::vector<int32_t>>> tsrc(nmat);
+    par_for(nmat, [&](int64_t i) {
+      const SymOut& so = sym[i];
+      const MatrixInput& mi = mats[i];
+      tpos[i].assign(nlevels, {});
+      tsrc[i].assign(nlevels, {});
+      std::vector<int32_t> owner(mi.n);
+      for (size_t k = 0; k < so.nodes.size(); ++k)
+        for (int32_t q = 0; q < so.nodes[k].np; ++q) owner[so.nodes[k].piv_begin + q] = (int32_t)k;
+      auto front_pos = [&](const SymNode& sn, int32_t j) -> int32_t {
+        if (j < sn.piv_begin + sn.np) return j - sn.piv_begin;
+        auto it = std::lower_bound(sn.upd.begin(), sn.upd.end(), j);
+        if (it == sn.upd.end() || *it != j) throw std::runtime_error("multifrontal: entry outside front");
+        return sn.np + (int32_t)(it - sn.upd.begin());
+      };
+      for (int32_t r = 0; r < mi.n; ++r)
+        for (int32_t e = mi.rowptr[r]; e < mi.rowptr[r + 1]; ++e) {
+          const int32_t a = so.iperm[r], b = so.iperm[mi.cols[e]];
+          const int32_t k = owner[std::min(a, b)];
+          const SymNode& sn = so.nodes[k];
+          const NodeDev& nd = h_nodes[node_base[i] + k];
+          const int64_t p = nd.front_off + (int64_t)front_pos(sn, a) * nd.m + front_pos(sn, b);
+          tpos[i][sn.level].push_back(p);
+          tsrc[i][sn.level].push_back(mi.src[e]);
+        }
+    });
+    for (int L = 0; L < nlevels; ++L)
+      for (int i = 0; i < nmat; ++i) {
+        epos[L].insert(epos[L].end(), tpos[i][L].begin(), tpos[i][L].end());
+        esrc[L].insert(esrc[L].end(), tsrc[i][L].begin(), tsrc[i][L].end());
+      }
+  }
+  // level lists
+  std::vector<std::vector<int32_t>> lev(nlevels);
+  for (int64_t g = 0; g < nn; ++g) lev[node_level[g]].push_back((int32_t)g);
+  std::vector<int64_t> h_epos;
+  std::vector<int32_t> h_esrc;
+  std::vector<int2> h_init, h_panel, h_fwd, h_bwd;
+  std::vector<int4> h_tile;
+  std::vector<int32_t> h_act;
+  std::vector<int64_t> h_woff;
+  lev_ent_off.assign(1, 0);
+  lev_init_off.assign(1, 0);
+  lev_fwd_off.assign(1, 0);
+  lev_bwd_off.assign(1, 0);
+  lev_steps.assign(nlevels, 0);
+  lev_step_base.assign(nlevels, 0);
+  step_act_off.assign(1, 0);
+  step_panel_off.assign(1, 0);
+  step_tile_off.assign(1, 0);
+  w_max = 0;
+  max_act = 0;
+  int64_t nsteps_total = 0;
+  for (int L = 0; L < nlevels; ++L) {
+    h_epos.insert(h_epos.end(), epos[L].begin(), epos[L].end());
+    h_esrc.insert(h_esrc.end(), esrc[L].begin(), esrc[L].end());
+    lev_ent_off.push_back((int64_t)h_epos.size());
+    int32_t lnp = 0;
+    for (int32_t g : lev[L]) {
+      const NodeDev& nd = h_nodes[g];
+      for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
+      lnp = std::max(lnp, nd.np);
+      if (nd.nu == 0) h_fwd.push_back(make_int2(g, 0));
+      for (int r = 0; r < nd.nu; r += kSolveRows) h_fwd.push_back(make_int2(g, r));
+      for (int r = 0; r < nd.np; r += kSolveRows) h_bwd.push_back(make_int2(g, r));
+    }
+    lev_init_off.push_back((int64_t)h_init.size());
+    lev_fwd_off.push_back((int64_t)h_fwd.size());
+    lev_bwd_off.push_back((int64_t)h_bwd.size());
+    const int nst = (lnp + kPB - 1) / kPB;
+    lev_steps[L] = nst;
+    lev_step_base[L] = nsteps_total;
+    for (int st = 0; st < nst; ++st) {
+      int64_t wo = 0;
+      int32_t nact = 0;
+      for (int32_t g : lev[L]) {
+        const NodeDev& nd = h_nodes[g];
+        if (nd.np <= st * kPB) continue;
+        const int32_t ai = nact++;
+        h_act.push_back(g);
+        h_woff.push_back(wo);
+        wo += (int64_t)nd.m * kPB;
+        for (int ch = 0; ch * kPanelCols < nd.m; ++ch) h_panel.push_back(make_int2(ai, ch));
+        const int K0 = st * kPB, kb = std::min(kPB, nd.np - K0);
+        const int nt = (nd.m + kTile - 1) / kTile;
+        for (int tr = 0; tr < nt; ++tr) {
+          const int rb = tr * kTile, re = std::min(nd.m, rb + kTile);
+          if (rb >= K0 && re <= K0 + kb) continue;  // tile rows all pivots
+          for (int tc = 0; tc < nt; ++tc) h_tile.push_back(make_int4(ai, tr, tc, 0));
+        }
+      }
+      w_max = std::max(w_max, wo);
+      max_act = std::max(max_act, nact);
+      step_act_off.push_back((int64_t)h_act.size());
+      step_panel_off.push_back((int64_t)h_panel.size());
+      step_tile_off.push_back((int64_t)h_tile.size());
+      ++nsteps_total;
+    }
+  }
+  nodes.upload(h_nodes, s);
+  children.upload(h_children, s);
+  gmap.upload(h_gmap, s);
+  upd.upload(h_upd, s);
+  ent_pos.upload(h_epos, s);
+  ent_src.upload(h_esrc, s);
+  init_tasks.upload(h_init, s);
+  panel_tasks.upload(h_panel, s);
+  tile_tasks.upload(h_tile, s);
+  act_node.upload(h_act, s);
+  act_woff.upload(h_woff, s);
+  fwd_tasks.upload(h_fwd, s);
+  bwd_tasks.upload(h_bwd, s);
+  fronts.alloc(front_total);
+  uvec.alloc(std::max<int64_t>(1, uvec_total));
+  pbuf.alloc(std::max<int64_t>(1, (int64_t)max_act * kPB * kPB));
+  wbuf.alloc(std::max<int64_t>(1, w_max));
+  pivstat.alloc(std::max<int64_t>(2, 2 * (int64_t)nn));
+  bloc.alloc(std::max<int64_t>(1, nloc));
+  fpst.alloc(std::max<int64_t>(1, nloc));
+  xloc.alloc(std::max<int64_t>(1, nloc));
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
+    CK(cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  if ((int64_t)max_m * 16 > 200 * 1024) fail(MDD_EINVAL, "front larger than the solve kernels support");
+  CK(cudaStreamSynchronize(s));
+}
+
+static unsigned gblocks(int64_t n, int bs, int cap) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, cap));
+}
+
+void FrontPlan::factor(const double2* vals, cudaStream_t s) {
+  if (nnodes == 0) return;
+  k_pivinit<<<gblocks(nnodes, 256, 1024), 256, 0, s>>>(pivstat.p, nnodes);
+  CK_LAUNCH(ctx);
+  const size_t upd_smem = sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1));
+  for (int L = 0; L < nlevels; ++L) {
+    const int64_t ni = lev_init_off[L + 1] - lev_init_off[L];
+    if (ni) {
+      k_front_init<<<(unsigned)((ni + 7) / 8), 256, 0, s>>>(init_tasks.p + lev_init_off[L], ni,
+                                                           nodes.p, children.p, gmap.p, fronts.p);
+      CK_LAUNCH(ctx);
+    }
+    const int64_t ne = lev_ent_off[L + 1] - lev_ent_off[L];
+    if (ne) {
+      k_front_scatter<<<gblocks(ne, 256, ctx->nsm * 32), 256, 0, s>>>(
+          ne, ent_pos.p + lev_ent_off[L], ent_src.p + lev_ent_off[L], vals, fronts.p);
+      CK_LAUNCH(ctx);
+    }
+    for (int st = 0; st < lev_steps[L]; ++st) {
+      const int64_t si = lev_step_base[L] + st;
+      const int64_t a0 = step_act_off[si], na = step_act_off[si + 1] - a0;
+      const int64_t p0 = step_panel_off[si], npn = step_panel_off[si + 1] - p0;
+      const int64_t t0 = step_tile_off[si], ntl = step_tile_off[si + 1] - t0;
+      if (!na) continue;
+      k_invert<<<(unsigned)na, 1024, 0, s>>>(nodes.p, act_node.p + a0, st, fronts.p, pbuf.p,
+                                             pivstat.p);
+      CK_LAUNCH(ctx);
+      k_panel<<<(unsigned)npn, kPanelCols, 0, s>>>(panel_tasks.p + p0, nodes.p, act_node.p + a0,
+                                                   act_woff.p + a0, st, fronts.p, pbuf.p, wbuf.p);
+      CK_LAUNCH(ctx);
+      if (ntl) {
+        k_update<<<(unsigned)ntl, 256, upd_smem, s>>>(tile_tasks.p + t0, nodes.p, act_node.p + a0,
+                                                      act_woff.p + a0, st, fronts.p, wbuf.p);
+        CK_LAUNCH(ctx);
+      }
+    }
+  }
+}
+
+int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {
+  std::vector<double> ps(2 * (size_t)nnodes);
+  if (nnodes) pivstat.download(ps.data(), ps.size(), s);
+  CK(cudaStreamSynchronize(s));
+  std::vector<double> mn(nmat, INFINITY), mx(nmat, 0.0);
+  for (int64_t g = 0; g < nnodes; ++g) {
+    if (h_nodes[g].np == 0) continue;
+    const int i = h_nodes[g].mat;
+    mn[i] = std::min(mn[i], ps[2 * g]);
+    mx[i] = std::max(mx[i], ps[2 * g + 1]);
+  }
+  for (int i = 0; i < nmat; ++i) {
+    if (mat_n[i] == 0) continue;
+    const bool bad = !(mx[i] > 0.0) || !std::isfinite(mx[i]) || !(mn[i] > 1e-14 * mx[i]);
+    if (bad) {
+      char buf[256];
+      snprintf(buf, sizeof(buf),
+               "pivot ratio %.2e below tolerance, matrix is numerically singular",
+               mn[i] / std::max(mx[i], 1e-300));
+      msg = buf;
+      return i;
+    }
+  }
+  return -1;
+}
+
+void FrontPlan::solve(cudaStream_t s) {
+  const size_t fsm = sizeof(double2) * std::max(1, max_np);
+  const size_t bsm = sizeof(double2) * std::max(1, max_m);
+  for (int L = 0; L < nlevels; ++L) {
+    const int64_t n = lev_fwd_off[L + 1] - lev_fwd_off[L];
+    if (!n) continue;
+    k_fwd<<<(unsigned)n, 256, fsm, s>>>(fwd_tasks.p + lev_fwd_off[L], nodes.p, children.p, gmap.p,
+                                        fronts.p, bloc.p, fpst.p, uvec.p);
+    CK_LAUNCH(ctx);
+  }
+  for (int L = nlevels - 1; L >= 0; --L) {
+    const int64_t n = lev_bwd_off[L + 1] - lev_bwd_off[L];
+    if (!n) continue;
+    k_bwd<<<(unsigned)n, 256, bsm, s>>>(bwd_tasks.p + lev_bwd_off[L], nodes.p, upd.p, fronts.p,
+                                        fpst.p, xloc.p);
+    CK_LAUNCH(ctx);
+  }
+}
+
+}  // namespace mdd

@@ -1,0 +1,99 @@
+// Batched multifrontal factorisation plan + numeric kernels (device).
+//
+// A "plan" holds several independent sparse matrices (the overlapping
+// subdomain blocks, or the coarse block) after nested-dissection analysis.
+// Each tree node owns a dense row-major front  F = [F_PP F_PU; F_UP F_UU]
+// (P = its pivots, U = its update rows).  The numeric phase assembles fronts
+// level by level (children's Schur complements extend-added in gather form,
+// original entries scattered), then applies block Gauss-Jordan sweeps over
+// the pivot blocks, leaving
+//     F_PP <- -F_PP^{-1},  F_PU <- F_PP^{-1} F_PU,  F_UP <- F_UP F_PP^{-1},
+//     F_UU <- F_UU - F_UP F_PP^{-1} F_PU           (Schur complement).
+// A solve is then a sequence of batched GEMVs per level:
+//     forward   r_U -= F_UP r_P                  (leaves -> root)
+//     backward  x_P  = -(F_PP r_P + F_PU x_U)     (root -> leaves)
+// No pivoting: the absorptive operators have Im(Theta v*Av) > 0 on every
+// principal submatrix; pivot magnitudes are still tracked and
+// the reference's ratio test (linalg.py:95-101) is applied per matrix.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "mdd_internal.h"
+#include "symbolic.h"
+
+namespace mdd {
+
+constexpr int kPB = 32;      // pivot block of the sweep
+constexpr int kTile = 64;    // update tile
+constexpr int kPanelCols = 128;
+constexpr int kSolveRows = 32;
+
+struct NodeDev {
+  int64_t front_off;  // complex elements into the front storage
+  int64_t upd_off;    // into upd (int32 ND indices)
+  int64_t uvec_off;   // into the forward update-vector buffer
+  int64_t gmap_off;   // into gmap: nch * m entries
+  int32_t m, np, nu, pivb;
+  int32_t mat_off;    // offset of the node's matrix in the local vector space
+  int32_t nch, child_off, mat;
+};
+
+struct MatrixInput {
+  int32_t n = 0;
+  std::vector<int32_t> rowptr, cols;  // local pattern (sorted)
+  std::vector<int32_t> src;           // per local entry: index into the value array
+  std::vector<int32_t> xyz;           // (n,3)
+};
+
+struct FrontPlan {
+  mdd_ctx* ctx = nullptr;
+  int32_t nmat = 0;
+  std::vector<int32_t> mat_n, mat_off;
+  std::vector<std::vector<int32_t>> perm;  // per matrix: ND index -> local index
+  int64_t nloc = 0;
+  int32_t nnodes = 0, nlevels = 0;
+  std::vector<NodeDev> h_nodes;
+  DevBuf<NodeDev> nodes;
+  DevBuf<int32_t> children, gmap, upd;
+  // original entries, grouped by level
+  DevBuf<int64_t> ent_pos;
+  DevBuf<int32_t> ent_src;
+  std::vector<int64_t> lev_ent_off;
+  // task lists
+  DevBuf<int2> init_tasks;
+  std::vector<int64_t> lev_init_off;
+  std::vector<int32_t> lev_steps;        // sweep steps per level
+  std::vector<int64_t> lev_step_base;    // index of (level, step 0) in step arrays
+  std::vector<int64_t> step_act_off;     // per (level,step): offset into act arrays
+  std::vector<int64_t> step_panel_off;
+  std::vector<int64_t> step_tile_off;
+  DevBuf<int32_t> act_node;
+  DevBuf<int64_t> act_woff;
+  DevBuf<int2> panel_tasks;
+  DevBuf<int4> tile_tasks;
+  DevBuf<int2> fwd_tasks, bwd_tasks;
+  std::vector<int64_t> lev_fwd_off, lev_bwd_off;
+  int32_t max_np = 0, max_m = 0, max_act = 0;
+  int64_t front_total = 0, uvec_total = 0, w_max = 0;
+  double factor_flops = 0, factor_entries = 0;
+  // numeric storage
+  DevBuf<double2> fronts, uvec, pbuf, wbuf;
+  DevBuf<double> pivstat;  // per node: [min |pivot|, max |pivot|]
+  // solve workspace (local vectors)
+  DevBuf<double2> bloc, fpst, xloc;
+  float factor_ms = 0;
+
+  // build from analysed matrices
+  void build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf);
+  // numeric factorisation from `vals` (complex, indexed by MatrixInput.src)
+  void factor(const double2* vals, cudaStream_t s);
+  // per-matrix pivot ratio check; returns index of the first failing matrix or -1
+  int check_pivots(std::string& msg, cudaStream_t s);
+  // solve in place: bloc (ND-ordered local rhs) -> xloc
+  void solve(cudaStream_t s);
+};
+
+}  // namespace mdd

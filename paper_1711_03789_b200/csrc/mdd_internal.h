@@ -1,0 +1,192 @@
+// Internal definitions shared by the libmdd translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mdd.h"
+
+namespace mdd {
+
+// ---------------------------------------------------------------- errors
+struct Error : public std::exception {
+  int code;
+  std::string msg;
+  int failed_ctx = -2;
+  Error(int c, std::string m, int fctx = -2) : code(c), msg(std::move(m)), failed_ctx(fctx) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+void set_last_error(const std::string& m);
+
+[[noreturn]] inline void fail(int code, const std::string& m, int fctx = -2) {
+  throw Error(code, m, fctx);
+}
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), file, line, what);
+    throw Error(e == cudaErrorMemoryAllocation ? MDD_ENOMEM : MDD_ECUDA, buf);
+  }
+}
+#define CK(call) ::mdd::cuda_check((call), #call, __FILE__, __LINE__)
+#define CK_LAUNCH(ctx)                                             \
+  do {                                                             \
+    ::mdd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+    (ctx)->launches++;                                             \
+  } while (0)
+
+// C-ABI wrapper: converts exceptions into codes + thread-local messages.
+#define MDD_API_BEGIN try {
+#define MDD_API_END                                \
+  }                                                \
+  catch (const ::mdd::Error& e) {                  \
+    ::mdd::set_last_error(e.msg);                  \
+    return e.code;                                 \
+  }                                                \
+  catch (const std::bad_alloc&) {                  \
+    ::mdd::set_last_error("host allocation failed"); \
+    return MDD_ENOMEM;                             \
+  }                                                \
+  catch (const std::exception& e) {                \
+    ::mdd::set_last_error(e.what());               \
+    return MDD_EINVAL;                             \
+  }                                                \
+  return MDD_OK;
+
+// ----------------------------------------------------------- device buffer
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    if (count > n) alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  void download(T* h, size_t count, cudaStream_t s) const {
+    if (count) CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+template <typename T>
+inline DevBuf<T> to_device(const std::vector<T>& h, cudaStream_t s) {
+  DevBuf<T> d(h.size());
+  d.upload(h, s);
+  return d;
+}
+
+}  // namespace mdd
+
+// --------------------------------------------------------- opaque objects
+struct mdd_ctx {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  bool timing = false;
+  double timers[6] = {0, 0, 0, 0, 0, 0};
+  // pinned staging used by host-pointer entry points
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* pinned_buf(size_t bytes);
+};
+
+struct mdd_pattern {
+  int64_t nrow = 0, ncol = 0, nnz = 0;
+  mdd::DevBuf<int32_t> rowptr, cols;
+  std::vector<int32_t> h_rowptr, h_cols;  // host copy (symbolic work)
+};
+
+struct mdd_csr {
+  mdd_ctx* ctx = nullptr;
+  std::shared_ptr<mdd_pattern> pat;
+  bool is_complex = true;
+  mdd::DevBuf<double> vals;  // nnz (real) or 2*nnz (complex, interleaved)
+  int64_t nrow() const { return pat->nrow; }
+  int64_t ncol() const { return pat->ncol; }
+  int64_t nnz() const { return pat->nnz; }
+};
+
+// Device-resident mesh + edge space + CSR pattern of the kept DOFs.
+struct mdd_space {
+  mdd_ctx* ctx = nullptr;
+  int32_t n = 0;  // cells per axis
+  int64_t nv = 0, nt = 0, ne = 0, ndof = 0;
+  // host copies (int32 unless noted)
+  std::vector<double> h_verts;      // nv*3
+  std::vector<int32_t> h_tets;      // nt*4
+  std::vector<int32_t> h_tet_edges; // nt*6
+  std::vector<int8_t> h_signs;      // nt*6
+  std::vector<int32_t> h_e2d;       // ne
+  // device copies
+  mdd::DevBuf<double> verts;
+  mdd::DevBuf<int32_t> tets, tet_edges, e2d;
+  mdd::DevBuf<int8_t> signs;
+  // kept-dof CSR pattern (shared by A, S, M, Dk)
+  std::shared_ptr<mdd_pattern> pat;
+  // cells grouped by parity colour (cx%2, cy%2, cz%2): no two cells of one
+  // colour share an edge, so one thread per cell scatters without atomics
+  mdd::DevBuf<int32_t> cells_by_color;
+  int64_t color_off[9] = {0};
+  // dof -> incident (tet*6 + local edge), ascending tet (rhs gather)
+  mdd::DevBuf<int32_t> inc_ptr, inc;
+};
+
+namespace mdd {
+// element geometry + 6x6 stiffness / mass (fem.py:154-195); shared by the
+// global assembly, the impras local assembly and the coarse Galerkin kernel
+struct ElemMats {
+  double s[6][6];
+  double m[6][6];
+  double vol;
+};
+
+// kernels shared across units ------------------------------------------
+// y = A x (x, y device complex)
+void spmv_dev(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y, cudaStream_t s);
+// y = beta*y + alpha*A x on device; variants used by the preconditioner
+void spmv_dev_axpby(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y,
+                    double2 alpha, double2 beta, const double2* z, cudaStream_t s);
+// out = a - b
+void vec_sub(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int64_t n,
+             cudaStream_t s);
+void vec_add(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int64_t n,
+             cudaStream_t s);
+// complex CSR with the given pattern, values zeroed
+mdd_csr* new_csr(mdd_ctx* ctx, std::shared_ptr<mdd_pattern> pat, bool cplx);
+std::shared_ptr<mdd_pattern> make_pattern(int64_t nrow, int64_t ncol,
+                                          std::vector<int32_t>&& rowptr,
+                                          std::vector<int32_t>&& cols, cudaStream_t s);
+}  // namespace mdd

@@ -1,0 +1,997 @@
+// Two-level overlapping Schwarz preconditioners on the device
+// (reference precond.PreconditionerState, precond.py:277-377).
+//
+//  setup : subdomain blocks R_l A_prec R_l^T (exact minors, linalg.py:48-70)
+//          are analysed by geometric nested dissection and factorised as one
+//          batched multifrontal plan; the coarse block R0 A_prec R0^T is
+//          formed element by element (each fine tet T lies in one coarse tet
+//          C(T), so R0 A R0^T = sum_T Q_T A_T Q_T^T with Q_T the 6x6 values of
+//          C(T)'s Whitney functions on T's edges) and factorised the same way.
+//  apply : gather v[I_l] -> batched forward/backward solves -> owner-computes
+//          scatter out[i] = sum_{l owning i} w_l(i) u_l(i) (subdomain order,
+//          as precond.py:350-355), fused with the coarse prolongation for
+//          the additive variant; hybrid / ADEF1 compose the same primitives
+//          (precond.py:360-375).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <atomic>
+#include <thread>
+#include <unordered_map>
+
+#include "fem_device.cuh"
+#include "frontal.h"
+#include "mdd_kernels.cuh"
+
+namespace mdd {
+
+void assemble_system(mdd_space* sp, const mdd_coeffs* co, int impedance, int64_t nbf,
+                     const int64_t* bfaces, mdd_csr** A, mdd_csr** S, mdd_csr** M, mdd_csr** Dk,
+                     mdd_csr** Mb);
+
+struct PrecCore {
+  mdd_ctx* ctx = nullptr;
+  int64_t ndof = 0;
+  int local_kind = 0;  // 0: conducting minors (as/ras), 1: impedance (impras)
+  int32_t nsub = 0;
+  FrontPlan sub;
+  DevBuf<int32_t> gidx;               // nloc
+  DevBuf<int32_t> own_ptr, own_idx;   // ndof+1, nloc
+  DevBuf<double> own_w;               // nloc (PoU weight of each ownership)
+  bool have_coarse = false;
+  int64_t ncs = 0;
+  FrontPlan coarse;
+  std::unique_ptr<mdd_csr> R0p, R0Tp;  // rows / columns in coarse ND order
+  std::unique_ptr<mdd_csr> A0;         // assembled coarse Galerkin matrix (coarse pattern)
+  // Galerkin data
+  const mdd_space* fine_space = nullptr;
+  const mdd_space* coarse_space = nullptr;
+  DevBuf<int32_t> tet_map, cfine_ptr, cfine_idx, face_tet, cface_ptr, cface_idx, gfaces;
+  int64_t n_gfaces = 0;
+  // impras local assembly data
+  DevBuf<double2> loc_vals;
+  DevBuf<int32_t> loc_tet, loc_tet_sub;          // (subdomain tet, subdomain) pairs by colour
+  std::vector<int64_t> loc_color_off;
+  DevBuf<int32_t> loc_rowptr, loc_cols;          // concatenated local patterns (local ids)
+  DevBuf<int32_t> loc_sub_off;                   // entry offset per subdomain
+  DevBuf<int32_t> loc_e2l;                       // per (pair, 6): local index or -1
+  DevBuf<int32_t> loc_face, loc_face_sub, loc_face_l;  // boundary faces
+  int64_t n_loc_faces = 0;
+  DevBuf<int32_t> loc_row_off;                   // per subdomain: offset into loc_rowptr
+  std::vector<double> stats = std::vector<double>(8, 0.0);
+  DevBuf<double2> t1, t2, t3, t4;
+};
+
+}  // namespace mdd
+
+struct mdd_prec {
+  std::shared_ptr<mdd::PrecCore> core;
+  int family = 0, levels = 1, correction = 0;
+  const mdd_csr* A_corr = nullptr;
+};
+
+namespace mdd {
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_gather(int64_t n, const int32_t* __restrict__ gidx, const double2* __restrict__ v,
+                         double2* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = v[gidx[t]];
+}
+
+// out[i] = (sum_k w_k x[own_idx[k]]) (+ add[i])
+__global__ void k_scatter_owner(int64_t ndof, const int32_t* __restrict__ ptr,
+                                const int32_t* __restrict__ idx, const double* __restrict__ w,
+                                const double2* __restrict__ x, const double2* __restrict__ add,
+                                double2* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+      const double2 u = x[idx[k]];
+      if (w) {
+        const double ww = w[k];
+        acc.x += ww * u.x;
+        acc.y += ww * u.y;
+      } else {
+        acc.x += u.x;
+        acc.y += u.y;
+      }
+    }
+    if (add) acc = cadd(acc, add[i]);
+    out[i] = acc;
+  }
+}
+
+// out = (a - b) + c
+__global__ void k_sub_add(int64_t n, const double2* a, const double2* b, const double2* c,
+                          double2* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = cadd(csub(a[i], b[i]), c[i]);
+}
+
+// barycentric coordinates of x in a tet with vertex 0 at p0 and gradients g
+__device__ __forceinline__ void bary(const TetGeom& g, const double* p0, const double* x,
+                                     double (&l)[4]) {
+  double d[3] = {x[0] - p0[0], x[1] - p0[1], x[2] - p0[2]};
+  for (int i = 1; i < 4; ++i) l[i] = g.g[i][0] * d[0] + g.g[i][1] * d[1] + g.g[i][2] * d[2];
+  l[0] = 1.0 - l[1] - l[2] - l[3];
+}
+
+struct GalArgs {
+  // fine
+  const double* fverts;
+  const int32_t* ftets;
+  const int32_t* ftet_edges;
+  const int8_t* fsigns;
+  const int32_t* fe2d;
+  // coarse
+  const double* cverts;
+  const int32_t* ctets;
+  const int8_t* csigns;
+  const int32_t* tet_map;
+};
+
+// Q[c][e]: coarse local edge c of C (oriented by its sign) on fine edge
+// (lo -> hi):  sc * (l_a(x0) l_b(x1) - l_a(x1) l_b(x0))   (exact line integral
+// of the Whitney function, = decomp.coarse_restriction's 2-point Gauss value)
+__device__ void coarse_Q_edges(const GalArgs& ga, int ct, const int64_t* lo, const int64_t* hi,
+                               int ne, double (&Q)[6][6]) {
+  double cc[4][3];
+  for (int i = 0; i < 4; ++i) {
+    const int v = ga.ctets[(int64_t)ct * 4 + i];
+    for (int k = 0; k < 3; ++k) cc[i][k] = ga.cverts[(int64_t)v * 3 + k];
+  }
+  TetGeom g;
+  tet_geometry(cc, g);
+  for (int e = 0; e < ne; ++e) {
+    double l0[4], l1[4];
+    bary(g, cc[0], ga.fverts + lo[e] * 3, l0);
+    bary(g, cc[0], ga.fverts + hi[e] * 3, l1);
+    for (int c = 0; c < 6; ++c) {
+      const int a = kEA[c], b = kEB[c];
+      const double sc = (double)ga.csigns[(int64_t)ct * 6 + c];
+      Q[c][e] = sc * (l0[a] * l1[b] - l1[a] * l0[b]);
+    }
+  }
+}
+
+// per fine tet: BS = Q S Q^T, BM = Q M Q^T (6x6 real each)
+__global__ void __launch_bounds__(128) k_galerkin_tets(int64_t nt, GalArgs ga, double* __restrict__ BS,
+                                                       double* __restrict__ BM) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  double c[4][3], sg[6];
+  int32_t vid[4];
+  for (int i = 0; i < 4; ++i) {
+    vid[i] = ga.ftets[t * 4 + i];
+    for (int k = 0; k < 3; ++k) c[i][k] = ga.fverts[(int64_t)vid[i] * 3 + k];
+  }
+  for (int e = 0; e < 6; ++e) sg[e] = (double)ga.fsigns[t * 6 + e];
+  ElemMats em;
+  element_matrices(c, sg, em);
+  int64_t lo[6], hi[6];
+  for (int e = 0; e < 6; ++e) {
+    const int64_t a = vid[kEA[e]], b = vid[kEB[e]];
+    lo[e] = a < b ? a : b;
+    hi[e] = a < b ? b : a;
+  }
+  double Q[6][6];
+  coarse_Q_edges(ga, ga.tet_map[t], lo, hi, 6, Q);
+  for (int e = 0; e < 6; ++e)
+    if (ga.fe2d[ga.ftet_edges[t * 6 + e]] < 0)
+      for (int cc = 0; cc < 6; ++cc) Q[cc][e] = 0.0;
+  // QS = Q S, then BS = QS Q^T  (same for M)
+  for (int pass = 0; pass < 2; ++pass) {
+    const double(*E)[6] = pass == 0 ? em.s : em.m;
+    double* out = (pass == 0 ? BS : BM) + t * 36;
+    double QE[6][6];
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) {
+        double s = 0.0;
+        for (int k = 0; k < 6; ++k) s += Q[a][k] * E[k][b];
+        QE[a][b] = s;
+      }
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) {
+        double s = 0.0;
+        for (int k = 0; k < 6; ++k) s += QE[a][k] * Q[b][k];
+        out[a * 6 + b] = s;
+      }
+  }
+}
+
+// per global impedance face: BF = Q_f m_f Q_f^T (6x6 real)
+__global__ void k_galerkin_faces(int64_t nf, GalArgs ga, const int32_t* __restrict__ faces,
+                                 const int32_t* __restrict__ face_tet, double* __restrict__ BF) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  double p[3][3];
+  int64_t v[3];
+  for (int i = 0; i < 3; ++i) {
+    v[i] = faces[f * 3 + i];
+    for (int k = 0; k < 3; ++k) p[i][k] = ga.fverts[v[i] * 3 + k];
+  }
+  double mf[3][3];
+  triangle_tangential_mass(p, mf);
+  const int64_t lo[3] = {v[0], v[0], v[1]}, hi[3] = {v[1], v[2], v[2]};
+  double Q[6][6];
+  coarse_Q_edges(ga, ga.tet_map[face_tet[f]], lo, hi, 3, Q);
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) {
+      double s = 0.0;
+      for (int x = 0; x < 3; ++x)
+        for (int y = 0; y < 3; ++y) s += Q[a][x] * mf[x][y] * Q[b][y];
+      BF[f * 36 + a * 6 + b] = s;
+    }
+}
+
+struct CoefArr {
+  const double* eps;
+  const double* mu;
+  const double* sigma;
+  double eps0, mu0, sigma0, k, xi;
+  int homogeneous;
+  double2 face_coef;  // -i*s*k
+};
+
+// per (coarse tet, entry): sum over its fine tets (ascending) and faces
+__global__ void k_galerkin_reduce(int64_t nct, const int32_t* __restrict__ fptr,
+                                  const int32_t* __restrict__ fidx, const double* __restrict__ BS,
+                                  const double* __restrict__ BM, const int32_t* __restrict__ gptr,
+                                  const int32_t* __restrict__ gidx, const double* __restrict__ BF,
+                                  CoefArr co, double2* __restrict__ blk) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nct * 36) return;
+  const int64_t ct = gid / 36;
+  const int e = (int)(gid % 36);
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = fptr[ct]; k < fptr[ct + 1]; ++k) {
+    const int64_t t = fidx[k];
+    const double s = BS[t * 36 + e], m = BM[t * 36 + e];
+    if (co.homogeneous) {
+      acc.x += s - co.k * co.k * m;
+      acc.y += -co.xi * m;
+    } else {
+      const double eps = co.eps ? co.eps[t] : co.eps0;
+      const double mu = co.mu ? co.mu[t] : co.mu0;
+      const double sig = co.sigma ? co.sigma[t] : co.sigma0;
+      const double wr = co.k * co.k * eps, wi = co.xi * eps + co.k * sig;
+      acc.x += s / mu - wr * m;
+      acc.y += -wi * m;
+    }
+  }
+  if (gptr)
+    for (int k = gptr[ct]; k < gptr[ct + 1]; ++k) {
+      const double b = BF[(int64_t)gidx[k] * 36 + e];
+      acc.x += co.face_coef.x * b;
+      acc.y += co.face_coef.y * b;
+    }
+  blk[gid] = acc;
+}
+
+// coloured scatter of complex 6x6 element blocks into a complex CSR
+__global__ void __launch_bounds__(128) k_scatter_blocks(const int32_t* __restrict__ cells, int64_t ncells,
+                                                        const int32_t* __restrict__ tet_edges,
+                                                        const int32_t* __restrict__ e2d,
+                                                        const int32_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ cols,
+                                                        const double2* __restrict__ blk,
+                                                        double2* __restrict__ A) {
+  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= ncells) return;
+  const int64_t cell = cells[ci];
+  for (int p = 0; p < 6; ++p) {
+    const int64_t t = cell * 6 + p;
+    int dof[6];
+    for (int e = 0; e < 6; ++e) dof[e] = e2d[tet_edges[t * 6 + e]];
+    for (int a = 0; a < 6; ++a) {
+      if (dof[a] < 0) continue;
+      for (int b = 0; b < 6; ++b) {
+        if (dof[b] < 0) continue;
+        const int slot = csr_find(rowptr, cols, dof[a], dof[b]);
+        A[slot] = cadd(A[slot], blk[t * 36 + a * 6 + b]);
+      }
+    }
+  }
+}
+
+// impras local assembly: one thread per (subdomain, cell) pair of one colour;
+// adds the subdomain tets of that cell into the subdomain's local CSR.
+__global__ void __launch_bounds__(128) k_local_cells(
+    int64_t npairs, const int32_t* __restrict__ pair_cell, const int32_t* __restrict__ pair_sub,
+    const int32_t* __restrict__ pair_mask, const double* __restrict__ verts,
+    const int32_t* __restrict__ tets, const int8_t* __restrict__ signs,
+    const int32_t* __restrict__ e2l, const int32_t* __restrict__ row_off,
+    const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+    const int32_t* __restrict__ ent_off, CoefArr co, double2* __restrict__ vals) {
+  const int64_t pi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pi >= npairs) return;
+  const int64_t cell = pair_cell[pi];
+  const int sub = pair_sub[pi];
+  const int mask = pair_mask[pi];
+  const int32_t* rp = rowptr + row_off[sub];
+  const int32_t* cl = cols + ent_off[sub];
+  double2* vv = vals + ent_off[sub];
+  for (int p = 0; p < 6; ++p) {
+    if (!((mask >> p) & 1)) continue;
+    const int64_t t = cell * 6 + p;
+    double c[4][3], sg[6];
+    for (int i = 0; i < 4; ++i) {
+      const int v = tets[t * 4 + i];
+      for (int k = 0; k < 3; ++k) c[i][k] = verts[(int64_t)v * 3 + k];
+    }
+    for (int e = 0; e < 6; ++e) sg[e] = (double)signs[t * 6 + e];
+    ElemMats em;
+    element_matrices(c, sg, em);
+    const double eps = co.eps ? co.eps[t] : co.eps0;
+    const double mu = co.mu ? co.mu[t] : co.mu0;
+    const double sig = co.sigma ? co.sigma[t] : co.sigma0;
+    const double wr = co.k * co.k * eps, wi = co.xi * eps + co.k * sig;
+    int l[6];
+    for (int e = 0; e < 6; ++e) l[e] = e2l[(pi * 6 + p) * 6 + e];
+    for (int a = 0; a < 6; ++a) {
+      if (l[a] < 0) continue;
+      for (int b = 0; b < 6; ++b) {
+        if (l[b] < 0) continue;
+        const int slot = csr_find(rp, cl, l[a], l[b]);
+        double2 v = vv[slot];
+        v.x += em.s[a][b] / mu - wr * em.m[a][b];
+        v.y += -wi * em.m[a][b];
+        vv[slot] = v;
+      }
+    }
+  }
+}
+
+// impras boundary faces: local boundary mass, -i*s*k times, added per face
+// (faces of one subdomain processed sequentially by one thread: no races)
+__global__ void k_local_faces(int32_t nsub, const int32_t* __restrict__ sub_face_ptr,
+                              const int32_t* __restrict__ faces, const int32_t* __restrict__ face_l,
+                              const double* __restrict__ verts, const int32_t* __restrict__ row_off,
+                              const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                              const int32_t* __restrict__ ent_off, double2 coef,
+                              double2* __restrict__ vals) {
+  const int sub = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sub >= nsub) return;
+  const int32_t* rp = rowptr + row_off[sub];
+  const int32_t* cl = cols + ent_off[sub];
+  double2* vv = vals + ent_off[sub];
+  for (int f = sub_face_ptr[sub]; f < sub_face_ptr[sub + 1]; ++f) {
+    double p[3][3];
+    for (int i = 0; i < 3; ++i) {
+      const int64_t v = faces[(int64_t)f * 3 + i];
+      for (int k = 0; k < 3; ++k) p[i][k] = verts[v * 3 + k];
+    }
+    double mf[3][3];
+    triangle_tangential_mass(p, mf);
+    for (int a = 0; a < 3; ++a) {
+      const int la = face_l[(int64_t)f * 3 + a];
+      if (la < 0) continue;
+      for (int b = 0; b < 3; ++b) {
+        const int lb = face_l[(int64_t)f * 3 + b];
+        if (lb < 0) continue;
+        const int slot = csr_find(rp, cl, la, lb);
+        vv[slot] = cadd(vv[slot], make_double2(coef.x * mf[a][b], coef.y * mf[a][b]));
+      }
+    }
+  }
+}
+
+static unsigned gsb(mdd_ctx* ctx, int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->nsm * 16));
+}
+static unsigned nb(int64_t n, int bs) { return (unsigned)std::max<int64_t>(1, (n + bs - 1) / bs); }
+
+// ------------------------------------------------------------ apply
+static void one_level(mdd_prec* P, const double2* v, const double2* add, double2* out,
+                      cudaStream_t s) {
+  PrecCore& c = *P->core;
+  mdd_ctx* ctx = c.ctx;
+  const int64_t nl = c.sub.nloc;
+  if (nl) {
+    k_gather<<<gsb(ctx, nl), 256, 0, s>>>(nl, c.gidx.p, v, c.sub.bloc.p);
+    CK_LAUNCH(ctx);
+    c.sub.solve(s);
+  }
+  const bool weighted = P->family != 0;  // ras / impras (precond.py:348)
+  k_scatter_owner<<<gsb(ctx, c.ndof), 256, 0, s>>>(c.ndof, c.own_ptr.p, c.own_idx.p,
+                                                   weighted ? c.own_w.p : nullptr, c.sub.xloc.p,
+                                                   add, out);
+  CK_LAUNCH(ctx);
+}
+
+// out = R0^T A0^{-1} R0 v   (precond.py:357-358)
+static void coarse_solve(mdd_prec* P, const double2* v, double2* out, cudaStream_t s) {
+  PrecCore& c = *P->core;
+  spmv_dev(c.ctx, c.R0p.get(), v, c.coarse.bloc.p, s);
+  c.coarse.solve(s);
+  spmv_dev(c.ctx, c.R0Tp.get(), c.coarse.xloc.p, out, s);
+}
+
+void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s) {
+  PrecCore& c = *P->core;
+  if (P->levels == 1) {
+    one_level(P, v, nullptr, out, s);
+    return;
+  }
+  const int64_t n = c.ndof;
+  double2* gv = c.t1.p;
+  coarse_solve(P, v, gv, s);
+  if (P->correction == 0) {  // additive: B1 v + G v
+    one_level(P, v, gv, out, s);
+    return;
+  }
+  // t = v - A_corr G v
+  double2* t = c.t2.p;
+  spmv_dev_axpby(c.ctx, P->A_corr, gv, t, make_double2(-1.0, 0.0), make_double2(1.0, 0.0), v, s);
+  if (P->correction == 2) {  // adef1: B1 (v - A G v) + G v
+    one_level(P, t, gv, out, s);
+    return;
+  }
+  // hybrid: y = B1 t ; out = y - G (A_corr y) + G v
+  double2* y = c.t3.p;
+  one_level(P, t, nullptr, y, s);
+  spmv_dev(c.ctx, P->A_corr, y, t, s);
+  double2* cy = c.t4.p;
+  coarse_solve(P, t, cy, s);
+  k_sub_add<<<gsb(c.ctx, n), 256, 0, s>>>(n, y, cy, gv, out);
+  CK_LAUNCH(c.ctx);
+}
+
+// ------------------------------------------------------------- setup
+static std::unique_ptr<mdd_csr> csr_host(mdd_ctx* ctx, int64_t nr, int64_t nc,
+                                         std::vector<int32_t>&& rp, std::vector<int32_t>&& cl,
+                                         const std::vector<double>& v) {
+  std::unique_ptr<mdd_csr> A(new mdd_csr());
+  A->ctx = ctx;
+  A->is_complex = false;
+  A->pat = make_pattern(nr, nc, std::move(rp), std::move(cl), ctx->stream);
+  A->vals.upload(v, ctx->stream);
+  return A;
+}
+
+static void galerkin_assemble(PrecCore& c, const mdd_coeffs* co, cudaStream_t s) {
+  mdd_ctx* ctx = c.ctx;
+  const mdd_space* fs = c.fine_space;
+  const mdd_space* cs = c.coarse_space;
+  GalArgs ga{fs->verts.p, fs->tets.p, fs->tet_edges.p, fs->signs.p, fs->e2d.p,
+             cs->verts.p, cs->tets.p, cs->signs.p,     c.tet_map.p};
+  DevBuf<double> BS(fs->nt * 36), BM(fs->nt * 36), BF;
+  k_galerkin_tets<<<nb(fs->nt, 128), 128, 0, s>>>(fs->nt, ga, BS.p, BM.p);
+  CK_LAUNCH(ctx);
+  if (c.n_gfaces) {
+    BF.alloc(c.n_gfaces * 36);
+    k_galerkin_faces<<<nb(c.n_gfaces, 128), 128, 0, s>>>(c.n_gfaces, ga, c.gfaces.p, c.face_tet.p,
+                                                        BF.p);
+    CK_LAUNCH(ctx);
+  }
+  DevBuf<double> deps, dmu, dsig;
+  CoefArr ca{nullptr, nullptr, nullptr, co->eps0, co->mu0, co->sigma0, co->k, co->xi,
+             co->homogeneous, make_double2(0.0, -(co->xi >= 0 ? 1.0 : -1.0) * co->k)};
+  if (!co->homogeneous) {
+    if (co->eps) { deps.upload(co->eps, fs->nt, s); ca.eps = deps.p; }
+    if (co->mu) { dmu.upload(co->mu, fs->nt, s); ca.mu = dmu.p; }
+    if (co->sigma) { dsig.upload(co->sigma, fs->nt, s); ca.sigma = dsig.p; }
+  }
+  DevBuf<double2> blk(cs->nt * 36);
+  k_galerkin_reduce<<<nb(cs->nt * 36, 256), 256, 0, s>>>(
+      cs->nt, c.cfine_ptr.p, c.cfine_idx.p, BS.p, BM.p, c.n_gfaces ? c.cface_ptr.p : nullptr,
+      c.n_gfaces ? c.cface_idx.p : nullptr, c.n_gfaces ? BF.p : nullptr, ca, blk.p);
+  CK_LAUNCH(ctx);
+  c.A0->vals.zero(s);
+  for (int col = 0; col < 8; ++col) {
+    const int64_t ncell = cs->color_off[col + 1] - cs->color_off[col];
+    if (!ncell) continue;
+    k_scatter_blocks<<<nb(ncell, 128), 128, 0, s>>>(
+        cs->cells_by_color.p + cs->color_off[col], ncell, cs->tet_edges.p, cs->e2d.p,
+        cs->pat->rowptr.p, cs->pat->cols.p, blk.p, reinterpret_cast<double2*>(c.A0->vals.p));
+    CK_LAUNCH(ctx);
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+static void impras_local_assemble(PrecCore& c, const mdd_coeffs* co, cudaStream_t s) {
+  mdd_ctx* ctx = c.ctx;
+  const mdd_space* fs = c.fine_space;
+  c.loc_vals.zero(s);
+  DevBuf<double> deps, dmu, dsig;
+  CoefArr ca{nullptr, nullptr, nullptr, co->eps0, co->mu0, co->sigma0, co->k, co->xi,
+             co->homogeneous, make_double2(0.0, 0.0)};
+  if (co->eps) { deps.upload(co->eps, fs->nt, s); ca.eps = deps.p; }
+  if (co->mu) { dmu.upload(co->mu, fs->nt, s); ca.mu = dmu.p; }
+  if (co->sigma) { dsig.upload(co->sigma, fs->nt, s); ca.sigma = dsig.p; }
+  for (int col = 0; col < 8; ++col) {
+    const int64_t b = c.loc_color_off[col], e = c.loc_color_off[col + 1];
+    if (e <= b) continue;
+    // pair arrays are laid out [cell | sub | mask] consecutively per colour block
+    k_local_cells<<<nb(e - b, 128), 128, 0, s>>>(
+        e - b, c.loc_tet.p + b, c.loc_tet_sub.p + b, c.loc_tet.p + c.loc_color_off[8] + b,
+        fs->verts.p, fs->tets.p, fs->signs.p, c.loc_e2l.p + b * 36, c.loc_row_off.p,
+        c.loc_rowptr.p, c.loc_cols.p, c.loc_sub_off.p, ca,
+        c.loc_vals.p);
+    CK_LAUNCH(ctx);
+  }
+  if (c.n_loc_faces) {
+    const double2 coef = make_double2(0.0, -(co->xi >= 0 ? 1.0 : -1.0) * co->k);
+    k_local_faces<<<nb(c.nsub, 64), 64, 0, s>>>(c.nsub, c.loc_face_sub.p, c.loc_face.p,
+                                                c.loc_face_l.p, fs->verts.p, c.loc_row_off.p,
+                                                c.loc_rowptr.p, c.loc_cols.p, c.loc_sub_off.p,
+                                                coef, c.loc_vals.p);
+    CK_LAUNCH(ctx);
+  }
+}
+
+static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc,
+                          int32_t* failed_ctx) {
+  PrecCore& c = *P->core;
+  mdd_ctx* ctx = c.ctx;
+  cudaStream_t s = ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  if (c.local_kind == 0) {
+    c.sub.factor(reinterpret_cast<const double2*>(A_prec->vals.p), s);
+  } else {
+    impras_local_assemble(c, pc, s);
+    c.sub.factor(c.loc_vals.p, s);
+  }
+  if (c.have_coarse) {
+    galerkin_assemble(c, pc, s);
+    c.coarse.factor(reinterpret_cast<const double2*>(c.A0->vals.p), s);
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c.stats[4] = ms;
+  std::string msg;
+  const int bad = c.sub.check_pivots(msg, s);
+  if (bad >= 0) {
+    if (failed_ctx) *failed_ctx = bad;
+    fail(MDD_ESINGULAR, "subdomain " + std::to_string(bad) + ": " + msg, bad);
+  }
+  if (c.have_coarse) {
+    if (c.coarse.check_pivots(msg, s) >= 0) {
+      if (failed_ctx) *failed_ctx = -1;
+      fail(MDD_ESINGULAR, "coarse space: " + msg, -1);
+    }
+  }
+}
+
+}  // namespace mdd
+
+using namespace mdd;
+
+extern "C" {
+
+int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_t* failed_ctx) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (failed_ctx) *failed_ctx = -2;
+  if (!d->A_prec || !d->A_prec->is_complex) fail(MDD_EINVAL, "prec: A_prec must be complex CSR");
+  auto core = std::make_shared<PrecCore>();
+  PrecCore& c = *core;
+  c.ctx = ctx;
+  c.ndof = d->A_prec->nrow();
+  c.nsub = d->nsub;
+  c.local_kind = d->family == 2 ? 1 : 0;
+  c.fine_space = d->space;
+  const int64_t ndof = c.ndof;
+  const int leaf = d->leaf_size > 0 ? d->leaf_size : 64;
+  const mdd_pattern& AP = *d->A_prec->pat;
+  // ---- size cap (linalg.py:80-84), checked in subdomain order
+  for (int l = 0; l < d->nsub; ++l) {
+    const int64_t nl = d->sub_ptr[l + 1] - d->sub_ptr[l];
+    if (d->lu_cap > 0 && nl > d->lu_cap) {
+      if (failed_ctx) *failed_ctx = l;
+      fail(MDD_ECAP, "subdomain " + std::to_string(l) + ": dense factor of size " +
+                         std::to_string(nl) + " exceeds cap " + std::to_string(d->lu_cap) +
+                         "; raise the cap or shrink the block", l);
+    }
+  }
+  // ---- local matrices (patterns + value sources)
+  std::vector<MatrixInput> mats(d->nsub);
+  if (c.local_kind == 0) {
+    // exact minors of A_prec on I_l (precond.py:296-301)
+    const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    for (unsigned t = 0; t < nth; ++t)
+      th.emplace_back([&] {
+        std::vector<int32_t> g2l(ndof, -1);
+        for (int l = next++; l < d->nsub; l = next++) {
+          MatrixInput& mi = mats[l];
+          const int64_t b = d->sub_ptr[l], e = d->sub_ptr[l + 1];
+          mi.n = (int32_t)(e - b);
+          for (int64_t i = b; i < e; ++i) g2l[d->sub_dofs[i]] = (int32_t)(i - b);
+          mi.rowptr.assign(1, 0);
+          mi.xyz.resize(3 * (size_t)mi.n);
+          for (int64_t i = b; i < e; ++i) {
+            const int64_t g = d->sub_dofs[i];
+            for (int32_t k = AP.h_rowptr[g]; k < AP.h_rowptr[g + 1]; ++k) {
+              const int32_t lc = g2l[AP.h_cols[k]];
+              if (lc >= 0) {
+                mi.cols.push_back(lc);
+                mi.src.push_back(k);
+              }
+            }
+            mi.rowptr.push_back((int32_t)mi.cols.size());
+            for (int a = 0; a < 3; ++a) mi.xyz[3 * (i - b) + a] = d->dof_xyz[3 * g + a];
+          }
+          for (int64_t i = b; i < e; ++i) g2l[d->sub_dofs[i]] = -1;
+        }
+      });
+    for (auto& x : th) x.join();
+  } else {
+    // impras: submesh assembly + boundary faces (precond.py:212-269)
+    const mdd_space* fs = d->space;
+    if (!fs || !d->sub_tet_ptr || !d->sub_tets) fail(MDD_EINVAL, "impras needs subdomain tets");
+    const int64_t nv = fs->nv;
+    std::vector<int32_t> h_cell, h_sub, h_mask, h_e2l;
+    std::vector<std::vector<int64_t>> pairs_by_col(8);  // encoded index into per-sub lists
+    std::vector<int32_t> row_off(d->nsub + 1, 0), ent_off(d->nsub + 1, 0);
+    std::vector<int32_t> all_rowptr, all_cols;
+    std::vector<std::vector<int32_t>> sub_e2l(d->nsub);
+    // edge key lookup for faces
+    std::vector<int64_t> ekeys(fs->ne);
+    {
+      static const int EA[6] = {0, 0, 0, 1, 1, 2}, EB[6] = {1, 2, 3, 2, 3, 3};
+      for (int64_t t = 0; t < fs->nt; ++t)
+        for (int e = 0; e < 6; ++e) {
+          int64_t a = fs->h_tets[t * 4 + EA[e]], b = fs->h_tets[t * 4 + EB[e]];
+          if (a > b) std::swap(a, b);
+          ekeys[fs->h_tet_edges[t * 6 + e]] = a * nv + b;
+        }
+    }
+    std::vector<int32_t> eorder(fs->ne);
+    std::iota(eorder.begin(), eorder.end(), 0);
+    std::sort(eorder.begin(), eorder.end(), [&](int32_t x, int32_t y) { return ekeys[x] < ekeys[y]; });
+    auto find_edge = [&](int64_t a, int64_t b) {
+      const int64_t key = a * nv + b;
+      auto it = std::lower_bound(eorder.begin(), eorder.end(), key,
+                                 [&](int32_t id, int64_t k) { return ekeys[id] < k; });
+      if (it == eorder.end() || ekeys[*it] != key) fail(MDD_EINVAL, "face edge not in mesh");
+      return *it;
+    };
+    std::vector<int32_t> face_flat, face_l, face_ptr(d->nsub + 1, 0);
+    const int64_t ncell = (int64_t)fs->n * fs->n * fs->n;
+    std::vector<int32_t> g2l(ndof, -1);
+    for (int l = 0; l < d->nsub; ++l) {
+      MatrixInput& mi = mats[l];
+      const int64_t b = d->sub_ptr[l], e = d->sub_ptr[l + 1];
+      mi.n = (int32_t)(e - b);
+      for (int64_t i = b; i < e; ++i) g2l[d->sub_dofs[i]] = (int32_t)(i - b);
+      // local pattern: pairs sharing a subdomain tet, plus boundary-face pairs (subset)
+      std::vector<std::vector<int32_t>> rows(mi.n);
+      const int64_t tb = d->sub_tet_ptr[l], te = d->sub_tet_ptr[l + 1];
+      std::unordered_map<int64_t, int32_t> cellmask;
+      for (int64_t k = tb; k < te; ++k) {
+        const int64_t t = d->sub_tets[k];
+        int32_t loc[6];
+        for (int q = 0; q < 6; ++q) {
+          const int32_t dd = fs->h_e2d[fs->h_tet_edges[t * 6 + q]];
+          loc[q] = dd >= 0 ? g2l[dd] : -1;
+        }
+        for (int a = 0; a < 6; ++a)
+          if (loc[a] >= 0)
+            for (int q = 0; q < 6; ++q)
+              if (loc[q] >= 0) rows[loc[a]].push_back(loc[q]);
+        cellmask[t / 6] |= 1 << (t % 6);
+      }
+      row_off[l + 1] = row_off[l] + mi.n + 1;
+      mi.rowptr.assign(1, 0);
+      for (int32_t i = 0; i < mi.n; ++i) {
+        auto& r = rows[i];
+        std::sort(r.begin(), r.end());
+        r.erase(std::unique(r.begin(), r.end()), r.end());
+        for (int32_t cc : r) mi.cols.push_back(cc);
+        mi.rowptr.push_back((int32_t)mi.cols.size());
+      }
+      mi.src.resize(mi.cols.size());
+      for (size_t k = 0; k < mi.cols.size(); ++k) mi.src[k] = ent_off[l] + (int32_t)k;
+      ent_off[l + 1] = ent_off[l] + (int32_t)mi.cols.size();
+      all_rowptr.insert(all_rowptr.end(), mi.rowptr.begin(), mi.rowptr.end());
+      all_cols.insert(all_cols.end(), mi.cols.begin(), mi.cols.end());
+      mi.xyz.resize(3 * (size_t)mi.n);
+      for (int64_t i = b; i < e; ++i)
+        for (int a = 0; a < 3; ++a) mi.xyz[3 * (i - b) + a] = d->dof_xyz[3 * d->sub_dofs[i] + a];
+      // (subdomain, cell) pairs by colour
+      std::vector<int64_t> cells;
+      for (auto& kv : cellmask) cells.push_back(kv.first);
+      std::sort(cells.begin(), cells.end());
+      for (int64_t cell : cells) {
+        const int64_t n = fs->n;
+        const int64_t cx = cell / (n * n), cy = (cell / n) % n, cz = cell % n;
+        const int colr = (int)(((cx & 1) << 2) | ((cy & 1) << 1) | (cz & 1));
+        pairs_by_col[colr].push_back((int64_t)h_cell.size());
+        h_cell.push_back((int32_t)cell);
+        h_sub.push_back(l);
+        h_mask.push_back(cellmask[cell]);
+        for (int p = 0; p < 6; ++p)
+          for (int q = 0; q < 6; ++q) {
+            const int64_t t = cell * 6 + p;
+            const int32_t dd = fs->h_e2d[fs->h_tet_edges[t * 6 + q]];
+            h_e2l.push_back(((cellmask[cell] >> p) & 1) && dd >= 0 ? g2l[dd] : -1);
+          }
+      }
+      // boundary faces of the subdomain
+      if (d->sub_bface_ptr) {
+        for (int64_t f = d->sub_bface_ptr[l]; f < d->sub_bface_ptr[l + 1]; ++f) {
+          const int64_t* fv = d->sub_bfaces + 3 * f;
+          const int tp[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+          for (int q = 0; q < 3; ++q) face_flat.push_back((int32_t)fv[q]);
+          for (int q = 0; q < 3; ++q) {
+            const int32_t dd = fs->h_e2d[find_edge(fv[tp[q][0]], fv[tp[q][1]])];
+            face_l.push_back(dd >= 0 ? g2l[dd] : -1);
+          }
+        }
+        face_ptr[l + 1] = (int32_t)(face_flat.size() / 3);
+      }
+      for (int64_t i = b; i < e; ++i) g2l[d->sub_dofs[i]] = -1;
+      (void)ncell;
+    }
+    // reorder pair arrays by colour
+    std::vector<int32_t> pc, ps, pm, pe;
+    c.loc_color_off.assign(9, 0);
+    for (int col = 0; col < 8; ++col) {
+      c.loc_color_off[col] = (int64_t)pc.size();
+      for (int64_t k : pairs_by_col[col]) {
+        pc.push_back(h_cell[k]);
+        ps.push_back(h_sub[k]);
+        pm.push_back(h_mask[k]);
+        pe.insert(pe.end(), h_e2l.begin() + k * 36, h_e2l.begin() + k * 36 + 36);
+      }
+    }
+    c.loc_color_off[8] = (int64_t)pc.size();
+    std::vector<int32_t> cellmask_arr(pc);
+    cellmask_arr.insert(cellmask_arr.end(), pm.begin(), pm.end());
+    c.loc_tet.upload(cellmask_arr, s);  // [cells | masks]
+    c.loc_tet_sub.upload(ps, s);
+    c.loc_e2l.upload(pe, s);
+    c.loc_row_off.upload(row_off, s);
+    c.loc_rowptr.upload(all_rowptr, s);
+    c.loc_cols.upload(all_cols, s);
+    c.loc_sub_off.upload(ent_off, s);
+    c.loc_vals.alloc(std::max<int64_t>(1, ent_off[d->nsub]));
+    c.loc_face.upload(face_flat, s);
+    c.loc_face_l.upload(face_l, s);
+    c.loc_face_sub.upload(face_ptr, s);
+    c.n_loc_faces = (int64_t)face_flat.size() / 3;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  c.sub.build(ctx, mats, leaf);
+  // gather indices + ownership (subdomain order)
+  {
+    std::vector<int32_t> gidx(c.sub.nloc);
+    std::vector<double> wloc(c.sub.nloc, 1.0);
+    for (int l = 0; l < d->nsub; ++l) {
+      const int64_t b = d->sub_ptr[l];
+      const auto& pm = c.sub.perm[l];
+      for (int32_t a = 0; a < c.sub.mat_n[l]; ++a) {
+        gidx[c.sub.mat_off[l] + a] = (int32_t)d->sub_dofs[b + pm[a]];
+        if (d->sub_pou) wloc[c.sub.mat_off[l] + a] = d->sub_pou[b + pm[a]];
+      }
+    }
+    std::vector<int32_t> optr(ndof + 1, 0), oidx(c.sub.nloc);
+    std::vector<double> ow(c.sub.nloc);
+    for (int64_t t = 0; t < c.sub.nloc; ++t) optr[gidx[t] + 1]++;
+    for (int64_t i = 0; i < ndof; ++i) optr[i + 1] += optr[i];
+    std::vector<int32_t> fillp(optr.begin(), optr.end() - 1);
+    for (int64_t t = 0; t < c.sub.nloc; ++t) {  // ascending t == ascending subdomain
+      const int32_t k = fillp[gidx[t]]++;
+      oidx[k] = (int32_t)t;
+      ow[k] = wloc[t];
+    }
+    c.gidx.upload(gidx, s);
+    c.own_ptr.upload(optr, s);
+    c.own_idx.upload(oidx, s);
+    c.own_w.upload(ow, s);
+  }
+  // ---- coarse level
+  if (d->levels == 2) {
+    if (!d->R0 || !d->coarse_space || !d->tet_map || !d->coarse_dof_xyz)
+      fail(MDD_EINVAL, "two-level preconditioner needs a coarse link");
+    c.have_coarse = true;
+    const mdd_space* cs = d->coarse_space;
+    c.coarse_space = cs;
+    c.ncs = cs->ndof;
+    if (d->R0->nrow() != c.ncs || d->R0->ncol() != ndof) fail(MDD_EINVAL, "R0 has the wrong shape");
+    if (d->lu_cap > 0 && c.ncs > d->lu_cap) {
+      if (failed_ctx) *failed_ctx = -1;
+      fail(MDD_ECAP, "coarse space: dense factor of size " + std::to_string(c.ncs) +
+                         " exceeds cap " + std::to_string(d->lu_cap) +
+                         "; raise the cap or shrink the block", -1);
+    }
+    c.A0.reset(new_csr(ctx, cs->pat, true));
+    std::vector<MatrixInput> cm(1);
+    cm[0].n = (int32_t)c.ncs;
+    cm[0].rowptr = cs->pat->h_rowptr;
+    cm[0].cols = cs->pat->h_cols;
+    cm[0].src.resize(cm[0].cols.size());
+    std::iota(cm[0].src.begin(), cm[0].src.end(), 0);
+    cm[0].xyz.assign(d->coarse_dof_xyz, d->coarse_dof_xyz + 3 * c.ncs);
+    c.coarse.build(ctx, cm, leaf);
+    // R0 with rows in coarse ND order; R0^T with columns in coarse ND order
+    const auto& pm = c.coarse.perm[0];
+    std::vector<int32_t> ip(c.ncs);
+    for (int64_t a = 0; a < c.ncs; ++a) ip[pm[a]] = (int32_t)a;
+    const mdd_pattern& RP = *d->R0->pat;
+    std::vector<double> rv(RP.nnz);
+    d->R0->vals.download(rv.data(), RP.nnz, s);
+    CK(cudaStreamSynchronize(s));
+    std::vector<int32_t> rp(c.ncs + 1, 0), rc;
+    std::vector<double> rvals;
+    rc.reserve(RP.nnz);
+    rvals.reserve(RP.nnz);
+    for (int64_t a = 0; a < c.ncs; ++a) {
+      const int32_t r = pm[a];
+      for (int32_t k = RP.h_rowptr[r]; k < RP.h_rowptr[r + 1]; ++k) {
+        rc.push_back(RP.h_cols[k]);
+        rvals.push_back(rv[k]);
+      }
+      rp[a + 1] = (int32_t)rc.size();
+    }
+    c.R0p = csr_host(ctx, c.ncs, ndof, std::move(rp), std::move(rc), rvals);
+    std::vector<int32_t> tp(ndof + 1, 0), tc(RP.nnz);
+    std::vector<double> tv(RP.nnz);
+    for (int64_t k = 0; k < RP.nnz; ++k) tp[RP.h_cols[k] + 1]++;
+    for (int64_t i = 0; i < ndof; ++i) tp[i + 1] += tp[i];
+    std::vector<int32_t> fp(tp.begin(), tp.end() - 1);
+    for (int64_t r = 0; r < c.ncs; ++r)  // ascending original coarse index p
+      for (int32_t k = RP.h_rowptr[r]; k < RP.h_rowptr[r + 1]; ++k) {
+        const int32_t pos = fp[RP.h_cols[k]]++;
+        tc[pos] = ip[r];
+        tv[pos] = rv[k];
+      }
+    c.R0Tp = csr_host(ctx, ndof, c.ncs, std::move(tp), std::move(tc), tv);
+    // Galerkin index data: fine tets per coarse tet (ascending)
+    const mdd_space* fs = d->space;
+    if (!fs) fail(MDD_EINVAL, "two-level preconditioner needs the fine space");
+    std::vector<int32_t> tm(fs->nt);
+    for (int64_t t = 0; t < fs->nt; ++t) {
+      if (d->tet_map[t] < 0 || d->tet_map[t] >= cs->nt) fail(MDD_EINVAL, "tet_map out of range");
+      tm[t] = (int32_t)d->tet_map[t];
+    }
+    std::vector<int32_t> cptr(cs->nt + 1, 0), cidx(fs->nt);
+    for (int64_t t = 0; t < fs->nt; ++t) cptr[tm[t] + 1]++;
+    for (int64_t q = 0; q < cs->nt; ++q) cptr[q + 1] += cptr[q];
+    {
+      std::vector<int32_t> f2(cptr.begin(), cptr.end() - 1);
+      for (int64_t t = 0; t < fs->nt; ++t) cidx[f2[tm[t]]++] = (int32_t)t;
+    }
+    c.tet_map.upload(tm, s);
+    c.cfine_ptr.upload(cptr, s);
+    c.cfine_idx.upload(cidx, s);
+    // global impedance faces -> containing fine tet
+    c.n_gfaces = d->nbf_global;
+    if (c.n_gfaces) {
+      const int64_t nv = fs->nv;
+      std::unordered_map<int64_t, int32_t> fkey;
+      fkey.reserve(c.n_gfaces * 2);
+      for (int64_t f = 0; f < c.n_gfaces; ++f) {
+        const int64_t* v = d->bfaces_global + 3 * f;
+        fkey[(v[0] * nv + v[1]) * nv + v[2]] = (int32_t)f;
+      }
+      std::vector<int32_t> ftet(c.n_gfaces, -1), gf(3 * c.n_gfaces);
+      static const int LF[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+      for (int64_t t = 0; t < fs->nt; ++t)
+        for (int q = 0; q < 4; ++q) {
+          int64_t v[3] = {fs->h_tets[t * 4 + LF[q][0]], fs->h_tets[t * 4 + LF[q][1]],
+                          fs->h_tets[t * 4 + LF[q][2]]};
+          std::sort(v, v + 3);
+          auto it = fkey.find((v[0] * nv + v[1]) * nv + v[2]);
+          if (it != fkey.end()) ftet[it->second] = (int32_t)t;
+        }
+      for (int64_t f = 0; f < c.n_gfaces; ++f) {
+        if (ftet[f] < 0) fail(MDD_EINVAL, "boundary face without a tet");
+        for (int q = 0; q < 3; ++q) gf[3 * f + q] = (int32_t)d->bfaces_global[3 * f + q];
+      }
+      std::vector<int32_t> gptr(cs->nt + 1, 0), gidx2(c.n_gfaces);
+      for (int64_t f = 0; f < c.n_gfaces; ++f) gptr[tm[ftet[f]] + 1]++;
+      for (int64_t q = 0; q < cs->nt; ++q) gptr[q + 1] += gptr[q];
+      std::vector<int32_t> f2(gptr.begin(), gptr.end() - 1);
+      for (int64_t f = 0; f < c.n_gfaces; ++f) gidx2[f2[tm[ftet[f]]]++] = (int32_t)f;
+      c.face_tet.upload(ftet, s);
+      c.gfaces.upload(gf, s);
+      c.cface_ptr.upload(gptr, s);
+      c.cface_idx.upload(gidx2, s);
+    }
+  }
+  c.t1.alloc(ndof);
+  c.t2.alloc(ndof);
+  c.t3.alloc(ndof);
+  c.t4.alloc(ndof);
+  const double sym_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  auto P = std::make_unique<mdd_prec>();
+  P->core = core;
+  P->family = d->family;
+  P->levels = d->levels;
+  P->correction = d->correction;
+  P->A_corr = d->A_corr ? d->A_corr : d->A_prec;
+  numeric_setup(P.get(), d->A_prec, d->prec_coeffs, failed_ctx);
+  c.stats[0] = c.sub.nnodes + c.coarse.nnodes;
+  c.stats[1] = std::max(c.sub.max_m, c.coarse.max_m);
+  c.stats[2] = c.sub.factor_entries + c.coarse.factor_entries;
+  c.stats[3] = c.sub.factor_flops + c.coarse.factor_flops;
+  c.stats[5] = std::max(c.sub.nlevels, c.coarse.nlevels);
+  c.stats[6] = (double)c.sub.nloc;
+  c.stats[7] = (double)c.ncs;
+  (void)sym_ms;
+  *out = P.release();
+  MDD_API_END
+}
+
+int mdd_prec_variant(const mdd_prec* base, int family, int levels, int correction,
+                     const mdd_csr* A_corr, mdd_prec** out) {
+  MDD_API_BEGIN
+  const int kind_b = base->family == 2 ? 1 : 0, kind_n = family == 2 ? 1 : 0;
+  if (kind_b != kind_n) fail(MDD_EINVAL, "variant would need different local factorizations");
+  if (levels == 2 && !base->core->have_coarse)
+    fail(MDD_EINVAL, "variant needs a coarse factor the state does not hold");
+  auto P = std::make_unique<mdd_prec>();
+  P->core = base->core;
+  P->family = family;
+  P->levels = levels;
+  P->correction = correction;
+  P->A_corr = A_corr ? A_corr : base->A_corr;
+  *out = P.release();
+  MDD_API_END
+}
+
+void mdd_prec_destroy(mdd_prec* P) {
+  if (!P) return;
+  cudaSetDevice(P->core->ctx->device);
+  delete P;
+}
+
+int mdd_prec_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out) {
+  MDD_API_BEGIN
+  mdd_ctx* ctx = P->core->ctx;
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = P->core->ndof;
+  DevBuf<double2> dv(n), dout(n);
+  dv.upload(reinterpret_cast<const double2*>(v), n, ctx->stream);
+  prec_apply_dev(P, dv.p, dout.p, ctx->stream);
+  dout.download(reinterpret_cast<double2*>(out), n, ctx->stream);
+  CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out) {
+  MDD_API_BEGIN
+  mdd_ctx* ctx = P->core->ctx;
+  CK(cudaSetDevice(ctx->device));
+  if (!P->core->have_coarse) fail(MDD_EINVAL, "preconditioner has no coarse level");
+  const int64_t n = P->core->ndof;
+  DevBuf<double2> dv(n), dout(n);
+  dv.upload(reinterpret_cast<const double2*>(v), n, ctx->stream);
+  coarse_solve(P, dv.p, dout.p, ctx->stream);
+  dout.download(reinterpret_cast<double2*>(out), n, ctx->stream);
+  CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+int mdd_prec_stats(const mdd_prec* P, double* out8) {
+  MDD_API_BEGIN
+  for (int i = 0; i < 8; ++i) out8[i] = P->core->stats[i];
+  MDD_API_END
+}
+
+int mdd_prec_refactor(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(P->core->ctx->device));
+  numeric_setup(P, A_prec, pc, nullptr);
+  MDD_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+"""Device sparse matrices and the reference's linear-algebra error classes.
+
+Mirrors reference ``maxwelldd.linalg`` (/root/reference/pkg/src/maxwelldd/
+linalg.py:1-130).  Matrices produced by the device path are
+:class:`DeviceCSR`: complex128/float64 CSR (int32 indptr/indices) resident
+on the GPU behind an opaque ``mdd_csr`` handle.  ``A @ x`` runs the sm_100a
+SpMV kernel (linalg.spmv, linalg.py:41-45); the scipy view (``to_scipy()``,
+``.data``/``.indices``/``.indptr``) is materialised lazily for callers that
+inspect entries.
+
+The dense LAPACK factorisation of the reference (``DenseLU``) has no
+counterpart: local and coarse blocks are factorised by the device
+multifrontal engine inside :func:`paper_1711_03789_b200.precond.setup`.
+``triple_product`` and ``selection_matrix`` are kept as host index helpers
+for callers and tests; the device path never calls them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+
+__all__ = [
+    "DEFAULT_LU_CAP",
+    "DeviceCSR",
+    "SingularMatrixError",
+    "SizeCapError",
+    "as_device_csr",
+    "selection_matrix",
+    "spmv",
+    "triple_product",
+    "weighted_dot",
+    "weighted_norm",
+]
+
+DEFAULT_LU_CAP = 4000  # reference linalg.py:30
+
+
+class SingularMatrixError(RuntimeError):
+    """A factorisation hit a pivot below tolerance (reference linalg.py:33)."""
+
+
+class SizeCapError(RuntimeError):
+    """A block exceeds the configured factor size cap (reference linalg.py:37)."""
+
+
+def raise_for(err: "_lib.MddError"):
+    """Translate a C-ABI error code into the reference exception class."""
+    msg = str(err)
+    if err.code == _lib.MDD_ESINGULAR:
+        raise SingularMatrixError(msg) from None
+    if err.code == _lib.MDD_ECAP:
+        raise SizeCapError(msg) from None
+    if err.code == _lib.MDD_EINVAL:
+        raise ValueError(msg) from None
+    raise RuntimeError(msg) from None
+
+
+class DeviceCSR:
+    """CSR matrix resident on the GPU (opaque ``mdd_csr``)."""
+
+    __array_priority__ = 20.0
+
+    def __init__(self, handle, ctx: "_lib.Context", shape, is_complex: bool, nnz: int):
+        self._h = handle
+        self._ctx = ctx
+        self.shape = (int(shape[0]), int(shape[1]))
+        self.dtype = np.dtype(np.complex128 if is_complex else np.float64)
+        self.nnz = int(nnz)
+        self._host = None
+
+    ndim = 2
+    format = "csr"
+
+    # ---------------------------------------------------------- creation
+    @classmethod
+    def from_handle(cls, handle, ctx=None) -> "DeviceCSR":
+        ctx = ctx or _lib.get_context()
+        nr, nc, nz, cx = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        _lib.check(_lib.lib.mdd_csr_info(handle, C.byref(nr), C.byref(nc), C.byref(nz), C.byref(cx)))
+        return cls(handle, ctx, (nr.value, nc.value), bool(cx.value), nz.value)
+
+    @classmethod
+    def from_scipy(cls, m, ctx=None, force_complex: bool = False) -> "DeviceCSR":
+        ctx = ctx or _lib.get_context()
+        m = sp.csr_matrix(m)
+        m.sort_indices()
+        cplx = force_complex or np.iscomplexobj(m.data)
+        vals = np.ascontiguousarray(m.data, dtype=np.complex128 if cplx else np.float64)
+        ip = np.ascontiguousarray(m.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(m.indices, dtype=np.int32)
+        h = C.c_void_p()
+        _lib.check(
+            _lib.lib.mdd_csr_from_host(
+                ctx.handle,
+                m.shape[0],
+                m.shape[1],
+                m.nnz,
+                _lib.ptr(ip, C.c_int32),
+                _lib.ptr(ix, C.c_int32),
+                vals.ctypes.data_as(C.c_void_p),
+                1 if cplx else 0,
+                C.byref(h),
+            )
+        )
+        out = cls(h, ctx, m.shape, cplx, m.nnz)
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib.mdd_csr_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---------------------------------------------------------- host view
+    def to_scipy(self) -> sp.csr_matrix:
+        if self._host is None:
+            ip = np.empty(self.shape[0] + 1, dtype=np.int32)
+            ix = np.empty(self.nnz, dtype=np.int32)
+            vals = np.empty(self.nnz, dtype=self.dtype)
+            _lib.check(
+                _lib.lib.mdd_csr_to_host(
+                    self._h, _lib.ptr(ip, C.c_int32), _lib.ptr(ix, C.c_int32), vals.ctypes.data_as(C.c_void_p)
+                )
+            )
+            m = sp.csr_matrix((vals, ix, ip), shape=self.shape)
+            m.has_sorted_indices = True
+            self._host = m
+        return self._host
+
+    def tocsr(self, copy=False):
+        return self.to_scipy().copy() if copy else self.to_scipy()
+
+    def toarray(self):
+        return self.to_scipy().toarray()
+
+    def todense(self):
+        return self.to_scipy().todense()
+
+    @property
+    def data(self):
+        return self.to_scipy().data
+
+    @property
+    def indices(self):
+        return self.to_scipy().indices
+
+    @property
+    def indptr(self):
+        return self.to_scipy().indptr
+
+    @property
+    def T(self):
+        return self.to_scipy().T
+
+    def transpose(self):
+        return self.to_scipy().transpose()
+
+    def astype(self, dtype):
+        return self.to_scipy().astype(dtype)
+
+    def __getattr__(self, name):
+        # any other scipy.sparse API goes to the host view
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.to_scipy(), name)
+
+    # ---------------------------------------------------------- products
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        if x.shape[0] != self.shape[1]:
+            raise ValueError(f"dimension mismatch: matrix is {self.shape}, vector has {x.shape[0]}")
+        y = np.empty(self.shape[0], dtype=np.complex128)
+        _lib.check(_lib.lib.mdd_spmv(self._ctx.handle, self._h, _lib.zptr(x), _lib.zptr(y)))
+        return y
+
+    def __matmul__(self, other):
+        if isinstance(other, np.ndarray) and other.ndim == 1:
+            y = self.matvec(other)
+            if self.dtype == np.float64 and not np.iscomplexobj(other):
+                return y.real.copy()
+            return y
+        if isinstance(other, np.ndarray) and other.ndim == 2:
+            cols = [self.matvec(other[:, j]) for j in range(other.shape[1])]
+            y = np.stack(cols, axis=1) if cols else np.zeros((self.shape[0], 0), complex)
+            if self.dtype == np.float64 and not np.iscomplexobj(other):
+                return y.real.copy()
+            return y
+        if isinstance(other, DeviceCSR):
+            other = other.to_scipy()
+        return self.to_scipy() @ other
+
+    def __rmatmul__(self, other):
+        if isinstance(other, DeviceCSR):
+            other = other.to_scipy()
+        return other @ self.to_scipy()
+
+    dot = __matmul__
+
+    def __mul__(self, other):
+        if np.isscalar(other):
+            return self.to_scipy() * other
+        return self.__matmul__(other)
+
+    def __rmul__(self, other):
+        return self.to_scipy().__rmul__(other)
+
+    def __add__(self, other):
+        return self.to_scipy() + (other.to_scipy() if isinstance(other, DeviceCSR) else other)
+
+    def __radd__(self, other):
+        return self.__add__(other)
+
+    def __sub__(self, other):
+        return self.to_scipy() - (other.to_scipy() if isinstance(other, DeviceCSR) else other)
+
+    def __rsub__(self, other):
+        return (other.to_scipy() if isinstance(other, DeviceCSR) else other) - self.to_scipy()
+
+    def __neg__(self):
+        return -self.to_scipy()
+
+    def __repr__(self):
+        return f"<DeviceCSR {self.shape[0]}x{self.shape[1]} nnz={self.nnz} {self.dtype} on cuda:{self._ctx.device}>"
+
+
+def as_device_csr(m, force_complex: bool = False) -> DeviceCSR:
+    """Device copy of a matrix (DeviceCSR passes through)."""
+    if isinstance(m, DeviceCSR):
+        return m
+    if sp.issparse(m):
+        return DeviceCSR.from_scipy(m, force_complex=force_complex)
+    a = np.asarray(m)
+    if a.ndim != 2:
+        raise ValueError("expected a matrix")
+    return DeviceCSR.from_scipy(sp.csr_matrix(a), force_complex=force_complex)
+
+
+def spmv(a, x: np.ndarray) -> np.ndarray:
+    """Sparse matrix-vector product with a dimension check (reference linalg.py:41-45)."""
+    if a.shape[1] != np.shape(x)[0]:
+        raise ValueError(f"dimension mismatch: matrix is {a.shape}, vector has {np.shape(x)[0]}")
+    return as_device_csr(a) @ np.asarray(x)
+
+
+def triple_product(r, a, rt=None):
+    """Host helper ``R A R^T`` (reference linalg.py:48-62); not used by the device path."""
+    r = r.to_scipy() if isinstance(r, DeviceCSR) else r
+    a = a.to_scipy() if isinstance(a, DeviceCSR) else a
+    if rt is None:
+        rt = r.T
+    if r.shape[1] != a.shape[0] or a.shape[1] != rt.shape[0]:
+        raise ValueError(f"dimension mismatch: R is {r.shape}, A is {a.shape}, Rt is {rt.shape}")
+    out = (r @ a @ rt).tocsr()
+    out.sort_indices()
+    return out
+
+
+def selection_matrix(indices: np.ndarray, n: int) -> sp.csr_matrix:
+    """0/1 restriction matrix (reference linalg.py:65-70)."""
+    idx = np.asarray(indices)
+    return sp.csr_matrix((np.ones(len(idx)), (np.arange(len(idx)), idx)), shape=(len(idx), n))
+
+
+def weighted_dot(d, x: np.ndarray, y: np.ndarray) -> complex:
+    """``<x, y>_D = y^* D x`` (reference linalg.py:118-122)."""
+    if d is None:
+        return np.vdot(y, x)
+    return np.vdot(y, d @ x)
+
+
+def weighted_norm(d, x: np.ndarray) -> float:
+    n2 = weighted_dot(d, x, x)
+    if n2.real < -1e-12 * max(1.0, abs(n2)):
+        raise ValueError(f"weight matrix is not positive definite: |x|^2 = {n2.real:.3e}")
+    return float(np.sqrt(max(n2.real, 0.0)))

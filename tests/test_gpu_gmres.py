@@ -1,0 +1,166 @@
+"""Device GMRES against the reference's golden runs and its own test
+strategy (reference test_krylov.py:14-161): iteration counts within +-1 and
+relative solution difference <= 1e-8 (north_star)."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_system(rng, n, shift=6.0):
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + shift * np.eye(n)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    return a, b
+
+
+@pytest.fixture(scope="module")
+def gg():
+    return load_golden("gmres.npz")
+
+
+def test_dense_system_matches_reference(gpu, gg):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    r = gmres(gg["dense_a"], gg["dense_b"], config=KrylovConfig(tol=1e-12, maxit=120))
+    assert r.converged and abs(r.iterations - int(gg["dense_it"])) <= 1
+    assert rel(r.x, gg["dense_x"]) <= 1e-10
+    k = min(len(r.residual_history), len(gg["dense_hist"]))
+    assert np.allclose(r.residual_history[:k], gg["dense_hist"][:k], rtol=1e-6, atol=1e-14)
+
+
+@pytest.mark.parametrize("fam,lev,cor,side,wt", [
+    ("as", "two", "additive", "right", None),
+    ("ras", "two", "hybrid", "left", None),
+    ("ras", "one", "additive", "right", "dk"),
+    ("as", "two", "adef1", "right", None),
+])
+def test_preconditioned_gmres_matches_reference(gpu, gg, fam, lev, cor, side, wt):
+    from paper_1711_03789_b200 import decomp, fem, mesh, precond
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(4), "pec")
+    prob = fem.assemble(s, fem.Coefficients(k=3.0, xi=9.0), source=fem.gaussian_source)
+    d = decomp.build_decomposition(s, 2, 1, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(2), "pec"))
+    st = precond.setup(prob, d, precond.PreconditionerSpec(fam, lev, cor, xi_prec=9.0, side=side))
+    cfg = KrylovConfig(tol=1e-8, maxit=200, side=side, weight=prob.Dk if wt else None)
+    r = gmres(prob.A, prob.rhs, precond=st.apply, config=cfg)
+    tag = f"{fam}_{lev}_{cor}_{side}_{wt or 'id'}"
+    assert r.converged
+    assert abs(r.iterations - int(gg[f"{tag}_it"])) <= 1
+    assert rel(r.x, gg[f"{tag}_x"]) <= 1e-8
+
+
+def test_random_initial_guess_matches_reference(gpu, gg):
+    from paper_1711_03789_b200 import fem, mesh
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(4), "pec")
+    prob = fem.assemble(s, fem.Coefficients(k=3.0, xi=9.0), source=fem.gaussian_source)
+    r = gmres(prob.A, prob.rhs, config=KrylovConfig(tol=1e-6, maxit=60, initial_guess="random", seed=5))
+    assert abs(r.iterations - int(gg["rand_it"])) <= 1
+    assert rel(r.x, gg["rand_x"]) <= 1e-8
+
+
+def test_identity_converges_in_one(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(20) + 1j * rng.standard_normal(20)
+    rep = gmres(sp.eye(20, format="csr", dtype=complex), b, config=KrylovConfig(tol=1e-10))
+    assert rep.iterations == 1 and rep.converged
+    assert np.allclose(rep.x, b, rtol=1e-12)
+
+
+def test_exact_inverse_preconditioner_callable(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(1)
+    a, b = _random_system(rng, 25)
+    inv = np.linalg.inv(a)
+    rep = gmres(a, b, precond=lambda v: inv @ v, config=KrylovConfig(tol=1e-8))
+    assert rep.iterations == 1 and rep.converged
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_matches_dense_solve(gpu, seed):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(seed)
+    a, b = _random_system(rng, 40)
+    rep = gmres(a, b, config=KrylovConfig(tol=1e-12, maxit=120))
+    assert rep.converged
+    assert rel(rep.x, np.linalg.solve(a, b)) <= 1e-8
+
+
+def test_monotone_history_and_maxit(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(3)
+    a, b = _random_system(rng, 50, shift=2.0)
+    rep = gmres(a, b, config=KrylovConfig(tol=1e-10, maxit=60))
+    assert np.all(np.diff(rep.residual_history) <= 0) and rep.residual_history[0] == 1.0
+    a, b = _random_system(np.random.default_rng(4), 30, shift=0.5)
+    rep = gmres(a, b, config=KrylovConfig(tol=1e-14, maxit=5))
+    assert not rep.converged and rep.iterations == 5 and rep.residual_history[-1] > 1e-14
+
+
+def test_weighted_identity_bit_for_bit(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(5)
+    a, b = _random_system(rng, 25)
+    plain = gmres(a, b, config=KrylovConfig(tol=1e-9))
+    weighted = gmres(a, b, config=KrylovConfig(tol=1e-9, weight=sp.eye(25, format="csr")))
+    assert np.array_equal(plain.residual_history, weighted.residual_history)
+    assert np.array_equal(plain.x, weighted.x)
+
+
+def test_weighted_basis_orthonormal(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(6)
+    a, b = _random_system(rng, 30)
+    d = sp.diags(rng.random(30) + 0.5).tocsr()
+    rep = gmres(a, b, config=KrylovConfig(tol=1e-10, weight=d, keep_basis=True, maxit=40))
+    v = rep.basis
+    assert np.abs(v.conj().T @ (d @ v) - np.eye(v.shape[1])).max() <= 1e-10
+
+
+def test_left_preconditioning_minimizes_preconditioned_residual(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(10)
+    a, b = _random_system(rng, 25)
+    m = np.linalg.inv(a + 0.3 * np.eye(25))
+    rep = gmres(a, b, precond=lambda v: m @ v, config=KrylovConfig(tol=1e-10, side="left"))
+    assert rep.converged
+    assert np.linalg.norm(m @ (b - a @ rep.x)) / np.linalg.norm(m @ b) <= 2e-10
+
+
+def test_happy_breakdown_and_zero_rhs(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    a = np.diag([1.0, 2.0, 3.0, 4.0])
+    rep = gmres(a, np.array([1.0, 1.0, 0.0, 0.0]), config=KrylovConfig(tol=1e-16, maxit=10))
+    assert rep.iterations <= 2 and rep.converged
+    assert np.allclose(rep.x, [1.0, 0.5, 0.0, 0.0], atol=1e-12)
+    rep = gmres(np.eye(4), np.zeros(4), config=KrylovConfig())
+    assert rep.converged and rep.iterations == 0 and np.array_equal(rep.x, np.zeros(4))
+
+
+def test_translation_invariance_and_determinism(gpu):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    rng = np.random.default_rng(8)
+    a, b = _random_system(rng, 30)
+    alpha = 1.7 - 0.9j
+    r1 = gmres(a, b, config=KrylovConfig(tol=1e-9))
+    r2 = gmres(a, alpha * b, config=KrylovConfig(tol=1e-9))
+    assert np.abs(r1.residual_history - r2.residual_history).max() <= 1e-12
+    assert rel(r2.x, alpha * r1.x) <= 1e-12
+    r3 = gmres(a, b, config=KrylovConfig(tol=1e-9))
+    assert np.array_equal(r1.x, r3.x)  # fixed reduction order: bitwise reruns
