@@ -1,0 +1,437 @@
+"""Benchmark: preconditioned GMRES time-to-solve on the BASELINE configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl mine|reference]
+
+One *step* = one complete numeric solve on a fixed mesh + decomposition:
+device assembly of the problem matrix A and of the shifted A_prec
+(fem.assemble), numeric factorisation of every subdomain block, element-wise
+Galerkin coarse block and its factorisation (PreconditionerState.refactor),
+and right-preconditioned GMRES (tol 1e-6, maxit 200, zero initial guess).
+Mesh, DOF pattern, decomposition and the nested-dissection symbolic analysis
+are per-mesh setup, done once before timing (SURVEY.md §3.6's "setup" phase
+is the numeric factorisation, which is timed).
+
+value : DoFs/s = n_gpus * ndof / (device time per step), inputs resident in HBM.
+e2e   : same metric through the public API with host buffers (rhs H2D and
+        x D2H inside the timed region), wall clock.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs (SURVEY.md §8d for the conventions chosen where BASELINE is silent)
+CONFIGS = {
+    0: dict(name="cfg0", N=20, k=10.0, xi=10.0, p=2, layers=2, nc=5, family="as", corr="additive",
+            rhs=("gauss", 100.0)),
+    1: dict(name="cfg1", N=40, k=20.0, xi=20.0, p=4, layers=2, nc=10, family="as", corr="additive",
+            rhs=("random", 0)),
+    3: dict(name="cfg3", N=60, k=30.0, xi=math.sqrt(30.0), p=4, layers=2, nc=15, family="impras",
+            corr="additive", rhs=("random", 0)),
+    4: dict(name="cfg4", N=80, k=40.0, xi=0.0, p=8, layers=2, nc=20, family="as", corr="additive",
+            rhs=("gauss", 400.0), hetero=True),
+}
+METRIC = "precond_gmres_time_to_solve"
+UNIT = "DoF/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- problem
+def build_problem(c, seed=0):
+    from paper_1711_03789_b200 import decomp, fem, mesh
+
+    m = mesh.build_cube_mesh(c["N"])
+    space = fem.build_edge_space(m, "pec")
+    nt = m.n_tets
+    if c.get("hetero"):
+        # eps_r per 4x4x4 block ~ U[1,4]; absorption per block ~ U[k/2, 2k] carried by
+        # sigma = absorption / k, so k*sigma is the block absorption (fem.py:254)
+        rng = np.random.default_rng(seed)
+        blk = np.clip((m.barycenters() * 4).astype(int), 0, 3)
+        bid = (blk[:, 0] * 4 + blk[:, 1]) * 4 + blk[:, 2]
+        eps_b = 1.0 + 3.0 * rng.random(64)
+        abs_b = c["k"] * (0.5 + 1.5 * rng.random(64))
+        coeffs = fem.Coefficients(k=c["k"], xi=c["xi"], eps=eps_b[bid], sigma=abs_b[bid] / c["k"])
+    else:
+        coeffs = fem.Coefficients(k=c["k"], xi=c["xi"])
+    if c["rhs"][0] == "random":
+        rng = np.random.default_rng(seed)
+        rhs = (rng.standard_normal(space.ndof) + 1j * rng.standard_normal(space.ndof)) / np.sqrt(2.0)
+    else:
+        rhs = fem.assemble_rhs(space, fem.GaussianSource(alpha=c["rhs"][1], direction=(0.0, 0.0, 1.0)))
+    coarse = fem.build_edge_space(mesh.build_cube_mesh(c["nc"]), "pec")
+    t0 = time.perf_counter()
+    dec = decomp.build_decomposition(space, c["p"], c["layers"], coarse_space=coarse)
+    t_dec = time.perf_counter() - t0
+    return space, coeffs, np.ascontiguousarray(rhs), dec, t_dec
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_sample(c, space, coeffs, rhs, dec, budget_s=12.0):
+    """Bounded oracle sample on host cores -> extrapolated time-to-solve.
+
+    Times (a) SuperLU factorisation + solves of a few subdomain blocks (the
+    oracle's restatement of the reference's per-subdomain LU, scaled to all
+    subdomains), (b) one SpMV and one coarse solve, (c) the MGS2 Arnoldi
+    step at two basis sizes (linear in m), then sums the full solve at the
+    GPU run's iteration count.
+    """
+    import scipy.sparse as sp
+
+    from oracle import maxwell_oracle as O
+
+    t_start = time.perf_counter()
+    md = {k: getattr(space.mesh, k) for k in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs",
+                                              "boundary_faces")}
+    t0 = time.perf_counter()
+    sysm = O.assemble(md, space.edge_to_dof, space.ndof, coeffs.k, coeffs.xi, eps=coeffs.eps, mu=coeffs.mu,
+                      sigma=coeffs.sigma)
+    t_asm = time.perf_counter() - t0
+    A = sysm["A"]
+    nsub = len(dec.dofs)
+    ks = max(1, min(nsub, 2))
+    fac_times, solve_times = [], []
+    rng = np.random.default_rng(0)
+    for ell in range(ks):
+        a_l = A[dec.dofs[ell]][:, dec.dofs[ell]]
+        t0 = time.perf_counter()
+        f = O._Sparse(a_l)
+        fac_times.append(time.perf_counter() - t0)
+        v = rng.standard_normal(len(dec.dofs[ell])) + 0j
+        t0 = time.perf_counter()
+        f.solve(v)
+        solve_times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    r0 = dec.coarse.R0
+    t0 = time.perf_counter()
+    a0 = (r0 @ A @ r0.T).tocsc()
+    f0 = O._Sparse(a0)
+    t_coarse_fac = time.perf_counter() - t0
+    x = rng.standard_normal(space.ndof) + 1j * rng.standard_normal(space.ndof)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        A @ x
+    t_spmv = (time.perf_counter() - t0) / 3
+    t0 = time.perf_counter()
+    r0.T @ f0.solve(r0 @ x)
+    t_coarse = time.perf_counter() - t0
+
+    def mgs(m):
+        V = [rng.standard_normal(space.ndof) + 0j for _ in range(m)]
+        w = x.copy()
+        t = time.perf_counter()
+        for _ in range(2):
+            for j in range(m):
+                h = np.vdot(V[j], w)
+                w = w - h * V[j]
+        return time.perf_counter() - t
+
+    m1, m2 = 8, 24
+    tm1, tm2 = mgs(m1), mgs(m2)
+    slope = max((tm2 - tm1) / (m2 - m1), 0.0)
+    return {
+        "t_asm": t_asm, "t_fac_sub": float(np.mean(fac_times)), "t_solve_sub": float(np.mean(solve_times)),
+        "t_coarse_fac": t_coarse_fac, "t_coarse": t_coarse, "t_spmv": t_spmv, "mgs_slope": slope,
+        "mgs_icpt": max(tm1 - slope * m1, 0.0), "nsub": nsub, "n_sampled": len(fac_times),
+        "sample_s": time.perf_counter() - t_start,
+    }
+
+
+def cpu_extrapolate(s, iterations):
+    t_fac = 2 * s["t_asm"] + s["nsub"] * s["t_fac_sub"] + s["t_coarse_fac"]
+    t_apply = s["nsub"] * s["t_solve_sub"] + s["t_coarse"]
+    t_it = (iterations + 1) * (t_apply + s["t_spmv"])
+    t_arn = sum(s["mgs_icpt"] + s["mgs_slope"] * m for m in range(1, iterations + 1)) * 1.5  # + drift check
+    return t_fac + t_it + t_arn
+
+
+# ---------------------------------------------------------------- our arm
+def run_mine(args, rank, world):
+    from paper_1711_03789_b200 import _lib, fem, krylov, precond
+
+    c = CONFIGS[args.config]
+    ctx = _lib.get_context()
+    t0 = time.perf_counter()
+    space, coeffs, rhs, dec, t_dec = build_problem(c)
+    n = space.ndof
+    spec = precond.PreconditionerSpec(c["family"], "two", c["corr"], xi_prec=c["xi"])
+    prob = fem.assemble(space, coeffs)
+    t1 = time.perf_counter()
+    st = precond.setup(prob, dec, spec, lu_cap=None)
+    t_setup = time.perf_counter() - t1
+    t_prep = time.perf_counter() - t0
+    stats = st.stats()
+    kcfg = krylov.KrylovConfig(tol=1e-6, maxit=200, side="right", initial_guess="zero")
+    rhs_dev = _lib.DeviceBuffer(ctx, 16 * n)
+    rhs_dev.upload(rhs)
+    x_dev = _lib.DeviceBuffer(ctx, 16 * n)
+    prec_coeffs = coeffs.with_xi(spec.xi_prec)
+
+    def step(device_io=True):
+        p = fem.assemble(space, coeffs)
+        ctx.record(1)
+        a_prec = fem.assemble(space, prec_coeffs).A
+        st.refactor(a_prec, prec_coeffs)
+        ctx.record(2)
+        if device_io:
+            rep = krylov.gmres(p.A, rhs_dev, precond=st, config=kcfg, out=x_dev)
+        else:
+            rep = krylov.gmres(p.A, rhs, precond=st.apply, config=kcfg)
+        return rep
+
+    log(f"[bench] {c['name']}: ndof={n} nsub={len(dec.dofs)} prep {t_prep:.1f}s (decomp {t_dec:.1f}s, "
+        f"setup {t_setup:.1f}s) fronts={stats['n_fronts']:.0f} max_front={stats['max_front']:.0f} "
+        f"factor_entries={stats['factor_entries']:.3e}")
+    for _ in range(args.warmup):
+        step()
+    ctx.set_timing(True)
+    dist_barrier(world)
+    ctx.synchronize()
+    launches0 = ctx.kernel_launches()
+    ms_steps, phases, reps = [], [], []
+    timers = np.zeros(3)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(args.steps):
+            ctx.record(0)
+            rep = step()
+            ctx.record(3)
+            ms = ctx.elapsed_ms(0, 3)
+            ms_steps.append(ms)
+            phases.append((ctx.elapsed_ms(0, 1), ctx.elapsed_ms(1, 2), ctx.elapsed_ms(2, 3)))
+            timers += np.array(ctx.timers()[:3])
+            reps.append(rep)
+    ctx.synchronize()
+    dist_barrier(world)
+    launches = ctx.kernel_launches() - launches0
+    ctx.set_timing(False)
+    ms_step = max_over_ranks(float(np.mean(ms_steps)), world)
+    # e2e through the public API with host buffers
+    e2e_t = []
+    for _ in range(max(1, args.steps)):
+        t = time.perf_counter()
+        rep_e = step(device_io=False)
+        e2e_t.append(time.perf_counter() - t)
+    e2e_s = max_over_ranks(float(np.mean(e2e_t)), world)
+    rep = reps[-1]
+    x = np.empty(n, dtype=np.complex128)
+    x_dev.download(x)
+    its = rep.iterations
+    # roofline of the dominant kernel family
+    t_op, t_prec, t_arn = timers / args.steps
+    fe = stats["factor_entries"]
+    sum_loc = stats["sum_local_dofs"]
+    r0nnz = dec.coarse.R0.nnz
+    b_prec = 16 * fe + 40 * sum_loc + 40 * r0nnz + 48 * n
+    b_arn = sum((32 * m + 16 * m + 64) * n for m in range(1, its + 1))  # 2 MGS passes + drift pass + w
+    b_spmv = (20 * prob.A.nnz + 36 * n) * its
+    peak = read_peaks()
+    cands = {
+        "precond_apply(k_fwd/k_bwd/k_gather/k_scatter_owner)": (b_prec * its, t_prec),
+        "k_arnoldi": (b_arn, t_arn),
+        "k_spmv": (b_spmv, t_op),
+    }
+    dom = max(cands, key=lambda k: cands[k][1])
+    roof_all = {}
+    for k, (b, t) in cands.items():
+        ach = b / (t / 1e3) / 1e9 if t > 0 else 0.0
+        roof_all[k] = {"achieved": ach, "frac": ach / peak["hbm_gbs"], "ms_per_step": t,
+                       "bytes_per_step": b}
+    hist = rep.residual_history
+    res = {
+        "metric": METRIC,
+        "value": world * n / (ms_step / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (seeded; BASELINE.json configs)",
+        "config": {
+            "workload": f"{c['name']}: N={c['N']} ({n} DoFs), k={c['k']}, xi={c['xi']:.4g}, "
+                        f"{c['p']}^3 subdomains, {c['layers']} overlap layers, coarse N={c['nc']}, "
+                        f"{spec.label()}, right GMRES tol 1e-6 maxit 200",
+            "ndof": n, "subdomains": len(dec.dofs), "iterations": its, "converged": bool(rep.converged),
+            "final_rel_residual": float(hist[-1]),
+            "parallelism": "replicas" if world > 1 else "single-gpu",
+            "l2": "working set (V basis, factors) >> 126 MB L2; no flush needed",
+        },
+        "iters_per_s": its / (ms_step / 1e3),
+        "phases_ms": {"assemble_A": float(np.mean([p[0] for p in phases])),
+                      "assemble_Aprec_factor": float(np.mean([p[1] for p in phases])),
+                      "gmres": float(np.mean([p[2] for p in phases])),
+                      "gmres_spmv": t_op, "gmres_precond": t_prec, "gmres_arnoldi": t_arn},
+        "setup_s": {"decomposition": t_dec, "first_setup_incl_symbolic": t_setup},
+        "factor": {k: stats[k] for k in ("n_fronts", "max_front", "factor_entries", "factor_flops", "factor_ms")},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": roof_all[dom]["achieved"], "peak": peak["hbm_gbs"],
+                     "unit": "GB/s", "frac": roof_all[dom]["frac"], "traffic": None,
+                     "peak_source": peak["source"]},
+        "roofline_all": roof_all,
+        "e2e": {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+                "s_per_step": e2e_s, "iterations": rep_e.iterations},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_sample(c, space, coeffs, rhs, dec)
+        t_cpu = cpu_extrapolate(s, its)
+        res["cpu_baseline"] = {"value": n / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
+                               "sample": f"oracle (numpy/SuperLU) on {s['n_sampled']} of {s['nsub']} subdomain "
+                                         f"factorisations+solves, 1 SpMV, 1 coarse solve, MGS2 at m=8,24; "
+                                         f"extrapolated to {its} iterations ({s['sample_s']:.1f}s sampled, "
+                                         f"est. {t_cpu:.0f}s per solve)",
+                               "est_s_per_solve": t_cpu}
+    return res
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference's CPU path (the oracle port: the reference is pure Python and
+    cannot travel to the GPU box) on a bounded sample of the same workload."""
+    c = CONFIGS[args.config]
+    space, coeffs, rhs, dec, _ = build_problem(c)
+    n = space.ndof
+    its = 200 if args.config == 1 else 60
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(c, space, coeffs, rhs, dec, budget_s=8.0)
+        if i >= args.warmup:
+            vals.append(cpu_extrapolate(s, its))
+    t = float(np.mean(vals))
+    return {
+        "metric": METRIC, "impl": "reference", "value": n / t, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded; BASELINE.json configs)",
+        "config": {"workload": f"{c['name']} (same as the GPU arm)", "ndof": n, "iterations_assumed": its},
+        "cpu_baseline": {"value": n / t, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": "oracle restatement of the reference (numpy + SuperLU), bounded sample per step: "
+                                   "2 subdomain factorisations+solves, SpMV, coarse solve, MGS2 timings, "
+                                   "extrapolated to a full solve"},
+        "e2e": {"value": n / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ------------------------------------------------------------ distributed
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world = dist_init()
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    res = run_mine(args, rank, world)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -59,6 +59,13 @@ int64_t mdd_ctx_kernel_launches(const mdd_ctx* ctx);
 /* device-time of the last mdd_gmres phases (ms): [assembly-free] spmv, precond, arnoldi */
 int mdd_ctx_timers(const mdd_ctx* ctx, double* out6);
 int mdd_ctx_set_timing(mdd_ctx* ctx, int enable);
+/* CUDA events on the context stream (slot 0..15) for device-side timing */
+int mdd_ctx_event_record(mdd_ctx* ctx, int slot);
+int mdd_ctx_event_elapsed(mdd_ctx* ctx, int slot0, int slot1, double* ms);
+/* device buffers (plumbing for device-resident benchmark inputs) */
+int mdd_dev_alloc(mdd_ctx* ctx, int64_t bytes, void** out);
+int mdd_dev_free(mdd_ctx* ctx, void* p);
+int mdd_memcpy(mdd_ctx* ctx, void* dst, const void* src, int64_t bytes, int kind /*1 h2d, 2 d2h, 3 d2d*/);
 
 /* ------------------------------------------------------------ CSR matrices
  * Replaces scipy.sparse CSR storage + linalg.spmv (reference linalg.py:41-45)
@@ -188,6 +195,7 @@ typedef struct {
   int32_t side;          /* 0 right, 1 left                                   */
   int32_t check_drift;   /* 1: compute the orthogonality drift (krylov.py:152) */
   int32_t keep_basis;
+  int32_t device_io;     /* 1: b, x0, x are device pointers (no H2D/D2H)      */
 } mdd_gmres_cfg;
 
 typedef struct {

@@ -77,6 +77,7 @@ class mdd_gmres_cfg(C.Structure):
         ("side", C.c_int32),
         ("check_drift", C.c_int32),
         ("keep_basis", C.c_int32),
+        ("device_io", C.c_int32),
     ]
 
 
@@ -113,6 +114,11 @@ SIGNATURES = {
     "mdd_ctx_kernel_launches": (C.c_int64, [_P]),
     "mdd_ctx_timers": (C.c_int, [_P, _pd]),
     "mdd_ctx_set_timing": (C.c_int, [_P, C.c_int]),
+    "mdd_ctx_event_record": (C.c_int, [_P, C.c_int]),
+    "mdd_ctx_event_elapsed": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
+    "mdd_dev_alloc": (C.c_int, [_P, _i64, _PP]),
+    "mdd_dev_free": (C.c_int, [_P, C.c_void_p]),
+    "mdd_memcpy": (C.c_int, [_P, C.c_void_p, C.c_void_p, _i64, C.c_int]),
     "mdd_csr_from_host": (C.c_int, [_P, _i64, _i64, _i64, _pi32, _pi32, C.c_void_p, C.c_int, _PP]),
     "mdd_csr_info": (C.c_int, [_P, _pi64, _pi64, _pi64, C.POINTER(C.c_int)]),
     "mdd_csr_to_host": (C.c_int, [_P, _pi32, _pi32, C.c_void_p]),
@@ -217,6 +223,14 @@ class Context:
     def set_timing(self, on: bool):
         check(lib.mdd_ctx_set_timing(self.handle, 1 if on else 0))
 
+    def record(self, slot: int):
+        check(lib.mdd_ctx_event_record(self.handle, slot))
+
+    def elapsed_ms(self, s0: int, s1: int) -> float:
+        ms = C.c_double()
+        check(lib.mdd_ctx_event_elapsed(self.handle, s0, s1, C.byref(ms)))
+        return ms.value
+
     def timers(self):
         out = (C.c_double * 6)()
         check(lib.mdd_ctx_timers(self.handle, out))
@@ -246,6 +260,31 @@ def get_context() -> Context:
         if _ctx is None:
             _ctx = Context(int(os.environ.get("MDD_DEVICE", os.environ.get("LOCAL_RANK", "0"))))
         return _ctx
+
+
+class DeviceBuffer:
+    """Raw device allocation (benchmark plumbing: device-resident inputs)."""
+
+    def __init__(self, ctx: Context, nbytes: int):
+        self.ctx = ctx
+        self.nbytes = int(nbytes)
+        p = C.c_void_p()
+        check(lib.mdd_dev_alloc(ctx.handle, self.nbytes, C.byref(p)))
+        self.ptr = p
+
+    def upload(self, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        check(lib.mdd_memcpy(self.ctx.handle, self.ptr, a.ctypes.data_as(C.c_void_p), a.nbytes, 1))
+
+    def download(self, a: np.ndarray):
+        check(lib.mdd_memcpy(self.ctx.handle, a.ctypes.data_as(C.c_void_p), self.ptr, a.nbytes, 2))
+        return a
+
+    def __del__(self):
+        p = getattr(self, "ptr", None)
+        if p:
+            lib.mdd_dev_free(self.ctx.handle, p)
+            self.ptr = None
 
 
 def exported_symbols():

@@ -191,6 +191,8 @@ void mdd_ctx_destroy(mdd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->events)
+    if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -213,6 +215,50 @@ int mdd_ctx_timers(const mdd_ctx* ctx, double* out6) {
 int mdd_ctx_set_timing(mdd_ctx* ctx, int enable) {
   MDD_API_BEGIN
   ctx->timing = enable != 0;
+  MDD_API_END
+}
+
+int mdd_ctx_event_record(mdd_ctx* ctx, int slot) {
+  MDD_API_BEGIN
+  if (slot < 0 || slot >= 16) fail(MDD_EINVAL, "event slot out of range");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->events[slot]) CK(cudaEventCreate(&ctx->events[slot]));
+  CK(cudaEventRecord(ctx->events[slot], ctx->stream));
+  MDD_API_END
+}
+
+int mdd_ctx_event_elapsed(mdd_ctx* ctx, int s0, int s1, double* ms) {
+  MDD_API_BEGIN
+  if (s0 < 0 || s0 >= 16 || s1 < 0 || s1 >= 16 || !ctx->events[s0] || !ctx->events[s1])
+    fail(MDD_EINVAL, "event slot not recorded");
+  CK(cudaEventSynchronize(ctx->events[s1]));
+  float f = 0;
+  CK(cudaEventElapsedTime(&f, ctx->events[s0], ctx->events[s1]));
+  *ms = f;
+  MDD_API_END
+}
+
+int mdd_dev_alloc(mdd_ctx* ctx, int64_t bytes, void** out) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMalloc(out, bytes > 0 ? (size_t)bytes : 16));
+  MDD_API_END
+}
+
+int mdd_dev_free(mdd_ctx* ctx, void* p) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  if (p) CK(cudaFree(p));
+  MDD_API_END
+}
+
+int mdd_memcpy(mdd_ctx* ctx, void* dst, const void* src, int64_t bytes, int kind) {
+  MDD_API_BEGIN
+  CK(cudaSetDevice(ctx->device));
+  const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CK(cudaMemcpyAsync(dst, src, (size_t)bytes, k, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   MDD_API_END
 }
 

@@ -343,8 +343,17 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     DV.alloc((size_t)(maxit + 1) * n);
     dr.alloc(n);
   }
-  db.upload(reinterpret_cast<const double2*>(b), n, s);
-  if (x0) dx0.upload(reinterpret_cast<const double2*>(x0), n, s);
+  const bool dio = cfg->device_io != 0;
+  if (dio) {
+    CK(cudaMemcpyAsync(db.p, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+    if (x0) {
+      dx0.alloc(n);
+      CK(cudaMemcpyAsync(dx0.p, x0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
+    db.upload(reinterpret_cast<const double2*>(b), n, s);
+    if (x0) dx0.upload(reinterpret_cast<const double2*>(x0), n, s);
+  }
 
   // r0 (krylov.py:94-106)
   if (x0) {
@@ -388,8 +397,15 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   CK(cudaStreamSynchronize(s));
   if (beta == 0.0) {
     // zero residual: 0 iterations (krylov.py:110-118)
-    if (x0) memcpy(x, x0, sizeof(mdd_complex) * n);
-    else memset(x, 0, sizeof(mdd_complex) * n);
+    if (dio) {
+      if (x0) CK(cudaMemcpyAsync(x, x0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+      else CK(cudaMemsetAsync(x, 0, sizeof(double2) * n, s));
+      CK(cudaStreamSynchronize(s));
+    } else if (x0) {
+      memcpy(x, x0, sizeof(mdd_complex) * n);
+    } else {
+      memset(x, 0, sizeof(mdd_complex) * n);
+    }
     history[0] = 0.0;
     *iterations = 0;
     *converged = 1;
@@ -476,11 +492,12 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     op.M(t.p, z.p);
     upd = z.p;
   }
-  DevBuf<double2> dxo(n);
+  DevBuf<double2> dxo(dio ? 0 : n);
+  double2* xout = dio ? reinterpret_cast<double2*>(x) : dxo.p;
   k_axpy_out<<<std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 8192)), 256, 0,
-               s>>>(n, x0 ? dx0.p : nullptr, upd, dxo.p);
+               s>>>(n, x0 ? dx0.p : nullptr, upd, xout);
   CK_LAUNCH(ctx);
-  dxo.download(reinterpret_cast<double2*>(x), n, s);
+  if (!dio) dxo.download(reinterpret_cast<double2*>(x), n, s);
   hist.download(history, m + 1, s);
   if (drift) ddrift.download(drift, m + 1, s);
   if (basis) {

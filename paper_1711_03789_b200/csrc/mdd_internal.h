@@ -120,6 +120,7 @@ struct mdd_ctx {
   // pinned staging used by host-pointer entry points
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  cudaEvent_t events[16] = {};
   void* pinned_buf(size_t bytes);
 };
 

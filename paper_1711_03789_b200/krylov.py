@@ -100,11 +100,25 @@ class _HostOp:
             return 1
 
 
-def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None) -> KrylovReport:
-    """Solve ``operator x = rhs`` by (weighted) GMRES (reference krylov.py:64-209)."""
+def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, out=None) -> KrylovReport:
+    """Solve ``operator x = rhs`` by (weighted) GMRES (reference krylov.py:64-209).
+
+    ``rhs`` may also be a device-resident :class:`_lib.DeviceBuffer` (then
+    ``out`` must be one too and ``report.x`` is ``out``): the benchmark's
+    HBM-resident path, with no host<->device copies of the vectors.
+    """
     cfg = config if config is not None else KrylovConfig()
-    b = np.ascontiguousarray(np.asarray(rhs, dtype=complex).reshape(-1))
-    n = b.shape[0]
+    dio = isinstance(rhs, _lib.DeviceBuffer)
+    if dio:
+        if not isinstance(out, _lib.DeviceBuffer):
+            raise ValueError("device-resident rhs needs a device-resident `out`")
+        n = rhs.nbytes // 16
+        if cfg.initial_guess != "zero":
+            raise ValueError("device-resident solve supports initial_guess='zero' only")
+        b = None
+    else:
+        b = np.ascontiguousarray(np.asarray(rhs, dtype=complex).reshape(-1))
+        n = b.shape[0]
     ctx = _lib.get_context()
     keep = []
     ops = _lib.mdd_gmres_ops()
@@ -155,17 +169,19 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None) -> Kr
     c.side = 0 if cfg.side == "right" else 1
     c.check_drift = 1 if cfg.check_orthogonality else 0
     c.keep_basis = 1 if cfg.keep_basis else 0
-    x = np.empty(n, dtype=np.complex128)
+    c.device_io = 1 if dio else 0
+    x = out if dio else np.empty(n, dtype=np.complex128)
     hist = np.empty(cfg.maxit + 1, dtype=np.float64)
     drift = np.full(cfg.maxit + 1, np.nan)
     basis = np.empty((cfg.maxit + 1, n), dtype=np.complex128) if cfg.keep_basis else None
     its, conv, secs = C.c_int32(), C.c_int32(), C.c_double()
+    zp = (lambda buf: C.cast(buf.ptr, C.POINTER(_lib.mdd_complex))) if dio else _lib.zptr
     try:
         _lib.check(
             _lib.lib.mdd_gmres(
-                ctx.handle, C.byref(ops), n, _lib.zptr(b),
+                ctx.handle, C.byref(ops), n, zp(rhs if dio else b),
                 _lib.zptr(x0) if x0 is not None else C.POINTER(_lib.mdd_complex)(),
-                C.byref(c), _lib.zptr(x), _lib.ptr(hist, C.c_double), _lib.ptr(drift, C.c_double),
+                C.byref(c), zp(x), _lib.ptr(hist, C.c_double), _lib.ptr(drift, C.c_double),
                 _lib.zptr(basis) if basis is not None else C.POINTER(_lib.mdd_complex)(),
                 C.byref(its), C.byref(conv), C.byref(secs),
             )
