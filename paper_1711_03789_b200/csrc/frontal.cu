@@ -216,6 +216,39 @@ __global__ void k_pivinit(double* p, int64_t n) {
   }
 }
 
+// Dot products of up to 4 consecutive front rows (row0 + k*ld) with z[0..len)
+// held in shared memory: 4 independent FMA chains and 2-way unrolling keep 8
+// streaming loads in flight per lane; the z operand is loaded once for all
+// rows.  Factor data are read exactly once per apply (>> L2): streaming loads.
+__device__ __forceinline__ void dot_rows4(const double2* __restrict__ row0, int64_t ld, int nr,
+                                          int len, const double2* __restrict__ z, int lane,
+                                          double2 (&out)[4]) {
+  double2 acc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = make_double2(0.0, 0.0);
+  int q = lane;
+  for (; q + 32 < len; q += 64) {
+    const double2 z0 = z[q], z1 = z[q + 32];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < nr) {
+        const double2 t0 = __ldcs(row0 + k * ld + q);
+        const double2 t1 = __ldcs(row0 + k * ld + q + 32);
+        acc[k] = cfma(t0, z0, acc[k]);
+        acc[k] = cfma(t1, z1, acc[k]);
+      }
+    }
+  }
+  if (q < len) {
+    const double2 z0 = z[q];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < nr) acc[k] = cfma(__ldcs(row0 + k * ld + q), z0, acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = warp_sum2(acc[k]);
+}
+
 // forward: fp = b_P + children contributions ; uvec = (children contributions)_U - F_UP fp
 __global__ void __launch_bounds__(256) k_fwd(const int2* __restrict__ tasks,
                                              const NodeDev* __restrict__ nodes,
@@ -241,21 +274,20 @@ __global__ void __launch_bounds__(256) k_fwd(const int2* __restrict__ tasks,
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int rr = wid; rr < kSolveRows; rr += blockDim.x >> 5) {
-    const int u = r0 + rr;
-    if (u >= nd.nu) break;
-    const double2* row = fronts + nd.front_off + (int64_t)(np + u) * m;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = lane; q < np; q += 32) acc = cfma(row[q], fp[q], acc);
-    acc = warp_sum2(acc);
-    if (lane == 0) {
-      double2 fu = make_double2(0.0, 0.0);
-      for (int ci = 0; ci < nd.nch; ++ci) {
-        const int g = gmap[nd.gmap_off + (int64_t)ci * m + np + u];
-        if (g >= 0) fu = cadd(fu, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
-      }
-      uvec[nd.uvec_off + u] = csub(fu, acc);
+  const int u0 = r0 + wid * 4;
+  const int nr = min(4, nd.nu - u0);
+  if (nr <= 0) return;
+  double2 d[4];
+  dot_rows4(fronts + nd.front_off + (int64_t)(np + u0) * m, m, nr, np, fp, lane, d);
+  if (lane < nr) {
+    const int u = u0 + lane;
+    double2 fu = make_double2(0.0, 0.0);
+    for (int ci = 0; ci < nd.nch; ++ci) {
+      const int g = gmap[nd.gmap_off + (int64_t)ci * m + np + u];
+      if (g >= 0) fu = cadd(fu, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
     }
+    const double2 acc = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
+    uvec[nd.uvec_off + u] = csub(fu, acc);
   }
 }
 
@@ -276,14 +308,14 @@ __global__ void __launch_bounds__(256) k_bwd(const int2* __restrict__ tasks,
     z[q] = q < np ? fpst[base + q] : xloc[(int64_t)nd.mat_off + upd[nd.upd_off + q - np]];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int rr = wid; rr < kSolveRows; rr += blockDim.x >> 5) {
-    const int i = r0 + rr;
-    if (i >= np) break;
-    const double2* row = fronts + nd.front_off + (int64_t)i * m;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = lane; q < m; q += 32) acc = cfma(row[q], z[q], acc);
-    acc = warp_sum2(acc);
-    if (lane == 0) xloc[base + i] = cneg(acc);
+  const int i0 = r0 + wid * 4;
+  const int nr = min(4, np - i0);
+  if (nr <= 0) return;
+  double2 d[4];
+  dot_rows4(fronts + nd.front_off + (int64_t)i0 * m, m, nr, m, z, lane, d);
+  if (lane < nr) {
+    const double2 acc = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
+    xloc[base + i0 + lane] = cneg(acc);
   }
 }
 

@@ -1,21 +1,31 @@
 // Unrestarted GMRES on the device (reference krylov.gmres, krylov.py:64-209).
 //
-// One iteration = operator/preconditioner kernels + ONE cooperative
-// persistent Arnoldi kernel that performs, exactly in the reference order
-// (krylov.py:134-187):
-//   2 passes x m modified Gram-Schmidt steps  h_j = <V_j, dw>, col[j] += h_j,
-//       w -= h_j V_j, dw -= h_j DV_j          (krylov.py:137-143)
-//   hnorm2 = Re vdot(w, dw), breakdown test, normalisation (krylov.py:144-151)
-//   orthogonality drift max_j |vdot(V_j, DV_m)|               (krylov.py:153)
-//   stored + new complex Givens rotations, history clamp     (krylov.py:162-187)
-// Each MGS step costs one grid barrier: the axpy of step j and the partial
-// dot of step j+1 are fused into one sweep over the CTA's slice, so w is read
-// and written once per step and V_j once (the slice of V_j is L2-resident for
-// the axpy).  Cross-CTA sums use a fixed order: reruns are bitwise identical.
+// The whole Arnoldi loop runs on the GPU: one iteration (preconditioner
+// kernels, SpMV, optional weight SpMV, Arnoldi kernel) is captured once into
+// the body of a CUDA-graph conditional WHILE node; the Arnoldi kernel clears
+// the condition on convergence / happy breakdown / maxit, so there is no host
+// round trip per iteration.  (A host-driven loop with per-phase CUDA events
+// is kept for `ctx->timing` and for Python-callable operators.)
+//
+// The Arnoldi kernel is a persistent cooperative kernel, one CTA per SM; each
+// CTA owns a contiguous slice of the vectors.  It performs, in the reference
+// order (krylov.py:134-187):
+//   2 passes x m MGS steps  h_j = <V_j, dw>; col[j] += h_j; w -= h_j V_j;
+//       dw -= h_j DV_j                                      (krylov.py:137-143)
+//   hnorm2 = Re vdot(w, dw), breakdown test, normalisation  (krylov.py:144-151)
+//   complex Givens rotations + history clamp                (krylov.py:162-187)
+// One grid barrier per MGS step: the axpy of step j and the partial dot of
+// step j+1 are one fused sweep, and the slice needed at step j+2 is prefetched
+// into L2 with a TMA bulk prefetch while the CTA waits at the barrier.  The
+// orthogonality drift of the vector appended by the previous iteration
+// (krylov.py:152-160) rides along in the first MGS pass (it needs the same
+// V_j reads), so it costs no extra pass over the basis.  Cross-CTA sums use a
+// fixed order: reruns are bitwise identical.
 #include <cooperative_groups.h>
 
 #include <chrono>
 #include <cmath>
+#include <cstring>
 
 #include "mdd_internal.h"
 #include "mdd_kernels.cuh"
@@ -26,83 +36,151 @@ namespace mdd {
 
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 
+constexpr int kArnThreads = 512;
+
 struct ArnoldiArgs {
   int64_t n;
-  int m;      // iteration (1-based); w = V[m]
+  int64_t slice;   // elements per CTA
   int maxit;
-  double2* V;   // (maxit+1) x n
-  double2* DV;  // weighted basis or nullptr (then dw == w)
-  double2* partials;  // 2*G
-  double2* dpart;     // maxit*G (drift partials)
-  double2* H;         // (maxit+1) x maxit, column j at H + j*(maxit+1)
+  double2* V;      // (maxit+1) x n
+  double2* DV;     // weighted basis or nullptr
+  double2* w;      // new direction (input: operator output)
+  double2* dw;     // D w (weighted) or nullptr
+  double2* vin;    // out: copy of V[m] = next operator input
+  double2* partials;  // 2 (parity) x 2 (dot, drift) x G
+  double2* H;      // (maxit+1) x maxit, column j at H + j*(maxit+1)
   double2* cs;
   double2* sn;
   double2* g;
-  double* hist;       // maxit+1
-  double* drift;      // maxit+1 (nan when not computed)
+  double* hist;
+  double* drift;
   const double* beta;
   double tol;
   int check_drift;
-  volatile int* status;  // [done, breakdown, iterations] (host-mapped)
+  int* iter;             // device: completed iterations
+  int* dstatus;          // device: [done, breakdown, iterations]
+  volatile int* hstatus; // host-mapped copy (host loop) or nullptr
+  cudaGraphConditionalHandle cond;
+  int use_cond;
 };
 
-// Deterministic sum of partials[0..G) (all threads of the CTA get it).
-__device__ __forceinline__ double2 reduce_partials(const double2* p, int G, double2* sh) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double2 a = make_double2(0.0, 0.0);
-    for (int b = threadIdx.x; b < G; b += 32) {
-      const double2 v = __ldcg(p + b);
-      a.x += v.x;
-      a.y += v.y;
-    }
-    a = warp_sum2(a);
-    if (threadIdx.x == 0) sh[0] = a;
-  }
-  __syncthreads();
-  return sh[0];
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  bytes &= ~(int64_t)15;
+  if (bytes <= 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_arnoldi(ArnoldiArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ double2 col[];  // m+1 entries, identical in every CTA
-  __shared__ double2 red[8];
-  __shared__ double2 bcast[1];
-  const int G = gridDim.x;
-  const int64_t n = a.n;
-  const int m = a.m;
-  const int64_t stride = (int64_t)G * blockDim.x;
-  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double2* w = a.V + (int64_t)m * n;
-  double2* dw = a.DV ? a.DV + (int64_t)m * n : w;
-  const bool weighted = a.DV != nullptr;
+// two complex block sums at once (all threads receive both)
+__device__ __forceinline__ void block_sum2x2(double2& a, double2& b, double2* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  a = warp_sum2(a);
+  b = warp_sum2(b);
+  __syncthreads();
+  if (lane == 0) {
+    sh[2 * wid] = a;
+    sh[2 * wid + 1] = b;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double2 x = lane < nw ? sh[2 * lane] : make_double2(0.0, 0.0);
+    double2 y = lane < nw ? sh[2 * lane + 1] : make_double2(0.0, 0.0);
+    x = warp_sum2(x);
+    y = warp_sum2(y);
+    if (lane == 0) {
+      sh[64] = x;
+      sh[65] = y;
+    }
+  }
+  __syncthreads();
+  a = sh[64];
+  b = sh[65];
+}
 
+// deterministic sums of the G partials of one step (dot and drift)
+__device__ __forceinline__ void reduce_step(const double2* p, int G, double2* sh, double2& dot,
+                                            double2& dr) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < G; k += 32) {
+      const double2 u = __ldcg(p + k), v = __ldcg(p + G + k);
+      a.x += u.x;
+      a.y += u.y;
+      b.x += v.x;
+      b.y += v.y;
+    }
+    a = warp_sum2(a);
+    b = warp_sum2(b);
+    if (threadIdx.x == 0) {
+      sh[66] = a;
+      sh[67] = b;
+    }
+  }
+  __syncthreads();
+  dot = sh[66];
+  dr = sh[67];
+}
+
+__global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 col[];  // m+1, identical in every CTA
+  __shared__ double2 red[68];
+  const int G = gridDim.x;
+  const int m = *a.iter + 1;
+  const int64_t n = a.n;
+  const int64_t lo = (int64_t)blockIdx.x * a.slice;
+  const int64_t hi = min(n, lo + a.slice);
+  const int64_t len = hi > lo ? hi - lo : 0;
+  const bool weighted = a.DV != nullptr;
+  double2* w = a.w;
+  double2* dw = weighted ? a.dw : a.w;
+  // drift of V_{m-1} against V_j, j < m-1 (needs m >= 2)
+  const bool do_drift = a.check_drift && m >= 2;
+  const double2* dvm1 = (weighted ? a.DV : a.V) + (int64_t)(m - 1) * n;
   for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
 
-  // first partial: <V_0, dw>
+  // step -1: partials of <V_0, dw> (+ <V_0, DV_{m-1}>)
+  if (threadIdx.x == 0) prefetch_l2(a.V + (m > 1 ? n : 0) + lo, len * 16);
   {
-    const double2* v0 = a.V;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t i = tid0; i < n; i += stride) {
-      const double2 x = v0[i], y = dw[i];
+    double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const double2 x = a.V[i], y = dw[i];
       acc.x += x.x * y.x + x.y * y.y;
       acc.y += x.x * y.y - x.y * y.x;
+      if (do_drift) {
+        const double2 z = dvm1[i];
+        dacc.x += x.x * z.x + x.y * z.y;
+        dacc.y += x.x * z.y - x.y * z.x;
+      }
     }
-    acc = block_sum2(acc, red);
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = acc;
+    block_sum2x2(acc, dacc, red);
+    if (threadIdx.x == 0) {
+      a.partials[blockIdx.x] = acc;
+      a.partials[G + blockIdx.x] = dacc;
+    }
   }
   grid.sync();
+  double dmax = 0.0;
   const int nsteps = 2 * m;
   for (int s = 0; s < nsteps; ++s) {
     const int j = s % m;
-    const double2 h = reduce_partials(a.partials + (s & 1) * G, G, bcast);
-    if (threadIdx.x == 0) col[j] = cadd(col[j], h);
+    double2 h, d;
+    reduce_step(a.partials + (s & 1) * 2 * G, G, red, h, d);
+    // the drift term reduced here belongs to V_j (dotted at step s-1), j < m-1
+    if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
+    if (threadIdx.x == 0) {
+      col[j] = cadd(col[j], h);
+      // L2 prefetch of the slice dotted at step s+1
+      if (s + 2 < nsteps) prefetch_l2(a.V + (int64_t)((s + 2) % m) * n + lo, len * 16);
+    }
     const double2* vj = a.V + (int64_t)j * n;
     const double2* dvj = weighted ? a.DV + (int64_t)j * n : nullptr;
     const bool last = (s + 1 == nsteps);
-    const double2* vn = last ? w : a.V + (int64_t)((s + 1) % m) * n;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t i = tid0; i < n; i += stride) {
+    const int jn = (s + 1) % m;
+    const double2* vn = last ? w : a.V + (int64_t)jn * n;
+    const bool drift_next = do_drift && s + 1 < m - 1;  // next vector is V_{s+1}, s+1 < m-1
+    double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const double2 v = vj[i];
       double2 wi = w[i];
       wi = make_double2(wi.x - (h.x * v.x - h.y * v.y), wi.y - (h.x * v.y + h.y * v.x));
@@ -117,13 +195,23 @@ __global__ void __launch_bounds__(256) k_arnoldi(ArnoldiArgs a) {
       const double2 x = last ? wi : vn[i];
       acc.x += x.x * dwi.x + x.y * dwi.y;
       acc.y += x.x * dwi.y - x.y * dwi.x;
+      if (drift_next) {
+        const double2 z = dvm1[i];
+        dacc.x += x.x * z.x + x.y * z.y;
+        dacc.y += x.x * z.y - x.y * z.x;
+      }
     }
-    acc = block_sum2(acc, red);
-    if (threadIdx.x == 0) a.partials[((s + 1) & 1) * G + blockIdx.x] = acc;
+    block_sum2x2(acc, dacc, red);
+    if (threadIdx.x == 0) {
+      double2* p = a.partials + ((s + 1) & 1) * 2 * G;
+      p[blockIdx.x] = acc;
+      p[G + blockIdx.x] = dacc;
+    }
     grid.sync();
   }
-  const double hnorm2 = reduce_partials(a.partials + (nsteps & 1) * G, G, bcast).x;
-  const double hlast = sqrt(fmax(hnorm2, 0.0));
+  double2 hn2, dummy;
+  reduce_step(a.partials + (nsteps & 1) * 2 * G, G, red, hn2, dummy);
+  const double hlast = sqrt(fmax(hn2.x, 0.0));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
   __syncthreads();
@@ -131,55 +219,22 @@ __global__ void __launch_bounds__(256) k_arnoldi(ArnoldiArgs a) {
   for (int j = 0; j <= m; ++j) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
   const bool breakdown = hlast <= 1e-13 * cmax;
   if (!breakdown) {
-    for (int64_t i = tid0; i < n; i += stride) {
+    double2* vm = a.V + (int64_t)m * n;
+    double2* dvm = weighted ? a.DV + (int64_t)m * n : nullptr;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const double2 wi = w[i];
-      w[i] = make_double2(wi.x / hlast, wi.y / hlast);
+      const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
+      vm[i] = q;
+      a.vin[i] = q;
       if (weighted) {
         const double2 d = dw[i];
-        dw[i] = make_double2(d.x / hlast, d.y / hlast);
+        dvm[i] = make_double2(d.x / hlast, d.y / hlast);
       }
-    }
-    if (a.check_drift) {
-      // partial vdot(V_j, DV_m) for all j < m over this thread's slice
-      for (int j = 0; j < m; ++j) {
-        const double2* vj = a.V + (int64_t)j * n;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int64_t i = tid0; i < n; i += stride) {
-          const double2 x = vj[i], y = dw[i];
-          acc.x += x.x * y.x + x.y * y.y;
-          acc.y += x.x * y.y - x.y * y.x;
-        }
-        acc = block_sum2(acc, red);
-        if (threadIdx.x == 0) a.dpart[(int64_t)j * G + blockIdx.x] = acc;
-      }
-      grid.sync();
     }
   }
-  if (blockIdx.x != 0) return;
-  // ---- CTA 0: drift reduction + Givens (krylov.py:153, 162-187) ----
-  if (!breakdown && a.check_drift) {
-    double dmax = 0.0;
-    for (int j = threadIdx.x >> 5; j < m; j += blockDim.x >> 5) {
-      double2 s2 = make_double2(0.0, 0.0);
-      for (int b = threadIdx.x & 31; b < G; b += 32) {
-        const double2 v = __ldcg(a.dpart + (int64_t)j * G + b);
-        s2.x += v.x;
-        s2.y += v.y;
-      }
-      s2 = warp_sum2(s2);
-      dmax = fmax(dmax, hypot(s2.x, s2.y));
-    }
-    dmax = warp_max(dmax);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5].x = dmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double d = 0.0;
-      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) d = fmax(d, red[k].x);
-      a.drift[m] = d;
-    }
-  }
-  if (threadIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  // ---- Givens (CTA 0, one thread) ----
+  if (do_drift) a.drift[m - 1] = dmax;
   for (int j = 0; j < m - 1; ++j) {
     const double2 csj = a.cs[j], snj = a.sn[j];
     const double2 t = cadd(cmul(csj, col[j]), cmul(snj, col[j + 1]));
@@ -212,17 +267,46 @@ __global__ void __launch_bounds__(256) k_arnoldi(ArnoldiArgs a) {
   const double rel = fmin(hypot(a.g[m].x, a.g[m].y) / *a.beta, a.hist[m - 1]);
   a.hist[m] = rel;
   const int done = (breakdown || rel <= a.tol) ? 1 : 0;
-  a.status[1] = breakdown ? 1 : 0;
-  a.status[2] = m;
-  __threadfence_system();
-  a.status[0] = done;
-  __threadfence_system();
+  *a.iter = m;
+  a.dstatus[0] = done;
+  a.dstatus[1] = breakdown ? 1 : 0;
+  a.dstatus[2] = m;
+  if (a.hstatus) {
+    a.hstatus[1] = breakdown ? 1 : 0;
+    a.hstatus[2] = m;
+    __threadfence_system();
+    a.hstatus[0] = done;
+    __threadfence_system();
+  }
+  if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
 }
 
-// beta = sqrt(Re vdot(r, dr)); V0 = r/beta, DV0 = dr/beta, g[0]=beta, hist[0]=1
+// drift of the final basis vector V_m: |vdot(V_j, DV_m)| for j < m (one CTA per j)
+__global__ void k_final_drift(int64_t n, int m, const double2* V, const double2* DVm, double* out) {
+  __shared__ double2 red[32];
+  const int j = blockIdx.x;
+  const double2* vj = V + (int64_t)j * n;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double2 x = vj[i], y = DVm[i];
+    acc.x += x.x * y.x + x.y * y.y;
+    acc.y += x.x * y.y - x.y * y.x;
+  }
+  acc = block_sum2(acc, red);
+  if (threadIdx.x == 0) out[j] = hypot(acc.x, acc.y);
+}
+
+__global__ void k_max_into(const double* v, int m, double* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double d = 0.0;
+  for (int j = 0; j < m; ++j) d = fmax(d, v[j]);
+  *out = d;
+}
+
+// phase 0: beta = sqrt(Re vdot(r, dr)), g[0]=beta, hist[0]=1 ; phase 1: V0 = r/beta (+DV0, vin)
 __global__ void k_init_basis(int64_t n, const double2* r, const double2* dr, double2* V0,
-                             double2* DV0, double* beta_out, double2* g, double* hist,
-                             double2* part, int phase) {
+                             double2* DV0, double2* vin, double* beta_out, double2* g, double* hist,
+                             int phase) {
   __shared__ double2 red[32];
   if (phase == 0) {
     double2 acc = make_double2(0.0, 0.0);
@@ -244,7 +328,9 @@ __global__ void k_init_basis(int64_t n, const double2* r, const double2* dr, dou
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double2 x = r[i];
-    V0[i] = make_double2(x.x / beta, x.y / beta);
+    const double2 q = make_double2(x.x / beta, x.y / beta);
+    V0[i] = q;
+    vin[i] = q;
     if (DV0) {
       const double2 d = dr[i];
       DV0[i] = make_double2(d.x / beta, d.y / beta);
@@ -287,6 +373,7 @@ struct OpRunner {
   cudaStream_t s;
   mdd_complex* hin = nullptr;
   mdd_complex* hout = nullptr;
+  bool host_ops() const { return ops->a_fn || ops->m_fn; }
   void host_call(mdd_host_op fn, void* user, const double2* in, double2* out) {
     CK(cudaMemcpyAsync(hin, in, sizeof(double2) * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -305,6 +392,10 @@ struct OpRunner {
     else host_call(ops->m_fn, ops->m_user, in, out);
   }
 };
+
+static unsigned gs_grid(int64_t n) {
+  return std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 8192));
+}
 
 }  // namespace mdd
 
@@ -325,7 +416,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (ops->A && (ops->A->nrow() != n || ops->A->ncol() != n))
     fail(MDD_EINVAL, "gmres: operator dimension mismatch");
   OpRunner op{ctx, ops, n, s};
-  if (ops->a_fn || ops->m_fn) {
+  if (op.host_ops()) {
     CK(cudaMallocHost(&op.hin, sizeof(double2) * (n ? n : 1)));
     CK(cudaMallocHost(&op.hout, sizeof(double2) * (n ? n : 1)));
   }
@@ -338,12 +429,13 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   } hf{op};
   const bool weighted = ops->D != nullptr;
   const bool right = cfg->side == 0;
-  DevBuf<double2> V((size_t)(maxit + 1) * n), DV, db(n), dx0, r(n), dr, z(n), t(n);
+  const bool dio = cfg->device_io != 0;
+  DevBuf<double2> V((size_t)(maxit + 1) * n), DV, db(n), dx0, r(n), dr, z(n), t(n), w(n), dw, vin(n);
   if (weighted) {
     DV.alloc((size_t)(maxit + 1) * n);
     dr.alloc(n);
+    dw.alloc(n);
   }
-  const bool dio = cfg->device_io != 0;
   if (dio) {
     CK(cudaMemcpyAsync(db.p, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
     if (x0) {
@@ -354,7 +446,6 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     db.upload(reinterpret_cast<const double2*>(b), n, s);
     if (x0) dx0.upload(reinterpret_cast<const double2*>(x0), n, s);
   }
-
   // r0 (krylov.py:94-106)
   if (x0) {
     op.A(dx0.p, t.p);
@@ -369,34 +460,25 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (weighted) spmv_dev(ctx, ops->D, r.p, dr.p, s);
 
   DevBuf<double2> H((size_t)(maxit + 1) * maxit), cs(maxit), sn(maxit), g(maxit + 1), y(maxit);
-  DevBuf<double> hist(maxit + 1), dbeta(1), ddrift(maxit + 1);
+  DevBuf<double> hist(maxit + 1), dbeta(1), ddrift(maxit + 1), dtmp(maxit + 1);
+  DevBuf<int> diter(1), dstat(4);
   H.zero(s);
   cs.zero(s);
   sn.zero(s);
   g.zero(s);
+  diter.zero(s);
+  dstat.zero(s);
   {
     std::vector<double> nanv(maxit + 1, NAN);
     ddrift.upload(nanv, s);
   }
-  // grid for the cooperative kernel
-  const int bs = 256;
-  int per_sm = 0;
-  const size_t shmem = sizeof(double2) * (maxit + 1);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi, bs, shmem));
-  if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
-  int G = ctx->nsm * std::min(per_sm, 4);
-  const int64_t need = (n + bs - 1) / bs;
-  if (need < G) G = (int)std::max<int64_t>(1, need);
-  DevBuf<double2> partials(2 * G), dpart(cfg->check_drift ? (size_t)maxit * G : 1);
-
-  k_init_basis<<<1, 1024, 0, s>>>(n, r.p, weighted ? dr.p : r.p, V.p, nullptr, dbeta.p, g.p,
-                                  hist.p, nullptr, 0);
+  k_init_basis<<<1, 1024, 0, s>>>(n, r.p, weighted ? dr.p : r.p, V.p, nullptr, vin.p, dbeta.p,
+                                  g.p, hist.p, 0);
   CK_LAUNCH(ctx);
   double beta = 0.0;
   dbeta.download(&beta, 1, s);
   CK(cudaStreamSynchronize(s));
-  if (beta == 0.0) {
-    // zero residual: 0 iterations (krylov.py:110-118)
+  if (beta == 0.0) {  // zero residual: 0 iterations (krylov.py:110-118)
     if (dio) {
       if (x0) CK(cudaMemcpyAsync(x, x0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
       else CK(cudaMemsetAsync(x, 0, sizeof(double2) * n, s));
@@ -412,80 +494,184 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return MDD_OK;
   }
-  k_init_basis<<<std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 4096)), 256, 0,
-                 s>>>(n, r.p, weighted ? dr.p : r.p, V.p, weighted ? DV.p : nullptr, dbeta.p, g.p,
-                      hist.p, nullptr, 1);
+  k_init_basis<<<gs_grid(n), 256, 0, s>>>(n, r.p, weighted ? dr.p : r.p, V.p,
+                                          weighted ? DV.p : nullptr, vin.p, dbeta.p, g.p, hist.p,
+                                          1);
   CK_LAUNCH(ctx);
 
-  int* status = nullptr;
-  CK(cudaHostAlloc(&status, sizeof(int) * 4, cudaHostAllocMapped));
+  // ---- Arnoldi launch configuration: one CTA per SM
+  int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nsm, (n + 255) / 256));
+  const int64_t slice = (n + G - 1) / G;
+  G = (int)((n + slice - 1) / slice);
+  const size_t shmem = sizeof(double2) * (maxit + 1);
+  CK(cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi, kArnThreads, shmem));
+  if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
+  DevBuf<double2> partials(4 * (size_t)G);
+  int* hstatus = nullptr;
+  CK(cudaHostAlloc(&hstatus, sizeof(int) * 4, cudaHostAllocMapped));
   struct StFree {
     int* p;
     ~StFree() { cudaFreeHost(p); }
-  } sf{status};
-  int* status_dev = nullptr;
-  CK(cudaHostGetDevicePointer(&status_dev, status, 0));
+  } sf{hstatus};
+  int* hstatus_dev = nullptr;
+  CK(cudaHostGetDevicePointer(&hstatus_dev, hstatus, 0));
 
-  cudaEvent_t ev[4];
-  for (auto& e : ev) CK(cudaEventCreate(&e));
-  double t_op = 0, t_prec = 0, t_arn = 0;
-  int m = 0;
-  bool done = false;
-  for (m = 1; m <= maxit; ++m) {
-    double2* vprev = V.p + (int64_t)(m - 1) * n;
-    double2* w = V.p + (int64_t)m * n;
-    if (ctx->timing) CK(cudaEventRecord(ev[0], s));
+  ArnoldiArgs aa{};
+  aa.n = n;
+  aa.slice = slice;
+  aa.maxit = maxit;
+  aa.V = V.p;
+  aa.DV = weighted ? DV.p : nullptr;
+  aa.w = w.p;
+  aa.dw = weighted ? dw.p : nullptr;
+  aa.vin = vin.p;
+  aa.partials = partials.p;
+  aa.H = H.p;
+  aa.cs = cs.p;
+  aa.sn = sn.p;
+  aa.g = g.p;
+  aa.hist = hist.p;
+  aa.drift = ddrift.p;
+  aa.beta = dbeta.p;
+  aa.tol = cfg->tol;
+  aa.check_drift = cfg->check_drift;
+  aa.iter = diter.p;
+  aa.dstatus = dstat.p;
+
+  auto launch_arnoldi = [&](const ArnoldiArgs& args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(G);
+    lc.blockDim = dim3(kArnThreads);
+    lc.dynamicSmemBytes = shmem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k_arnoldi, args));
+    CK_LAUNCH(ctx);
+  };
+  // one iteration's operator part: w = A M vin (right) or M A vin (left)
+  auto op_part = [&]() {
     if (right) {
       if (op.has_M()) {
-        op.M(vprev, z.p);
-        if (ctx->timing) CK(cudaEventRecord(ev[1], s));
-        op.A(z.p, w);
+        op.M(vin.p, z.p);
+        op.A(z.p, w.p);
       } else {
-        if (ctx->timing) CK(cudaEventRecord(ev[1], s));
-        op.A(vprev, w);
+        op.A(vin.p, w.p);
       }
     } else {
       if (op.has_M()) {
-        op.A(vprev, t.p);
-        if (ctx->timing) CK(cudaEventRecord(ev[1], s));
-        op.M(t.p, w);
+        op.A(vin.p, t.p);
+        op.M(t.p, w.p);
       } else {
-        if (ctx->timing) CK(cudaEventRecord(ev[1], s));
-        op.A(vprev, w);
+        op.A(vin.p, w.p);
       }
     }
-    if (weighted) spmv_dev(ctx, ops->D, w, DV.p + (int64_t)m * n, s);
-    if (ctx->timing) CK(cudaEventRecord(ev[2], s));
-    status[0] = 0;
-    ArnoldiArgs aa{n,       m,      maxit,  V.p,    weighted ? DV.p : nullptr,
-                   partials.p, dpart.p, H.p, cs.p,   sn.p,
-                   g.p,     hist.p, ddrift.p, dbeta.p, cfg->tol,
-                   cfg->check_drift, status_dev};
-    void* args[] = {&aa};
-    CK(cudaLaunchCooperativeKernel((void*)k_arnoldi, dim3(G), dim3(bs), args, shmem, s));
-    CK_LAUNCH(ctx);
-    if (ctx->timing) CK(cudaEventRecord(ev[3], s));
+    if (weighted) spmv_dev(ctx, ops->D, w.p, dw.p, s);
+  };
+
+  double t_op = 0, t_prec = 0, t_arn = 0;
+  const bool use_graph = !ctx->timing && !op.host_ops();
+  int64_t body_launches = 0;
+  if (use_graph) {
+    const int64_t l0 = ctx->launches;
+    // device-side while loop: no host round trip per iteration
+    cudaGraph_t graph;
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    op_part();
+    ArnoldiArgs ga = aa;
+    ga.hstatus = nullptr;
+    ga.cond = cond;
+    ga.use_cond = 1;
+    launch_arnoldi(ga);
+    cudaGraph_t captured = nullptr;
+    CK(cudaStreamEndCapture(s, &captured));
+    body_launches = ctx->launches - l0;
+    cudaGraphExec_t exec;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    CK(cudaGraphLaunch(exec, s));
     CK(cudaStreamSynchronize(s));
-    if (ctx->timing) {
-      float a = 0, b2 = 0, c = 0;
-      CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
-      CK(cudaEventElapsedTime(&b2, ev[1], ev[2]));
-      CK(cudaEventElapsedTime(&c, ev[2], ev[3]));
-      if (right) { t_prec += a; t_op += b2; } else { t_op += a; t_prec += b2; }
-      t_arn += c;
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+  } else {
+    cudaEvent_t ev[4];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    ArnoldiArgs ha = aa;
+    ha.hstatus = hstatus_dev;
+    ha.use_cond = 0;
+    for (int it = 1; it <= maxit; ++it) {
+      if (ctx->timing) CK(cudaEventRecord(ev[0], s));
+      if (right) {
+        if (op.has_M()) {
+          op.M(vin.p, z.p);
+          if (ctx->timing) CK(cudaEventRecord(ev[1], s));
+          op.A(z.p, w.p);
+        } else {
+          if (ctx->timing) CK(cudaEventRecord(ev[1], s));
+          op.A(vin.p, w.p);
+        }
+      } else {
+        if (op.has_M()) {
+          op.A(vin.p, t.p);
+          if (ctx->timing) CK(cudaEventRecord(ev[1], s));
+          op.M(t.p, w.p);
+        } else {
+          if (ctx->timing) CK(cudaEventRecord(ev[1], s));
+          op.A(vin.p, w.p);
+        }
+      }
+      if (weighted) spmv_dev(ctx, ops->D, w.p, dw.p, s);
+      if (ctx->timing) CK(cudaEventRecord(ev[2], s));
+      hstatus[0] = 0;
+      launch_arnoldi(ha);
+      if (ctx->timing) CK(cudaEventRecord(ev[3], s));
+      CK(cudaStreamSynchronize(s));
+      if (ctx->timing) {
+        float a1 = 0, b1 = 0, c1 = 0;
+        CK(cudaEventElapsedTime(&a1, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&b1, ev[1], ev[2]));
+        CK(cudaEventElapsedTime(&c1, ev[2], ev[3]));
+        if (right) { t_prec += a1; t_op += b1; } else { t_op += a1; t_prec += b1; }
+        t_arn += c1;
+      }
+      if (((volatile int*)hstatus)[0]) break;
     }
-    if (((volatile int*)status)[0]) {
-      done = true;
-      break;
-    }
+    for (auto& e : ev) cudaEventDestroy(e);
   }
-  if (m > maxit) m = maxit;
-  const bool breakdown = done && status[1];
+  int st[4] = {0, 0, 0, 0};
+  dstat.download(st, 4, s);
+  CK(cudaStreamSynchronize(s));
+  const int m = st[2];
+  const bool done = st[0] != 0;
+  const bool breakdown = done && st[1];
+  if (m < 1) fail(MDD_ECUDA, "gmres: no iteration completed");
+  if (use_graph) ctx->launches += body_launches * (m - 1);  // graph replays of the loop body
+  // drift of the final appended vector (krylov.py:152-160)
+  if (cfg->check_drift && !breakdown) {
+    k_final_drift<<<m, 256, 0, s>>>(n, m, V.p, (weighted ? DV.p : V.p) + (int64_t)m * n, dtmp.p);
+    CK_LAUNCH(ctx);
+    k_max_into<<<1, 32, 0, s>>>(dtmp.p, m, ddrift.p + m);
+    CK_LAUNCH(ctx);
+  }
   // solution (krylov.py:189-198)
   k_backsub<<<1, 32, 0, s>>>(m, maxit, H.p, g.p, y.p);
   CK_LAUNCH(ctx);
-  k_combine_basis<<<std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 8192)), 256,
-                    0, s>>>(n, m, V.p, y.p, t.p);
+  k_combine_basis<<<gs_grid(n), 256, 0, s>>>(n, m, V.p, y.p, t.p);
   CK_LAUNCH(ctx);
   double2* upd = t.p;
   if (right && op.has_M()) {
@@ -494,8 +680,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   }
   DevBuf<double2> dxo(dio ? 0 : n);
   double2* xout = dio ? reinterpret_cast<double2*>(x) : dxo.p;
-  k_axpy_out<<<std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 8192)), 256, 0,
-               s>>>(n, x0 ? dx0.p : nullptr, upd, xout);
+  k_axpy_out<<<gs_grid(n), 256, 0, s>>>(n, x0 ? dx0.p : nullptr, upd, xout);
   CK_LAUNCH(ctx);
   if (!dio) dxo.download(reinterpret_cast<double2*>(x), n, s);
   hist.download(history, m + 1, s);
@@ -505,14 +690,13 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     V.download(reinterpret_cast<double2*>(basis), (size_t)nb * n, s);
   }
   CK(cudaStreamSynchronize(s));
-  for (auto& e : ev) cudaEventDestroy(e);
   if (ctx->timing) {
     ctx->timers[0] = t_op;
     ctx->timers[1] = t_prec;
     ctx->timers[2] = t_arn;
   }
   *iterations = m;
-  *converged = done ? (breakdown ? 2 : 1) : 0;  // 2: happy breakdown
+  *converged = done ? (breakdown ? 2 : 1) : 0;
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   MDD_API_END
 }
