@@ -245,12 +245,11 @@ def run_mine(args, rank, world):
         f"factor_entries={stats['factor_entries']:.3e}")
     for _ in range(args.warmup):
         step()
-    ctx.set_timing(True)
     dist_barrier(world)
     ctx.synchronize()
     launches0 = ctx.kernel_launches()
     ms_steps, phases, reps = [], [], []
-    timers = np.zeros(3)
+    host = np.zeros(3)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         for _ in range(args.steps):
             ctx.record(0)
@@ -259,11 +258,16 @@ def run_mine(args, rank, world):
             ms = ctx.elapsed_ms(0, 3)
             ms_steps.append(ms)
             phases.append((ctx.elapsed_ms(0, 1), ctx.elapsed_ms(1, 2), ctx.elapsed_ms(2, 3)))
-            timers += np.array(ctx.timers()[:3])
+            host += np.array(ctx.timers()[3:6])
             reps.append(rep)
     ctx.synchronize()
     dist_barrier(world)
     launches = ctx.kernel_launches() - launches0
+    # one extra instrumented step (host-driven loop with per-phase CUDA events) for the
+    # per-kernel-family breakdown; not part of the timed value
+    ctx.set_timing(True)
+    step()
+    timers = np.array(ctx.timers()[:3])
     ctx.set_timing(False)
     ms_step = max_over_ranks(float(np.mean(ms_steps)), world)
     # e2e through the public API with host buffers
@@ -278,7 +282,8 @@ def run_mine(args, rank, world):
     x_dev.download(x)
     its = rep.iterations
     # roofline of the dominant kernel family
-    t_op, t_prec, t_arn = timers / args.steps
+    t_op, t_prec, t_arn = timers
+    h_setup, h_loop, h_final = host / args.steps
     fe = stats["factor_entries"]
     sum_loc = stats["sum_local_dofs"]
     r0nnz = dec.coarse.R0.nnz
@@ -324,7 +329,8 @@ def run_mine(args, rank, world):
         "phases_ms": {"assemble_A": float(np.mean([p[0] for p in phases])),
                       "assemble_Aprec_factor": float(np.mean([p[1] for p in phases])),
                       "gmres": float(np.mean([p[2] for p in phases])),
-                      "gmres_spmv": t_op, "gmres_precond": t_prec, "gmres_arnoldi": t_arn},
+                      "gmres_spmv": t_op, "gmres_precond": t_prec, "gmres_arnoldi": t_arn,
+                      "gmres_host_setup": h_setup, "gmres_host_loop": h_loop, "gmres_host_final": h_final},
         "setup_s": {"decomposition": t_dec, "first_setup_incl_symbolic": t_setup},
         "factor": {k: stats[k] for k in ("n_fronts", "max_front", "factor_entries", "factor_flops", "factor_ms")},
         "gpu_launches": int(launches),

@@ -216,37 +216,48 @@ __global__ void k_pivinit(double* p, int64_t n) {
   }
 }
 
-// Dot products of up to 4 consecutive front rows (row0 + k*ld) with z[0..len)
-// held in shared memory: 4 independent FMA chains and 2-way unrolling keep 8
-// streaming loads in flight per lane; the z operand is loaded once for all
-// rows.  Factor data are read exactly once per apply (>> L2): streaming loads.
-__device__ __forceinline__ void dot_rows4(const double2* __restrict__ row0, int64_t ld, int nr,
-                                          int len, const double2* __restrict__ z, int lane,
-                                          double2 (&out)[4]) {
-  double2 acc[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) acc[k] = make_double2(0.0, 0.0);
-  int q = lane;
-  for (; q + 32 < len; q += 64) {
-    const double2 z0 = z[q], z1 = z[q + 32];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < nr) {
-        const double2 t0 = __ldcs(row0 + k * ld + q);
-        const double2 t1 = __ldcs(row0 + k * ld + q + 32);
-        acc[k] = cfma(t0, z0, acc[k]);
-        acc[k] = cfma(t1, z1, acc[k]);
-      }
+// Row-block GEMV of a front: rows [r0, r0+kSolveRows) of the row-major block
+// T (leading dimension ld), each dotted with z[0..len) held in shared memory.
+// A group of TPR lanes owns one row (TPR matched to the row length so short
+// rows do not waste a full warp reduction); each lane keeps 4 streaming loads
+// in flight.  emit(row, value) is called by the group's first lane.
+template <int TPR, typename Emit>
+__device__ __forceinline__ void gemv_rows(const double2* __restrict__ T, int64_t ld, int r0, int rend,
+                                          int len, const double2* __restrict__ z, Emit emit) {
+  constexpr int kGroups = 256 / TPR;
+  const int grp = threadIdx.x / TPR, lig = threadIdx.x % TPR;
+  for (int rr = grp; rr < kSolveRows; rr += kGroups) {
+    const int r = r0 + rr;
+    if (r >= rend) break;  // uniform within the group
+    const double2* row = T + (int64_t)r * ld;
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+    int q = lig;
+    for (; q + 3 * TPR < len; q += 4 * TPR) {
+      const double2 t0 = __ldcs(row + q), t1 = __ldcs(row + q + TPR);
+      const double2 t2 = __ldcs(row + q + 2 * TPR), t3 = __ldcs(row + q + 3 * TPR);
+      a0 = cfma(t0, z[q], a0);
+      a1 = cfma(t1, z[q + TPR], a1);
+      a2 = cfma(t2, z[q + 2 * TPR], a2);
+      a3 = cfma(t3, z[q + 3 * TPR], a3);
     }
-  }
-  if (q < len) {
-    const double2 z0 = z[q];
+    for (; q < len; q += TPR) a0 = cfma(__ldcs(row + q), z[q], a0);
+    double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (k < nr) acc[k] = cfma(__ldcs(row0 + k * ld + q), z0, acc[k]);
+    for (int o = TPR / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, TPR);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, TPR);
+    }
+    if (lig == 0) emit(r, acc);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) out[k] = warp_sum2(acc[k]);
+}
+
+template <typename Emit>
+__device__ __forceinline__ void gemv_rows_any(const double2* T, int64_t ld, int r0, int rend, int len,
+                                              const double2* z, Emit emit) {
+  if (len <= 48) gemv_rows<4>(T, ld, r0, rend, len, z, emit);
+  else if (len <= 160) gemv_rows<8>(T, ld, r0, rend, len, z, emit);
+  else if (len <= 512) gemv_rows<16>(T, ld, r0, rend, len, z, emit);
+  else gemv_rows<32>(T, ld, r0, rend, len, z, emit);
 }
 
 // forward: fp = b_P + children contributions ; uvec = (children contributions)_U - F_UP fp
@@ -273,22 +284,16 @@ __global__ void __launch_bounds__(256) k_fwd(const int2* __restrict__ tasks,
     if (r0 == 0) fpst[base + q] = f;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int u0 = r0 + wid * 4;
-  const int nr = min(4, nd.nu - u0);
-  if (nr <= 0) return;
-  double2 d[4];
-  dot_rows4(fronts + nd.front_off + (int64_t)(np + u0) * m, m, nr, np, fp, lane, d);
-  if (lane < nr) {
-    const int u = u0 + lane;
+  if (r0 >= nd.nu) return;
+  const double2* TU = fronts + nd.front_off + (int64_t)np * m;  // row u of F_UP
+  gemv_rows_any(TU, m, r0, nd.nu, np, fp, [&](int u, double2 acc) {
     double2 fu = make_double2(0.0, 0.0);
     for (int ci = 0; ci < nd.nch; ++ci) {
       const int g = gmap[nd.gmap_off + (int64_t)ci * m + np + u];
       if (g >= 0) fu = cadd(fu, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
     }
-    const double2 acc = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
     uvec[nd.uvec_off + u] = csub(fu, acc);
-  }
+  });
 }
 
 // backward: x_P = -(F_PP fp + F_PU x_U)
@@ -307,16 +312,8 @@ __global__ void __launch_bounds__(256) k_bwd(const int2* __restrict__ tasks,
   for (int q = threadIdx.x; q < m; q += blockDim.x)
     z[q] = q < np ? fpst[base + q] : xloc[(int64_t)nd.mat_off + upd[nd.upd_off + q - np]];
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i0 = r0 + wid * 4;
-  const int nr = min(4, np - i0);
-  if (nr <= 0) return;
-  double2 d[4];
-  dot_rows4(fronts + nd.front_off + (int64_t)i0 * m, m, nr, m, z, lane, d);
-  if (lane < nr) {
-    const double2 acc = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
-    xloc[base + i0 + lane] = cneg(acc);
-  }
+  gemv_rows_any(fronts + nd.front_off, m, r0, np, m, z,
+                [&](int i, double2 acc) { xloc[base + i] = cneg(acc); });
 }
 
 // ------------------------------------------------------------- host plan

@@ -48,6 +48,7 @@ struct ArnoldiArgs {
   double2* dw;     // D w (weighted) or nullptr
   double2* vin;    // out: copy of V[m] = next operator input
   double2* partials;  // 2 (parity) x 2 (dot, drift) x G
+  unsigned* flags;    // G publication tags
   double2* H;      // (maxit+1) x maxit, column j at H + j*(maxit+1)
   double2* cs;
   double2* sn;
@@ -121,8 +122,72 @@ __device__ __forceinline__ void reduce_step(const double2* p, int G, double2* sh
   dr = sh[67];
 }
 
+constexpr int kArnE = 6;  // vector elements per thread kept in registers (register path)
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Publish this CTA's two partial sums for step `tag` (thread 0 only): the
+// values first, then a release store of the tag into the CTA's flag.
+__device__ __forceinline__ void publish(double2* part, int G, double2 a, double2 b,
+                                        unsigned* flags, unsigned tag) {
+  part[blockIdx.x] = a;
+  part[G + blockIdx.x] = b;
+  st_release_u32(flags + blockIdx.x, tag);
+}
+
+// All-gather barrier fused with the reduction: warp 0 acquires every CTA's
+// flag for `tag`, then sums the published partials in CTA order (fixed order
+// -> bitwise reproducible) and broadcasts through shared memory.  One
+// acquire round trip + one read round trip; no atomics.
+__device__ __forceinline__ void gather_sum(const double2* part, int G, const unsigned* flags,
+                                           unsigned tag, double2* sh, double2& dot, double2& dr) {
+  if (threadIdx.x < 32) {
+    for (int k = threadIdx.x; k < G; k += 32)
+      while (ld_acquire_u32(flags + k) != tag) {
+      }
+    double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < G; k += 32) {
+      const double2 u = __ldcg(part + k), v = __ldcg(part + G + k);
+      x.x += u.x;
+      x.y += u.y;
+      y.x += v.x;
+      y.y += v.y;
+    }
+    x = warp_sum2(x);
+    y = warp_sum2(y);
+    if (threadIdx.x == 0) {
+      sh[66] = x;
+      sh[67] = y;
+    }
+  }
+  __syncthreads();
+  dot = sh[66];
+  dr = sh[67];
+}
+
+__device__ __forceinline__ double2 cdotc_acc(double2 acc, double2 x, double2 y) {  // acc + conj(x) y
+  acc.x += x.x * y.x + x.y * y.y;
+  acc.y += x.x * y.y - x.y * y.x;
+  return acc;
+}
+__device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // w - h v
+  return make_double2(w.x - (h.x * v.x - h.y * v.y), w.y - (h.x * v.y + h.y * v.x));
+}
+
+// REG: unweighted, every CTA slice fits in registers (slice <= kArnThreads*kArnE):
+// w stays in registers for the whole kernel and the basis slice of step s+2
+// is loaded into registers right after publishing step s, so its latency
+// overlaps the barrier wait.  Otherwise: w and the basis are streamed from
+// L2/HBM with a TMA bulk L2 prefetch of the step s+2 slice.
+template <bool REG>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ double2 col[];  // m+1, identical in every CTA
   __shared__ double2 red[68];
   const int G = gridDim.x;
@@ -131,86 +196,116 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const int64_t lo = (int64_t)blockIdx.x * a.slice;
   const int64_t hi = min(n, lo + a.slice);
   const int64_t len = hi > lo ? hi - lo : 0;
-  const bool weighted = a.DV != nullptr;
+  const bool weighted = !REG && a.DV != nullptr;
   double2* w = a.w;
   double2* dw = weighted ? a.dw : a.w;
-  // drift of V_{m-1} against V_j, j < m-1 (needs m >= 2)
-  const bool do_drift = a.check_drift && m >= 2;
+  const bool do_drift = a.check_drift && m >= 2;  // drift of V_{m-1} vs V_j, j < m-1
   const double2* dvm1 = (weighted ? a.DV : a.V) + (int64_t)(m - 1) * n;
+  const int nsteps = 2 * m;
+  const unsigned tbase = ((unsigned)m << 16) + 1u;  // tag(s) = tbase + (s + 1), s >= -1
   for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
+  // X_t = V_{t mod m} for t < nsteps; X_nsteps = w (the norm)
+  auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n; };
 
-  // step -1: partials of <V_0, dw> (+ <V_0, DV_{m-1}>)
-  if (threadIdx.x == 0) prefetch_l2(a.V + (m > 1 ? n : 0) + lo, len * 16);
+  double2 W[kArnE], XN[kArnE], XNN[kArnE];
+  double2* DM = col + (a.maxit + 1);  // drift vector slice in shared memory (REG path)
+  if constexpr (REG) {
+#pragma unroll
+    for (int k = 0; k < kArnE; ++k) {
+      const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+      const bool ok = i < hi;
+      W[k] = ok ? w[i] : make_double2(0.0, 0.0);
+      XN[k] = ok ? a.V[i] : make_double2(0.0, 0.0);
+      DM[threadIdx.x + k * kArnThreads] = (ok && do_drift) ? dvm1[i] : make_double2(0.0, 0.0);
+    }
+  } else if (threadIdx.x == 0) {
+    prefetch_l2(xvec(1) + lo, len * 16);
+  }
+  // iteration -1: dot with X_0 (+ drift of X_0 if 0 < m-1)
   {
     double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const double2 x = a.V[i], y = dw[i];
-      acc.x += x.x * y.x + x.y * y.y;
-      acc.y += x.x * y.y - x.y * y.x;
-      if (do_drift) {
-        const double2 z = dvm1[i];
-        dacc.x += x.x * z.x + x.y * z.y;
-        dacc.y += x.x * z.y - x.y * z.x;
+    if constexpr (REG) {
+#pragma unroll
+      for (int k = 0; k < kArnE; ++k) {
+        acc = cdotc_acc(acc, XN[k], W[k]);
+        if (do_drift) dacc = cdotc_acc(dacc, XN[k], DM[threadIdx.x + k * kArnThreads]);
+      }
+    } else {
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 x = a.V[i];
+        acc = cdotc_acc(acc, x, dw[i]);
+        if (do_drift) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
     block_sum2x2(acc, dacc, red);
-    if (threadIdx.x == 0) {
-      a.partials[blockIdx.x] = acc;
-      a.partials[G + blockIdx.x] = dacc;
+    if (threadIdx.x == 0) publish(a.partials, G, acc, dacc, a.flags, tbase);
+    if constexpr (REG) {
+      const double2* x1 = xvec(1);
+#pragma unroll
+      for (int k = 0; k < kArnE; ++k) {
+        const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+        XNN[k] = i < hi ? x1[i] : make_double2(0.0, 0.0);
+      }
     }
   }
-  grid.sync();
   double dmax = 0.0;
-  const int nsteps = 2 * m;
   for (int s = 0; s < nsteps; ++s) {
     const int j = s % m;
     double2 h, d;
-    reduce_step(a.partials + (s & 1) * 2 * G, G, red, h, d);
-    // the drift term reduced here belongs to V_j (dotted at step s-1), j < m-1
-    if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
+    gather_sum(a.partials + (s & 1) * 2 * G, G, a.flags, tbase + (unsigned)s, red, h, d);
+    if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));  // drift term of X_s = V_s
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
-      // L2 prefetch of the slice dotted at step s+1
-      if (s + 2 < nsteps) prefetch_l2(a.V + (int64_t)((s + 2) % m) * n + lo, len * 16);
+      if (!REG && s + 2 < nsteps) prefetch_l2(xvec(s + 2) + lo, len * 16);
     }
-    const double2* vj = a.V + (int64_t)j * n;
-    const double2* dvj = weighted ? a.DV + (int64_t)j * n : nullptr;
     const bool last = (s + 1 == nsteps);
-    const int jn = (s + 1) % m;
-    const double2* vn = last ? w : a.V + (int64_t)jn * n;
-    const bool drift_next = do_drift && s + 1 < m - 1;  // next vector is V_{s+1}, s+1 < m-1
+    const bool drift_next = do_drift && s + 1 < m - 1;
     double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const double2 v = vj[i];
-      double2 wi = w[i];
-      wi = make_double2(wi.x - (h.x * v.x - h.y * v.y), wi.y - (h.x * v.y + h.y * v.x));
-      w[i] = wi;
-      double2 dwi = wi;
-      if (weighted) {
-        const double2 dv = dvj[i];
-        dwi = dw[i];
-        dwi = make_double2(dwi.x - (h.x * dv.x - h.y * dv.y), dwi.y - (h.x * dv.y + h.y * dv.x));
-        dw[i] = dwi;
+    if constexpr (REG) {
+      // axpy with X_s (= XN), dot with X_{s+1} (= XNN, or w itself at the end)
+#pragma unroll
+      for (int k = 0; k < kArnE; ++k) {
+        W[k] = caxmy(W[k], h, XN[k]);
+        const double2 x = last ? W[k] : XNN[k];
+        acc = cdotc_acc(acc, x, W[k]);
+        if (drift_next) dacc = cdotc_acc(dacc, x, DM[threadIdx.x + k * kArnThreads]);
+        XN[k] = XNN[k];
       }
-      const double2 x = last ? wi : vn[i];
-      acc.x += x.x * dwi.x + x.y * dwi.y;
-      acc.y += x.x * dwi.y - x.y * dwi.x;
-      if (drift_next) {
-        const double2 z = dvm1[i];
-        dacc.x += x.x * z.x + x.y * z.y;
-        dacc.y += x.x * z.y - x.y * z.x;
+    } else {
+      const double2* vj = a.V + (int64_t)j * n;
+      const double2* dvj = weighted ? a.DV + (int64_t)j * n : nullptr;
+      const double2* vn = last ? w : xvec(s + 1);
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 v = vj[i];
+        const double2 wi = caxmy(w[i], h, v);
+        w[i] = wi;
+        double2 dwi = wi;
+        if (weighted) {
+          dwi = caxmy(dw[i], h, dvj[i]);
+          dw[i] = dwi;
+        }
+        const double2 x = last ? wi : vn[i];
+        acc = cdotc_acc(acc, x, dwi);
+        if (drift_next) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
     block_sum2x2(acc, dacc, red);
-    if (threadIdx.x == 0) {
-      double2* p = a.partials + ((s + 1) & 1) * 2 * G;
-      p[blockIdx.x] = acc;
-      p[G + blockIdx.x] = dacc;
+    if (threadIdx.x == 0) publish(a.partials + ((s + 1) & 1) * 2 * G, G, acc, dacc, a.flags,
+                                  tbase + (unsigned)(s + 1));
+    if constexpr (REG) {
+      if (s + 2 < nsteps) {  // preload X_{s+2} while the other CTAs arrive
+        const double2* x2 = xvec(s + 2);
+#pragma unroll
+        for (int k = 0; k < kArnE; ++k) {
+          const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+          XNN[k] = i < hi ? x2[i] : make_double2(0.0, 0.0);
+        }
+      }
     }
-    grid.sync();
   }
   double2 hn2, dummy;
-  reduce_step(a.partials + (nsteps & 1) * 2 * G, G, red, hn2, dummy);
+  gather_sum(a.partials + (nsteps & 1) * 2 * G, G, a.flags, tbase + (unsigned)nsteps, red, hn2,
+             dummy);
   const double hlast = sqrt(fmax(hn2.x, 0.0));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
@@ -220,15 +315,27 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const bool breakdown = hlast <= 1e-13 * cmax;
   if (!breakdown) {
     double2* vm = a.V + (int64_t)m * n;
-    double2* dvm = weighted ? a.DV + (int64_t)m * n : nullptr;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const double2 wi = w[i];
-      const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
-      vm[i] = q;
-      a.vin[i] = q;
-      if (weighted) {
-        const double2 d = dw[i];
-        dvm[i] = make_double2(d.x / hlast, d.y / hlast);
+    if constexpr (REG) {
+#pragma unroll
+      for (int k = 0; k < kArnE; ++k) {
+        const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+        if (i < hi) {
+          const double2 q = make_double2(W[k].x / hlast, W[k].y / hlast);
+          vm[i] = q;
+          a.vin[i] = q;
+        }
+      }
+    } else {
+      double2* dvm = weighted ? a.DV + (int64_t)m * n : nullptr;
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double2 wi = w[i];
+        const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
+        vm[i] = q;
+        a.vin[i] = q;
+        if (weighted) {
+          const double2 dd = dw[i];
+          dvm[i] = make_double2(dd.x / hlast, dd.y / hlast);
+        }
       }
     }
   }
@@ -503,12 +610,17 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nsm, (n + 255) / 256));
   const int64_t slice = (n + G - 1) / G;
   G = (int)((n + slice - 1) / slice);
-  const size_t shmem = sizeof(double2) * (maxit + 1);
-  CK(cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+  const size_t shmem = sizeof(double2) * ((size_t)maxit + 1 + (size_t)kArnThreads * kArnE);
+  const bool reg_path = !weighted && slice <= (int64_t)kArnThreads * kArnE;
+  auto kfn = reg_path ? k_arnoldi<true> : k_arnoldi<false>;
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi, kArnThreads, shmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
+  if (G > per_sm * ctx->nsm) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
   DevBuf<double2> partials(4 * (size_t)G);
+  DevBuf<unsigned> flags(G);
+  flags.zero(s);
   int* hstatus = nullptr;
   CK(cudaHostAlloc(&hstatus, sizeof(int) * 4, cudaHostAllocMapped));
   struct StFree {
@@ -528,6 +640,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.dw = weighted ? dw.p : nullptr;
   aa.vin = vin.p;
   aa.partials = partials.p;
+  aa.flags = flags.p;
   aa.H = H.p;
   aa.cs = cs.p;
   aa.sn = sn.p;
@@ -551,7 +664,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, k_arnoldi, args));
+    CK(cudaLaunchKernelEx(&lc, kfn, args));
     CK_LAUNCH(ctx);
   };
   // one iteration's operator part: w = A M vin (right) or M A vin (left)
@@ -575,6 +688,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   };
 
   double t_op = 0, t_prec = 0, t_arn = 0;
+  CK(cudaStreamSynchronize(s));
+  auto t_loop0 = std::chrono::steady_clock::now();
   const bool use_graph = !ctx->timing && !op.host_ops();
   int64_t body_launches = 0;
   if (use_graph) {
@@ -653,6 +768,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     }
     for (auto& e : ev) cudaEventDestroy(e);
   }
+  auto t_loop1 = std::chrono::steady_clock::now();
   int st[4] = {0, 0, 0, 0};
   dstat.download(st, 4, s);
   CK(cudaStreamSynchronize(s));
@@ -690,11 +806,16 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     V.download(reinterpret_cast<double2*>(basis), (size_t)nb * n, s);
   }
   CK(cudaStreamSynchronize(s));
+  auto t_end = std::chrono::steady_clock::now();
   if (ctx->timing) {
     ctx->timers[0] = t_op;
     ctx->timers[1] = t_prec;
     ctx->timers[2] = t_arn;
   }
+  // host wall split: setup (allocation, r0, basis), loop, finalisation (ms)
+  ctx->timers[3] = std::chrono::duration<double, std::milli>(t_loop0 - t0).count();
+  ctx->timers[4] = std::chrono::duration<double, std::milli>(t_loop1 - t_loop0).count();
+  ctx->timers[5] = std::chrono::duration<double, std::milli>(t_end - t_loop1).count();
   *iterations = m;
   *converged = done ? (breakdown ? 2 : 1) : 0;
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
