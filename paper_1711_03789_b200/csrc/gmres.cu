@@ -37,6 +37,7 @@ namespace mdd {
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 
 constexpr int kArnThreads = 512;
+constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
 
 struct ArnoldiArgs {
   int64_t n;
@@ -142,23 +143,30 @@ __device__ __forceinline__ void publish(double2* part, int G, double2 a, double2
   st_release_u32(flags + blockIdx.x, tag);
 }
 
-// All-gather barrier fused with the reduction: warp 0 acquires every CTA's
-// flag for `tag`, then sums the published partials in CTA order (fixed order
-// -> bitwise reproducible) and broadcasts through shared memory.  One
-// acquire round trip + one read round trip; no atomics.
+// All-gather barrier fused with the reduction: thread t < G acquires CTA t's
+// flag for `tag` and reads CTA t's partials (its own acquire orders the
+// read), all G polls in flight at once; warp 0 then sums the staged values in
+// CTA order (fixed order -> bitwise reproducible) and broadcasts them.  One
+// poll round trip + one read round trip; no atomics.
 __device__ __forceinline__ void gather_sum(const double2* part, int G, const unsigned* flags,
                                            unsigned tag, double2* sh, double2& dot, double2& dr) {
+  double2* stage = sh + 68;  // 2*G slots after the block-reduce scratch
+  if ((int)threadIdx.x < G) {
+    const int k = threadIdx.x;
+    long long spins = 0;
+    // tags grow monotonically: a fast CTA may already have published tag+1
+    while (ld_acquire_u32(flags + k) < tag) {
+      if (++spins > (1ll << 28)) __trap();  // never hang the device on a protocol bug
+    }
+    stage[k] = __ldcg(part + k);
+    stage[G + k] = __ldcg(part + G + k);
+  }
+  __syncthreads();
   if (threadIdx.x < 32) {
-    for (int k = threadIdx.x; k < G; k += 32)
-      while (ld_acquire_u32(flags + k) != tag) {
-      }
     double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
     for (int k = threadIdx.x; k < G; k += 32) {
-      const double2 u = __ldcg(part + k), v = __ldcg(part + G + k);
-      x.x += u.x;
-      x.y += u.y;
-      y.x += v.x;
-      y.y += v.y;
+      x = cadd(x, stage[k]);
+      y = cadd(y, stage[G + k]);
     }
     x = warp_sum2(x);
     y = warp_sum2(y);
@@ -189,7 +197,7 @@ __device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // 
 template <bool REG>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   extern __shared__ double2 col[];  // m+1, identical in every CTA
-  __shared__ double2 red[68];
+  __shared__ double2 red[68 + 2 * kMaxArnCTAs];
   const int G = gridDim.x;
   const int m = *a.iter + 1;
   const int64_t n = a.n;
@@ -617,7 +625,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
-  if (G > per_sm * ctx->nsm) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
+  if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
   DevBuf<double2> partials(4 * (size_t)G);
   DevBuf<unsigned> flags(G);
   flags.zero(s);

@@ -74,6 +74,20 @@ def _device_prec(precond):
     return None
 
 
+def _is_identity(m, n) -> bool:
+    """An exact identity weight: the reference's D @ w is then bitwise w
+    (krylov.py:80-81), so the unweighted path is bitwise-equivalent."""
+    if isinstance(m, DeviceCSR):
+        m = m.to_scipy()
+    if sp.issparse(m):
+        c = m.tocsr()
+        c.sum_duplicates()
+        return (c.shape == (n, n) and c.nnz == n and np.array_equal(c.indices, np.arange(n))
+                and np.array_equal(c.indptr, np.arange(n + 1)) and np.all(c.data == 1.0))
+    a = np.asarray(m)
+    return a.shape == (n, n) and np.array_equal(a, np.eye(n))
+
+
 def _is_matrix(op) -> bool:
     return isinstance(op, (DeviceCSR, np.ndarray)) or sp.issparse(op)
 
@@ -153,7 +167,7 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, ou
             ops.m_fn = h.cb
         else:
             raise TypeError("precond must be a matrix, a PreconditionerState or a callable")
-    if cfg.weight is not None:
+    if cfg.weight is not None and not _is_identity(cfg.weight, n):
         D = as_device_csr(cfg.weight)
         keep.append(D)
         ops.D = D.handle
