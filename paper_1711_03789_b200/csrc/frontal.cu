@@ -226,9 +226,7 @@ __device__ __forceinline__ void gemv_rows(const double2* __restrict__ T, int64_t
                                           int len, const double2* __restrict__ z, Emit emit) {
   constexpr int kGroups = 256 / TPR;
   const int grp = threadIdx.x / TPR, lig = threadIdx.x % TPR;
-  for (int rr = grp; rr < kSolveRows; rr += kGroups) {
-    const int r = r0 + rr;
-    if (r >= rend) break;  // uniform within the group
+  for (int r = r0 + grp; r < rend; r += kGroups) {
     const double2* row = T + (int64_t)r * ld;
     double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
     int q = lig;
@@ -261,58 +259,60 @@ __device__ __forceinline__ void gemv_rows_any(const double2* T, int64_t ld, int 
 }
 
 // forward: fp = b_P + children contributions ; uvec = (children contributions)_U - F_UP fp
-__global__ void __launch_bounds__(256) k_fwd(const int2* __restrict__ tasks,
+// gmap_abs holds, per child, the absolute uvec index feeding each front
+// position (or -1), so each contribution is a 2-deep load chain.
+__global__ void __launch_bounds__(256) k_fwd(const int4* __restrict__ tasks,
                                              const NodeDev* __restrict__ nodes,
-                                             const int32_t* __restrict__ children,
-                                             const int32_t* __restrict__ gmap,
+                                             const int32_t* __restrict__ gmap_abs,
                                              const double2* __restrict__ fronts,
                                              const double2* __restrict__ bloc,
                                              double2* __restrict__ fpst, double2* __restrict__ uvec) {
   extern __shared__ double2 fp[];
-  const int2 tk = tasks[blockIdx.x];
+  const int4 tk = tasks[blockIdx.x];
   const NodeDev nd = nodes[tk.x];
-  const int r0 = tk.y;
+  const int r0 = tk.y, r1 = tk.z;
   const int np = nd.np, m = nd.m;
   const int64_t base = (int64_t)nd.mat_off + nd.pivb;
+  const int32_t* ga = gmap_abs + nd.gmap_off;
   for (int q = threadIdx.x; q < np; q += blockDim.x) {
     double2 f = bloc[base + q];
     for (int ci = 0; ci < nd.nch; ++ci) {
-      const int g = gmap[nd.gmap_off + (int64_t)ci * m + q];
-      if (g >= 0) f = cadd(f, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
+      const int g = ga[(int64_t)ci * m + q];
+      if (g >= 0) f = cadd(f, uvec[g]);
     }
     fp[q] = f;
     if (r0 == 0) fpst[base + q] = f;
   }
   __syncthreads();
-  if (r0 >= nd.nu) return;
+  if (r0 >= r1) return;
   const double2* TU = fronts + nd.front_off + (int64_t)np * m;  // row u of F_UP
-  gemv_rows_any(TU, m, r0, nd.nu, np, fp, [&](int u, double2 acc) {
+  gemv_rows_any(TU, m, r0, r1, np, fp, [&](int u, double2 acc) {
     double2 fu = make_double2(0.0, 0.0);
     for (int ci = 0; ci < nd.nch; ++ci) {
-      const int g = gmap[nd.gmap_off + (int64_t)ci * m + np + u];
-      if (g >= 0) fu = cadd(fu, uvec[nodes[children[nd.child_off + ci]].uvec_off + g]);
+      const int g = ga[(int64_t)ci * m + np + u];
+      if (g >= 0) fu = cadd(fu, uvec[g]);
     }
     uvec[nd.uvec_off + u] = csub(fu, acc);
   });
 }
 
 // backward: x_P = -(F_PP fp + F_PU x_U)
-__global__ void __launch_bounds__(256) k_bwd(const int2* __restrict__ tasks,
+__global__ void __launch_bounds__(256) k_bwd(const int4* __restrict__ tasks,
                                              const NodeDev* __restrict__ nodes,
                                              const int32_t* __restrict__ upd,
                                              const double2* __restrict__ fronts,
                                              const double2* __restrict__ fpst,
                                              double2* __restrict__ xloc) {
   extern __shared__ double2 z[];
-  const int2 tk = tasks[blockIdx.x];
+  const int4 tk = tasks[blockIdx.x];
   const NodeDev nd = nodes[tk.x];
-  const int r0 = tk.y;
+  const int r0 = tk.y, r1 = tk.z;
   const int np = nd.np, m = nd.m;
   const int64_t base = (int64_t)nd.mat_off + nd.pivb;
   for (int q = threadIdx.x; q < m; q += blockDim.x)
     z[q] = q < np ? fpst[base + q] : xloc[(int64_t)nd.mat_off + upd[nd.upd_off + q - np]];
   __syncthreads();
-  gemv_rows_any(fronts + nd.front_off, m, r0, np, m, z,
+  gemv_rows_any(fronts + nd.front_off, m, r0, r1, m, z,
                 [&](int i, double2 acc) { xloc[base + i] = cneg(acc); });
 }
 
@@ -482,7 +482,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   for (int64_t g = 0; g < nn; ++g) lev[node_level[g]].push_back((int32_t)g);
   std::vector<int64_t> h_epos;
   std::vector<int32_t> h_esrc;
-  std::vector<int2> h_init, h_panel, h_fwd, h_bwd;
+  std::vector<int2> h_init, h_panel;
+  std::vector<int4> h_fwd, h_bwd;
   std::vector<int4> h_tile;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
@@ -507,9 +508,17 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       const NodeDev& nd = h_nodes[g];
       for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
       lnp = std::max(lnp, nd.np);
-      if (nd.nu == 0) h_fwd.push_back(make_int2(g, 0));
-      for (int r = 0; r < nd.nu; r += kSolveRows) h_fwd.push_back(make_int2(g, r));
-      for (int r = 0; r < nd.np; r += kSolveRows) h_bwd.push_back(make_int2(g, r));
+      // solve tasks: row ranges holding ~kSolveTaskElems factor entries
+      auto rows_for = [](int len) {
+        int r = len > 0 ? kSolveTaskElems / len : 512;
+        r = std::max(kSolveRows, std::min(512, r));
+        return (r / kSolveRows) * kSolveRows;
+      };
+      if (nd.nu == 0) h_fwd.push_back(make_int4(g, 0, 0, 0));
+      for (int r = 0, step = rows_for(nd.np); r < nd.nu; r += step)
+        h_fwd.push_back(make_int4(g, r, std::min(nd.nu, r + step), 0));
+      for (int r = 0, step = rows_for(nd.m); r < nd.np; r += step)
+        h_bwd.push_back(make_int4(g, r, std::min(nd.np, r + step), 0));
     }
     lev_init_off.push_back((int64_t)h_init.size());
     lev_fwd_off.push_back((int64_t)h_fwd.size());
@@ -544,9 +553,22 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       ++nsteps_total;
     }
   }
+  std::vector<int32_t> h_gabs(h_gmap.size(), -1);
+  for (int64_t g = 0; g < nn; ++g) {
+    const NodeDev& nd = h_nodes[g];
+    for (int ci = 0; ci < nd.nch; ++ci) {
+      const NodeDev& ch = h_nodes[h_children[nd.child_off + ci]];
+      if (ch.uvec_off + ch.nu > INT32_MAX) fail(MDD_EINVAL, "update-vector space exceeds 2^31");
+      for (int q = 0; q < nd.m; ++q) {
+        const int32_t r = h_gmap[nd.gmap_off + (int64_t)ci * nd.m + q];
+        if (r >= 0) h_gabs[nd.gmap_off + (int64_t)ci * nd.m + q] = (int32_t)(ch.uvec_off + r);
+      }
+    }
+  }
   nodes.upload(h_nodes, s);
   children.upload(h_children, s);
   gmap.upload(h_gmap, s);
+  gmap_abs.upload(h_gabs, s);
   upd.upload(h_upd, s);
   ent_pos.upload(h_epos, s);
   ent_src.upload(h_esrc, s);
@@ -652,7 +674,7 @@ void FrontPlan::solve(cudaStream_t s) {
   for (int L = 0; L < nlevels; ++L) {
     const int64_t n = lev_fwd_off[L + 1] - lev_fwd_off[L];
     if (!n) continue;
-    k_fwd<<<(unsigned)n, 256, fsm, s>>>(fwd_tasks.p + lev_fwd_off[L], nodes.p, children.p, gmap.p,
+    k_fwd<<<(unsigned)n, 256, fsm, s>>>(fwd_tasks.p + lev_fwd_off[L], nodes.p, gmap_abs.p,
                                         fronts.p, bloc.p, fpst.p, uvec.p);
     CK_LAUNCH(ctx);
   }

@@ -29,7 +29,8 @@ namespace mdd {
 constexpr int kPB = 32;      // pivot block of the sweep
 constexpr int kTile = 64;    // update tile
 constexpr int kPanelCols = 128;
-constexpr int kSolveRows = 32;
+constexpr int kSolveRows = 32;          // minimum rows per solve task
+constexpr int kSolveTaskElems = 3072;   // ~48 KB of factor data per solve task
 
 struct NodeDev {
   int64_t front_off;  // complex elements into the front storage
@@ -74,7 +75,8 @@ struct FrontPlan {
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
-  DevBuf<int2> fwd_tasks, bwd_tasks;
+  DevBuf<int4> fwd_tasks, bwd_tasks;  // {node, row0, row1, 0}
+  DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   std::vector<int64_t> lev_fwd_off, lev_bwd_off;
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;

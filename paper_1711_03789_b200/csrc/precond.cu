@@ -62,6 +62,13 @@ struct PrecCore {
   DevBuf<int32_t> loc_row_off;                   // per subdomain: offset into loc_rowptr
   std::vector<double> stats = std::vector<double>(8, 0.0);
   DevBuf<double2> t1, t2, t3, t4;
+  cudaStream_t s2 = nullptr;  // coarse-solve branch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~PrecCore() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s2) cudaStreamDestroy(s2);
+  }
 };
 
 }  // namespace mdd
@@ -388,21 +395,30 @@ static unsigned gsb(mdd_ctx* ctx, int64_t n) {
 static unsigned nb(int64_t n, int bs) { return (unsigned)std::max<int64_t>(1, (n + bs - 1) / bs); }
 
 // ------------------------------------------------------------ apply
-static void one_level(mdd_prec* P, const double2* v, const double2* add, double2* out,
-                      cudaStream_t s) {
+static void one_level_solve(mdd_prec* P, const double2* v, cudaStream_t s) {
   PrecCore& c = *P->core;
-  mdd_ctx* ctx = c.ctx;
   const int64_t nl = c.sub.nloc;
   if (nl) {
-    k_gather<<<gsb(ctx, nl), 256, 0, s>>>(nl, c.gidx.p, v, c.sub.bloc.p);
-    CK_LAUNCH(ctx);
+    k_gather<<<gsb(c.ctx, nl), 256, 0, s>>>(nl, c.gidx.p, v, c.sub.bloc.p);
+    CK_LAUNCH(c.ctx);
     c.sub.solve(s);
   }
+}
+
+static void one_level_scatter(mdd_prec* P, const double2* add, double2* out, cudaStream_t s) {
+  PrecCore& c = *P->core;
+  mdd_ctx* ctx = c.ctx;
   const bool weighted = P->family != 0;  // ras / impras (precond.py:348)
   k_scatter_owner<<<gsb(ctx, c.ndof), 256, 0, s>>>(c.ndof, c.own_ptr.p, c.own_idx.p,
                                                    weighted ? c.own_w.p : nullptr, c.sub.xloc.p,
                                                    add, out);
   CK_LAUNCH(ctx);
+}
+
+static void one_level(mdd_prec* P, const double2* v, const double2* add, double2* out,
+                      cudaStream_t s) {
+  one_level_solve(P, v, s);
+  one_level_scatter(P, add, out, s);
 }
 
 // out = R0^T A0^{-1} R0 v   (precond.py:357-358)
@@ -421,11 +437,19 @@ void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s)
   }
   const int64_t n = c.ndof;
   double2* gv = c.t1.p;
-  coarse_solve(P, v, gv, s);
   if (P->correction == 0) {  // additive: B1 v + G v
-    one_level(P, v, gv, out, s);
+    // the coarse solve is independent of the subdomain solves: fork it onto a
+    // second stream (a parallel branch when captured into the GMRES graph)
+    CK(cudaEventRecord(c.ev_fork, s));
+    CK(cudaStreamWaitEvent(c.s2, c.ev_fork, 0));
+    coarse_solve(P, v, gv, c.s2);
+    CK(cudaEventRecord(c.ev_join, c.s2));
+    one_level_solve(P, v, s);
+    CK(cudaStreamWaitEvent(s, c.ev_join, 0));
+    one_level_scatter(P, gv, out, s);
     return;
   }
+  coarse_solve(P, v, gv, s);
   // t = v - A_corr G v
   double2* t = c.t2.p;
   spmv_dev_axpby(c.ctx, P->A_corr, gv, t, make_double2(-1.0, 0.0), make_double2(1.0, 0.0), v, s);
@@ -906,6 +930,9 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
       c.cface_idx.upload(gidx2, s);
     }
   }
+  CK(cudaStreamCreateWithFlags(&c.s2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
   c.t1.alloc(ndof);
   c.t2.alloc(ndof);
   c.t3.alloc(ndof);
