@@ -145,7 +145,21 @@ __global__ void __launch_bounds__(kPanelCols) k_panel(const int2* __restrict__ t
   }
 }
 
-// Trailing update of one 64x64 tile:  F[r][c] = (c in K ? 0 : F[r][c]) - W[r][:] F[K][c]
+// FP64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) * B(4x8, col).
+// Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+//            d0,d1 = D[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Trailing update of one 64x64 tile on the FP64 tensor cores:
+//   F[r][c] = (c in K ? 0 : F[r][c]) - W[r][:] F[K][c]
+// Complex product = 4 real DMMA products per 8x8x4 block
+//   (re += Ar Br - Ai Bi, im += Ar Bi + Ai Br).
+// 8 warps, each owning a 16x32 sub-tile = 2x4 DMMA blocks; W (64 x kPB) and
+// the pivot row panel F[K][c0:c0+64] are staged in shared memory.
 __global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
                                                 const NodeDev* __restrict__ nodes,
                                                 const int32_t* __restrict__ act,
@@ -175,36 +189,54 @@ __global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
     Ks[l][cc] = (l < kb && c < m) ? T[(int64_t)(K0 + l) * m + c] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  double2 acc[4][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+  double cre[2][4][2], cim[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
-#pragma unroll 4
-  for (int l = 0; l < kPB; ++l) {
-    double2 wv[4], kv[4];
+    for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
+#pragma unroll 2
+  for (int kk = 0; kk < kPB / 4; ++kk) {
+    double are[2], aim[2], naim[2], bre[4], bim[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) wv[a] = Ws[ty + 16 * a][l];
+    for (int i = 0; i < 2; ++i) {
+      const double2 v = Ws[wr + 8 * i + gid][4 * kk + tig];
+      are[i] = v.x;
+      aim[i] = v.y;
+      naim[i] = -v.y;
+    }
 #pragma unroll
-    for (int b = 0; b < 4; ++b) kv[b] = Ks[l][tx + 16 * b];
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = Ks[4 * kk + tig][wc + 8 * j + gid];
+      bre[j] = v.x;
+      bim[j] = v.y;
+    }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = cfma(wv[a], kv[b], acc[a][b]);
+      for (int j = 0; j < 4; ++j) {
+        dmma884(cre[i][j][0], cre[i][j][1], are[i], bre[j]);
+        dmma884(cre[i][j][0], cre[i][j][1], naim[i], bim[j]);
+        dmma884(cim[i][j][0], cim[i][j][1], are[i], bim[j]);
+        dmma884(cim[i][j][0], cim[i][j][1], aim[i], bre[j]);
+      }
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int r = r0 + ty + 16 * a;
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + wr + 8 * i + gid;
     if (r >= m || (r >= K0 && r < K0 + kb)) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = c0 + tx + 16 * b;
-      if (c >= m) continue;
-      double2* p = T + (int64_t)r * m + c;
-      const double2 old = (c >= K0 && c < K0 + kb) ? make_double2(0.0, 0.0) : *p;
-      *p = csub(old, acc[a][b]);
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + wc + 8 * j + 2 * tig + e;
+        if (c >= m) continue;
+        double2* p = T + (int64_t)r * m + c;
+        const double2 old = (c >= K0 && c < K0 + kb) ? make_double2(0.0, 0.0) : *p;
+        *p = make_double2(old.x - cre[i][j][e], old.y - cim[i][j][e]);
+      }
   }
 }
 

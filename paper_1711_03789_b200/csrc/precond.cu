@@ -281,7 +281,9 @@ __global__ void k_galerkin_reduce(int64_t nct, const int32_t* __restrict__ fptr,
   blk[gid] = acc;
 }
 
-// coloured scatter of complex 6x6 element blocks into a complex CSR
+// coloured scatter of complex 6x6 element blocks into a complex CSR: one warp
+// per cell of a colour; the lanes cover the 36 (distinct) slots of one tet and
+// the cell's 6 tets follow in order (they share slots), so no atomics.
 __global__ void __launch_bounds__(128) k_scatter_blocks(const int32_t* __restrict__ cells, int64_t ncells,
                                                         const int32_t* __restrict__ tet_edges,
                                                         const int32_t* __restrict__ e2d,
@@ -289,21 +291,21 @@ __global__ void __launch_bounds__(128) k_scatter_blocks(const int32_t* __restric
                                                         const int32_t* __restrict__ cols,
                                                         const double2* __restrict__ blk,
                                                         double2* __restrict__ A) {
-  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (ci >= ncells) return;
   const int64_t cell = cells[ci];
   for (int p = 0; p < 6; ++p) {
     const int64_t t = cell * 6 + p;
-    int dof[6];
-    for (int e = 0; e < 6; ++e) dof[e] = e2d[tet_edges[t * 6 + e]];
-    for (int a = 0; a < 6; ++a) {
-      if (dof[a] < 0) continue;
-      for (int b = 0; b < 6; ++b) {
-        if (dof[b] < 0) continue;
-        const int slot = csr_find(rowptr, cols, dof[a], dof[b]);
-        A[slot] = cadd(A[slot], blk[t * 36 + a * 6 + b]);
+    for (int e = lane; e < 36; e += 32) {
+      const int a = e / 6, b = e % 6;
+      const int da = e2d[tet_edges[t * 6 + a]], db = e2d[tet_edges[t * 6 + b]];
+      if (da >= 0 && db >= 0) {
+        const int slot = csr_find(rowptr, cols, da, db);
+        A[slot] = cadd(A[slot], blk[t * 36 + e]);
       }
     }
+    __syncwarp();
   }
 }
 
@@ -511,7 +513,7 @@ static void galerkin_assemble(PrecCore& c, const mdd_coeffs* co, cudaStream_t s)
   for (int col = 0; col < 8; ++col) {
     const int64_t ncell = cs->color_off[col + 1] - cs->color_off[col];
     if (!ncell) continue;
-    k_scatter_blocks<<<nb(ncell, 128), 128, 0, s>>>(
+    k_scatter_blocks<<<nb(ncell * 32, 128), 128, 0, s>>>(
         cs->cells_by_color.p + cs->color_off[col], ncell, cs->tet_edges.p, cs->e2d.p,
         cs->pat->rowptr.p, cs->pat->cols.p, blk.p, reinterpret_cast<double2*>(c.A0->vals.p));
     CK_LAUNCH(ctx);
