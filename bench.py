@@ -40,7 +40,7 @@ CONFIGS = {
     1: dict(name="cfg1", N=40, k=20.0, xi=20.0, p=4, layers=2, nc=10, family="as", corr="additive",
             rhs=("random", 0)),
     3: dict(name="cfg3", N=60, k=30.0, xi=math.sqrt(30.0), p=4, layers=2, nc=15, family="impras",
-            corr="additive", rhs=("random", 0)),
+            corr="hybrid", rhs=("random", 0)),  # ImpHRAS: the paper's coarse combination for ImpRAS
     4: dict(name="cfg4", N=80, k=40.0, xi=0.0, p=8, layers=2, nc=20, family="as", corr="additive",
             rhs=("gauss", 400.0), hetero=True),
 }

@@ -70,27 +70,28 @@ __device__ __forceinline__ void load_tet(const double* __restrict__ verts,
   for (int e = 0; e < 6; ++e) sg[e] = (double)signs[t * 6 + e];
 }
 
-// One thread per cell of one colour class.  Adds S_e, M_e (and, when
-// heterogeneous, the complex a_e = S_e/mu - w M_e, fem.py:253-256) into the
-// CSR slots of the kept DOFs.
+// One warp per cell of one colour class: for each of the cell's 6 Kuhn tets
+// the lanes compute the 36 entries of S_e, M_e (and, when heterogeneous, the
+// complex a_e = S_e/mu - w M_e, fem.py:253-256) in parallel and add them into
+// the CSR slots of the kept DOFs.  The 36 slots of one tet are distinct; the
+// tets of a cell share slots and follow in order; cells of one colour share
+// no edge -> no atomics, fixed summation order.
 __global__ void __launch_bounds__(128) k_assemble_cells(
     const int32_t* __restrict__ cells, int64_t ncells, const double* __restrict__ verts,
     const int32_t* __restrict__ tets, const int32_t* __restrict__ tet_edges,
     const int8_t* __restrict__ signs, const int32_t* __restrict__ e2d,
     const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols, double* __restrict__ S,
     double* __restrict__ M, double2* __restrict__ A, CoefDev co) {
-  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ci = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (ci >= ncells) return;
   const int64_t cell = cells[ci];
   for (int p = 0; p < 6; ++p) {
     const int64_t t = cell * 6 + p;
     double c[4][3], sg[6];
     load_tet(verts, tets, signs, t, c, sg);
-    ElemMats em;
-    element_matrices(c, sg, em);
-    int dof[6];
-#pragma unroll
-    for (int e = 0; e < 6; ++e) dof[e] = e2d[tet_edges[t * 6 + e]];
+    TetGeom g;
+    tet_geometry(c, g);
     double2 w = make_double2(0.0, 0.0);
     double imu = 1.0;
     if (A) {
@@ -100,22 +101,24 @@ __global__ void __launch_bounds__(128) k_assemble_cells(
       w = make_double2(co.k * co.k * eps, co.xi * eps + co.k * sig);
       imu = mu;
     }
-    for (int a = 0; a < 6; ++a) {
-      if (dof[a] < 0) continue;
-      for (int b = 0; b < 6; ++b) {
-        if (dof[b] < 0) continue;
-        const int slot = csr_find(rowptr, cols, dof[a], dof[b]);
-        S[slot] += em.s[a][b];
-        M[slot] += em.m[a][b];
-        if (A) {
-          const double sm = em.s[a][b] / imu;
-          double2 v = A[slot];
-          v.x += sm - w.x * em.m[a][b];
-          v.y += -w.y * em.m[a][b];
-          A[slot] = v;
-        }
+    for (int e = lane; e < 36; e += 32) {
+      const int a = e / 6, b = e % 6;
+      const int da = e2d[tet_edges[t * 6 + a]], db = e2d[tet_edges[t * 6 + b]];
+      if (da < 0 || db < 0) continue;
+      double sv, mv;
+      element_entry(g, sg, a, b, sv, mv);
+      const int slot = csr_find(rowptr, cols, da, db);
+      S[slot] += sv;
+      M[slot] += mv;
+      if (A) {
+        const double sm = sv / imu;
+        double2 v = A[slot];
+        v.x += sm - w.x * mv;
+        v.y += -w.y * mv;
+        A[slot] = v;
       }
     }
+    __syncwarp();
   }
 }
 
@@ -401,7 +404,7 @@ void assemble_system(mdd_space* sp, const mdd_coeffs* co, int impedance, int64_t
   for (int c = 0; c < 8; ++c) {
     const int64_t nc = sp->color_off[c + 1] - sp->color_off[c];
     if (!nc) continue;
-    k_assemble_cells<<<nblocks(nc, 128), 128, 0, s>>>(
+    k_assemble_cells<<<nblocks(nc * 32, 128), 128, 0, s>>>(
         sp->cells_by_color.p + sp->color_off[c], nc, sp->verts.p, sp->tets.p, sp->tet_edges.p,
         sp->signs.p, sp->e2d.p, sp->pat->rowptr.p, sp->pat->cols.p, cS->vals.p, cM->vals.p,
         het ? reinterpret_cast<double2*>(cA->vals.p) : nullptr, cd);

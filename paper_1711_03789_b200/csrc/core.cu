@@ -13,8 +13,91 @@
 #include "mdd_internal.h"
 #include "mdd_kernels.cuh"
 
+#include <map>
+
 namespace mdd {
 static thread_local std::string g_last_error;
+
+// ------------------------------------------------------- caching allocator
+namespace {
+struct DevCache {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;  // (device, size) -> blocks
+  size_t cached = 0;
+  static constexpr size_t kCap = size_t(24) << 30;  // keep at most 24 GB cached
+};
+DevCache& cache() {
+  static DevCache* c = new DevCache();  // never destroyed: outlives static DevBufs
+  return *c;
+}
+size_t bucket(size_t bytes) {
+  if (bytes <= 256) return 256;
+  if (bytes < (size_t(1) << 20)) {
+    size_t b = 256;
+    while (b < bytes) b <<= 1;
+    return b;
+  }
+  const size_t g = size_t(2) << 20;
+  return (bytes + g - 1) / g * g;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  const size_t b = bucket(bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevCache& c = cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.free_blocks.find({dev, b});
+    if (it != c.free_blocks.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      c.cached -= b;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    dev_cache_flush();
+    e = cudaMalloc(&p, b);
+  }
+  CK(e);
+  return p;
+}
+
+void dev_free(void* p, size_t bytes) {
+  if (!p) return;
+  const size_t b = bucket(bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevCache& c = cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    if (c.cached + b <= DevCache::kCap) {
+      c.free_blocks[{dev, b}].push_back(p);
+      c.cached += b;
+      return;
+    }
+  }
+  cudaFree(p);
+}
+
+void dev_cache_flush() {
+  DevCache& c = cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : c.free_blocks) {
+    cudaSetDevice(kv.first.first);
+    for (void* p : kv.second) cudaFree(p);
+  }
+  cudaSetDevice(cur);
+  c.free_blocks.clear();
+  c.cached = 0;
+}
 void set_last_error(const std::string& m) { g_last_error = m; }
 
 std::shared_ptr<mdd_pattern> make_pattern(int64_t nrow, int64_t ncol,

@@ -98,6 +98,33 @@ __device__ __forceinline__ void element_matrices(const double (&c)[4][3], const 
   em.vol = v;
 }
 
+// One entry (a, b) of the oriented S_e, M_e from precomputed geometry
+// (same formulas as element_matrices; used by the warp-per-cell assembly).
+__device__ __forceinline__ void element_entry(const TetGeom& t, const double (&sgn)[6], int e, int f,
+                                              double& s_out, double& m_out) {
+  const int ia = kEA[e], ib = kEB[e], ja = kEA[f], jb = kEB[f];
+  double ce[3], cf[3];
+  ce[0] = 2.0 * (t.g[ia][1] * t.g[ib][2] - t.g[ia][2] * t.g[ib][1]);
+  ce[1] = 2.0 * (t.g[ia][2] * t.g[ib][0] - t.g[ia][0] * t.g[ib][2]);
+  ce[2] = 2.0 * (t.g[ia][0] * t.g[ib][1] - t.g[ia][1] * t.g[ib][0]);
+  cf[0] = 2.0 * (t.g[ja][1] * t.g[jb][2] - t.g[ja][2] * t.g[jb][1]);
+  cf[1] = 2.0 * (t.g[ja][2] * t.g[jb][0] - t.g[ja][0] * t.g[jb][2]);
+  cf[2] = 2.0 * (t.g[ja][0] * t.g[jb][1] - t.g[ja][1] * t.g[jb][0]);
+  auto dot = [&](int i, int j) {
+    return t.g[i][0] * t.g[j][0] + t.g[i][1] * t.g[j][1] + t.g[i][2] * t.g[j][2];
+  };
+  const double v = t.vol;
+  const double o = sgn[e] * sgn[f];
+  const double sv = (ce[0] * cf[0] + ce[1] * cf[1] + ce[2] * cf[2]) * v;
+  const double l_aa = (ia == ja ? 2.0 : 1.0) / 20.0;
+  const double l_ab = (ia == jb ? 2.0 : 1.0) / 20.0;
+  const double l_ba = (ib == ja ? 2.0 : 1.0) / 20.0;
+  const double l_bb = (ib == jb ? 2.0 : 1.0) / 20.0;
+  const double mv = (dot(ib, jb) * l_aa - dot(ib, ja) * l_ab - dot(ia, jb) * l_ba + dot(ia, ja) * l_bb) * v;
+  s_out = sv * o;
+  m_out = mv * o;
+}
+
 // Tangential mass of the three edge functions of a boundary triangle whose
 // vertices p0<p1<p2 are in ascending global order (fem.py:286-316): the
 // three-midpoint rule, exact for the quadratic integrand.

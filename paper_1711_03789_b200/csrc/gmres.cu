@@ -48,8 +48,7 @@ struct ArnoldiArgs {
   double2* w;      // new direction (input: operator output)
   double2* dw;     // D w (weighted) or nullptr
   double2* vin;    // out: copy of V[m] = next operator input
-  double2* partials;  // 2 (parity) x 2 (dot, drift) x G
-  unsigned* flags;    // G publication tags
+  double2* partials;  // (2*maxit+1) publications x 2 (dot, drift) x G, NaN-filled per launch
   double2* H;      // (maxit+1) x maxit, column j at H + j*(maxit+1)
   double2* cs;
   double2* sn;
@@ -134,32 +133,38 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Publish this CTA's two partial sums for step `tag` (thread 0 only): the
-// values first, then a release store of the tag into the CTA's flag.
-__device__ __forceinline__ void publish(double2* part, int G, double2 a, double2 b,
-                                        unsigned* flags, unsigned tag) {
-  part[blockIdx.x] = a;
-  part[G + blockIdx.x] = b;
-  st_release_u32(flags + blockIdx.x, tag);
+// Self-validating all-gather.  Every (step, CTA) pair has its own pair of
+// 16-byte slots, NaN-filled by a memset before the kernel; a CTA publishes
+// by plain stores, and a reader polls a slot until both 8-byte halves are
+// non-NaN (each half is single-copy atomic).  Reading the value *is* the
+// synchronisation: one round trip, no flags, no fences.  Partial sums of
+// finite vectors are finite; a NaN input traps instead of hanging.
+__device__ __forceinline__ void publish(double2* slot_step, int G, double2 a, double2 b) {
+  __stcg(slot_step + blockIdx.x, a);
+  __stcg(slot_step + G + blockIdx.x, b);
 }
 
-// All-gather barrier fused with the reduction: thread t < G acquires CTA t's
-// flag for `tag` and reads CTA t's partials (its own acquire orders the
-// read), all G polls in flight at once; warp 0 then sums the staged values in
-// CTA order (fixed order -> bitwise reproducible) and broadcasts them.  One
-// poll round trip + one read round trip; no atomics.
-__device__ __forceinline__ void gather_sum(const double2* part, int G, const unsigned* flags,
-                                           unsigned tag, double2* sh, double2& dot, double2& dr) {
+__device__ __forceinline__ bool bad2(double2 v) { return isnan(v.x) || isnan(v.y); }
+
+// Thread t < G waits for CTA t's slots of this step (the dot slot, and the
+// drift slot only when `with_drift`: both loads in flight together); warp 0
+// then sums them in CTA order (fixed order -> bitwise reproducible) and
+// broadcasts the result.
+__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, double2* sh,
+                                           double2& dot, double2& dr, bool with_drift = true) {
   double2* stage = sh + 68;  // 2*G slots after the block-reduce scratch
   if ((int)threadIdx.x < G) {
     const int k = threadIdx.x;
     long long spins = 0;
-    // tags grow monotonically: a fast CTA may already have published tag+1
-    while (ld_acquire_u32(flags + k) < tag) {
-      if (++spins > (1ll << 28)) __trap();  // never hang the device on a protocol bug
+    double2 u = __ldcv(slot_step + k);
+    double2 v = with_drift ? __ldcv(slot_step + G + k) : make_double2(0.0, 0.0);
+    while (bad2(u) || bad2(v)) {
+      if (++spins > (1ll << 28)) __trap();  // never hang the device
+      if (bad2(u)) u = __ldcv(slot_step + k);
+      if (bad2(v)) v = __ldcv(slot_step + G + k);
     }
-    stage[k] = __ldcg(part + k);
-    stage[G + k] = __ldcg(part + G + k);
+    stage[k] = u;
+    stage[G + k] = v;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -210,7 +215,8 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const bool do_drift = a.check_drift && m >= 2;  // drift of V_{m-1} vs V_j, j < m-1
   const double2* dvm1 = (weighted ? a.DV : a.V) + (int64_t)(m - 1) * n;
   const int nsteps = 2 * m;
-  const unsigned tbase = ((unsigned)m << 16) + 1u;  // tag(s) = tbase + (s + 1), s >= -1
+  // slots of publication k (k = s+1 for step s; k = 0 for the initial dot)
+  auto slots = [&](int k) { return a.partials + (int64_t)k * 2 * G; };
   for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
   // X_t = V_{t mod m} for t < nsteps; X_nsteps = w (the norm)
   auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n; };
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
       }
     }
     block_sum2x2(acc, dacc, red);
-    if (threadIdx.x == 0) publish(a.partials, G, acc, dacc, a.flags, tbase);
+    if (threadIdx.x == 0) publish(slots(0), G, acc, dacc);
     if constexpr (REG) {
       const double2* x1 = xvec(1);
 #pragma unroll
@@ -260,7 +266,8 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   for (int s = 0; s < nsteps; ++s) {
     const int j = s % m;
     double2 h, d;
-    gather_sum(a.partials + (s & 1) * 2 * G, G, a.flags, tbase + (unsigned)s, red, h, d);
+    // the drift slot carries data only in the first pass (s <= m-2)
+    gather_sum(slots(s), G, red, h, d, do_drift && s < m - 1);
     if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));  // drift term of X_s = V_s
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
@@ -298,8 +305,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
       }
     }
     block_sum2x2(acc, dacc, red);
-    if (threadIdx.x == 0) publish(a.partials + ((s + 1) & 1) * 2 * G, G, acc, dacc, a.flags,
-                                  tbase + (unsigned)(s + 1));
+    if (threadIdx.x == 0) publish(slots(s + 1), G, acc, dacc);
     if constexpr (REG) {
       if (s + 2 < nsteps) {  // preload X_{s+2} while the other CTAs arrive
         const double2* x2 = xvec(s + 2);
@@ -312,8 +318,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     }
   }
   double2 hn2, dummy;
-  gather_sum(a.partials + (nsteps & 1) * 2 * G, G, a.flags, tbase + (unsigned)nsteps, red, hn2,
-             dummy);
+  gather_sum(slots(nsteps), G, red, hn2, dummy, false);
   const double hlast = sqrt(fmax(hn2.x, 0.0));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
@@ -626,9 +631,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
   if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
-  DevBuf<double2> partials(4 * (size_t)G);
-  DevBuf<unsigned> flags(G);
-  flags.zero(s);
+  const size_t part_elems = (size_t)(2 * maxit + 1) * 2 * G;
+  DevBuf<double2> partials(part_elems);
   int* hstatus = nullptr;
   CK(cudaHostAlloc(&hstatus, sizeof(int) * 4, cudaHostAllocMapped));
   struct StFree {
@@ -648,7 +652,6 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.dw = weighted ? dw.p : nullptr;
   aa.vin = vin.p;
   aa.partials = partials.p;
-  aa.flags = flags.p;
   aa.H = H.p;
   aa.cs = cs.p;
   aa.sn = sn.p;
@@ -662,6 +665,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.dstatus = dstat.p;
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
+    // NaN-fill the publication slots (0xFF bytes are a NaN pattern)
+    CK(cudaMemsetAsync(partials.p, 0xFF, part_elems * sizeof(double2), s));
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(G);
     lc.blockDim = dim3(kArnThreads);

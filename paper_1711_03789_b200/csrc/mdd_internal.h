@@ -62,7 +62,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   }                                                \
   return MDD_OK;
 
-// ----------------------------------------------------------- device buffer
+// ----------------------------------------------------------- device memory
+// Caching allocator: freed blocks go to size-bucketed free lists and are
+// reused, so steady-state solves perform no cudaMalloc/cudaFree (cudaFree
+// synchronises the device).  On allocation failure the cache is flushed and
+// the allocation retried.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+void dev_cache_flush();
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -80,10 +88,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }
