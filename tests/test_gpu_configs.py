@@ -66,3 +66,66 @@ def test_cfg1_properties(gpu):
     r = np.linalg.norm(rhs - a @ rep.x) / np.linalg.norm(rhs)
     assert r == pytest.approx(rep.residual_history[-1], rel=1e-5)
     assert np.all(np.diff(rep.residual_history) <= 0)
+
+
+def _oracle_case(N, p, L, nc, k, xi, family, corr, hetero=False, seed=0):
+    """Mid-size problem of a BASELINE config's kind, solved by device and oracle."""
+    from oracle import maxwell_oracle as O
+    from paper_1711_03789_b200 import decomp, fem, mesh
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(N), "pec")
+    m = s.mesh
+    eps = mu = 1.0
+    sigma = 0.0
+    if hetero:
+        rng = np.random.default_rng(seed)
+        blk = np.clip((m.barycenters() * 4).astype(int), 0, 3)
+        bid = (blk[:, 0] * 4 + blk[:, 1]) * 4 + blk[:, 2]
+        eps = (1.0 + 3.0 * rng.random(64))[bid]
+        sigma = (k * (0.5 + 1.5 * rng.random(64)))[bid] / k
+    coeffs = fem.Coefficients(k=k, xi=xi, eps=eps, mu=mu, sigma=sigma)
+    rng = np.random.default_rng(seed + 1)
+    b = (rng.standard_normal(s.ndof) + 1j * rng.standard_normal(s.ndof)) / np.sqrt(2.0)
+    d = decomp.build_decomposition(s, p, L, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(nc), "pec"))
+    md = {kk: getattr(m, kk) for kk in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs", "boundary_faces")}
+    A = O.assemble(md, s.edge_to_dof, s.ndof, k, xi, eps=eps, mu=mu, sigma=sigma)["A"]
+    if family == "impras":
+        sets = decomp.impedance_dof_sets(s, d.elements)
+        pou = decomp.build_pou(sets, s.ndof)
+        loc = [O.impedance_local_matrix(md, s.edge_to_dof, s.kept_edges, g, e, k, xi, eps=eps, mu=mu, sigma=sigma)
+               for g, e in zip(sets, d.elements)]
+    else:
+        sets, pou, loc = d.dofs, d.pou, O.minors(A, d.dofs)
+    r0 = d.coarse.R0
+    P = O.Schwarz(sets, pou, loc, family, "two", corr, R0=r0, A0=(r0 @ A @ r0.T).tocsr(), A_corr=A,
+                  ndof=s.ndof, solver="sparse")
+    return s, coeffs, b, d, A, P
+
+
+@pytest.mark.parametrize("name,args", [
+    ("cfg3-kind: ImpHRAS, xi=sqrt(k)", dict(N=16, p=4, L=2, nc=4, k=8.0, xi=np.sqrt(8.0), family="impras", corr="hybrid")),
+    ("cfg4-kind: heterogeneous AS2, xi=0", dict(N=16, p=4, L=2, nc=4, k=8.0, xi=0.0, family="as", corr="additive", hetero=True)),
+])
+def test_config_kinds_vs_oracle(gpu, name, args):
+    """The device solve of each BASELINE config's algorithm variant matches the
+    oracle (reference restatement) at a size the oracle finishes in seconds:
+    preconditioner map to 1e-10, iteration count +-1, solution to 1e-8."""
+    from oracle import maxwell_oracle as O
+    from paper_1711_03789_b200 import fem, krylov, precond
+
+    s, coeffs, b, d, A, P = _oracle_case(**args)
+    prob = fem.assemble(s, coeffs)
+    st = precond.setup(prob, d, precond.PreconditionerSpec(args["family"], "two", args["corr"], xi_prec=args["xi"]),
+                       lu_cap=None)
+    v = np.random.default_rng(3).standard_normal(s.ndof) * (1 - 0.5j)
+    assert rel(st.apply(v), P.apply(v)) <= 1e-10
+    rep = krylov.gmres(prob.A, b, precond=st.apply, config=krylov.KrylovConfig(tol=1e-6, maxit=200))
+    x, hist, it, conv = O.gmres(A, b, P, tol=1e-6, maxit=200)
+    assert rep.converged == conv
+    assert abs(rep.iterations - it) <= 1
+    k = min(len(hist), len(rep.residual_history))
+    # rounding differences grow slowly over a long run: strict early, looser tail
+    assert np.allclose(rep.residual_history[:20], hist[:20], rtol=1e-8)
+    assert np.allclose(rep.residual_history[:k], hist[:k], rtol=1e-4)
+    if conv:
+        assert rel(rep.x, x) <= 1e-8
