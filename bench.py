@@ -84,6 +84,10 @@ def build_problem(c, seed=0):
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
+    """One long-lived `nvidia-smi -lms 200` process, started before the timed
+    region and stopped after it (B200_PROFILING.md's clocks line): a single
+    fork outside the timed region instead of one per sample."""
+
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
              "clocks_event_reasons.sw_power_cap"
@@ -91,28 +95,32 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.samples = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:  # noqa: BLE001
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:  # noqa: BLE001
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
 
     def summary(self):
         if not self.samples:
@@ -249,7 +257,7 @@ def run_mine(args, rank, world):
     ctx.synchronize()
     launches0 = ctx.kernel_launches()
     ms_steps, phases, reps = [], [], []
-    host = np.zeros(3)
+    host = np.zeros(4)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         for _ in range(args.steps):
             ctx.record(0)
@@ -258,7 +266,7 @@ def run_mine(args, rank, world):
             ms = ctx.elapsed_ms(0, 3)
             ms_steps.append(ms)
             phases.append((ctx.elapsed_ms(0, 1), ctx.elapsed_ms(1, 2), ctx.elapsed_ms(2, 3)))
-            host += np.array(ctx.timers()[3:6])
+            host += np.array(ctx.timers()[3:7])
             reps.append(rep)
     ctx.synchronize()
     dist_barrier(world)
@@ -283,7 +291,7 @@ def run_mine(args, rank, world):
     its = rep.iterations
     # roofline of the dominant kernel family
     t_op, t_prec, t_arn = timers
-    h_setup, h_loop, h_final = host / args.steps
+    h_setup, h_loop, h_final, h_graph = host / args.steps
     fe = stats["factor_entries"]
     sum_loc = stats["sum_local_dofs"]
     r0nnz = dec.coarse.R0.nnz
@@ -326,11 +334,13 @@ def run_mine(args, rank, world):
             "l2": "working set (V basis, factors) >> 126 MB L2; no flush needed",
         },
         "iters_per_s": its / (ms_step / 1e3),
+        "ms_steps": [round(x, 3) for x in ms_steps],
         "phases_ms": {"assemble_A": float(np.mean([p[0] for p in phases])),
                       "assemble_Aprec_factor": float(np.mean([p[1] for p in phases])),
                       "gmres": float(np.mean([p[2] for p in phases])),
                       "gmres_spmv": t_op, "gmres_precond": t_prec, "gmres_arnoldi": t_arn,
-                      "gmres_host_setup": h_setup, "gmres_host_loop": h_loop, "gmres_host_final": h_final},
+                      "gmres_host_setup": h_setup, "gmres_host_loop": h_loop, "gmres_host_final": h_final,
+                      "gmres_graph_build": h_graph},
         "setup_s": {"decomposition": t_dec, "first_setup_incl_symbolic": t_setup},
         "factor": {k: stats[k] for k in ("n_fronts", "max_front", "factor_entries", "factor_flops", "factor_ms")},
         "gpu_launches": int(launches),

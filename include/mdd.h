@@ -56,8 +56,10 @@ void mdd_ctx_destroy(mdd_ctx* ctx);
 int mdd_ctx_synchronize(mdd_ctx* ctx);
 /* number of this library's kernels launched on the context so far */
 int64_t mdd_ctx_kernel_launches(const mdd_ctx* ctx);
-/* device-time of the last mdd_gmres phases (ms): [assembly-free] spmv, precond, arnoldi */
-int mdd_ctx_timers(const mdd_ctx* ctx, double* out6);
+/* timers of the last mdd_gmres (ms): [0..2] device time of spmv / precond /
+ * arnoldi (timing mode only), [3..5] host wall of setup / loop / finalisation,
+ * [6] CUDA-graph construction */
+int mdd_ctx_timers(const mdd_ctx* ctx, double* out8);
 int mdd_ctx_set_timing(mdd_ctx* ctx, int enable);
 /* CUDA events on the context stream (slot 0..15) for device-side timing */
 int mdd_ctx_event_record(mdd_ctx* ctx, int slot);

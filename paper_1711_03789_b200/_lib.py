@@ -232,7 +232,7 @@ class Context:
         return ms.value
 
     def timers(self):
-        out = (C.c_double * 6)()
+        out = (C.c_double * 8)()
         check(lib.mdd_ctx_timers(self.handle, out))
         return list(out)
 

@@ -277,6 +277,7 @@ void mdd_ctx_destroy(mdd_ctx* ctx) {
   for (auto& e : ctx->events)
     if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->mapped_status) cudaFreeHost(ctx->mapped_status);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -289,9 +290,9 @@ int mdd_ctx_synchronize(mdd_ctx* ctx) {
 
 int64_t mdd_ctx_kernel_launches(const mdd_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-int mdd_ctx_timers(const mdd_ctx* ctx, double* out6) {
+int mdd_ctx_timers(const mdd_ctx* ctx, double* out8) {
   MDD_API_BEGIN
-  for (int i = 0; i < 6; ++i) out6[i] = ctx->timers[i];
+  for (int i = 0; i < 8; ++i) out8[i] = ctx->timers[i];
   MDD_API_END
 }
 

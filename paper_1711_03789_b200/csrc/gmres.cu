@@ -37,7 +37,7 @@ namespace mdd {
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 
 constexpr int kArnThreads = 512;
-constexpr int kMaxArnCTAs = 160;  // grid <= #SMs (148 on B200)
+constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
 
 struct ArnoldiArgs {
   int64_t n;
@@ -146,46 +146,43 @@ __device__ __forceinline__ void publish(double2* slot_step, int G, double2 a, do
 
 __device__ __forceinline__ bool bad2(double2 v) { return isnan(v.x) || isnan(v.y); }
 
-constexpr int kArnWarps = kArnThreads / 32;
-constexpr int kGatherPerLane = (kMaxArnCTAs + 31) / 32;
-
-// Warp 0 only: wait until all G CTAs' slots of one publication are filled
-// (all loads in flight together, re-polling only the empty ones) and sum
-// them in CTA order (lane-strided then xor tree: fixed order -> bitwise
-// reproducible).  Partial sums of finite vectors are finite; a NaN input
-// traps instead of hanging.
-__device__ __forceinline__ void warp_gather(const double2* slot, int G, bool with_drift,
-                                            double2& dot, double2& dr) {
-  const int lane = threadIdx.x & 31;
-  double2 u[kGatherPerLane], v[kGatherPerLane];
-#pragma unroll
-  for (int q = 0; q < kGatherPerLane; ++q) {
-    const int k = lane + 32 * q;
-    u[q] = k < G ? __ldcv(slot + k) : make_double2(0.0, 0.0);
-    v[q] = (k < G && with_drift) ? __ldcv(slot + G + k) : make_double2(0.0, 0.0);
+// Thread t < G waits for CTA t's slots of this step (the dot slot, and the
+// drift slot only when `with_drift`: both loads in flight together); warp 0
+// then sums them in CTA order (fixed order -> bitwise reproducible) and
+// broadcasts the result.
+__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, double2* sh,
+                                           double2& dot, double2& dr, bool with_drift = true) {
+  double2* stage = sh + 68;  // 2*G slots after the block-reduce scratch
+  if ((int)threadIdx.x < G) {
+    const int k = threadIdx.x;
+    long long spins = 0;
+    double2 u = __ldcv(slot_step + k);
+    double2 v = with_drift ? __ldcv(slot_step + G + k) : make_double2(0.0, 0.0);
+    while (bad2(u) || bad2(v)) {
+      if (++spins > (1ll << 28)) __trap();  // never hang the device
+      if (bad2(u)) u = __ldcv(slot_step + k);
+      if (bad2(v)) v = __ldcv(slot_step + G + k);
+    }
+    stage[k] = u;
+    stage[G + k] = v;
   }
-  long long spins = 0;
-  for (;;) {
-    bool ok = true;
-#pragma unroll
-    for (int q = 0; q < kGatherPerLane; ++q) ok = ok && !bad2(u[q]) && !bad2(v[q]);
-    if (__all_sync(0xffffffffu, ok)) break;
-    if (++spins > (1ll << 28)) __trap();  // never hang the device
-#pragma unroll
-    for (int q = 0; q < kGatherPerLane; ++q) {
-      const int k = lane + 32 * q;
-      if (k < G && bad2(u[q])) u[q] = __ldcv(slot + k);
-      if (k < G && with_drift && bad2(v[q])) v[q] = __ldcv(slot + G + k);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < G; k += 32) {
+      x = cadd(x, stage[k]);
+      y = cadd(y, stage[G + k]);
+    }
+    x = warp_sum2(x);
+    y = warp_sum2(y);
+    if (threadIdx.x == 0) {
+      sh[66] = x;
+      sh[67] = y;
     }
   }
-  double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int q = 0; q < kGatherPerLane; ++q) {
-    x = cadd(x, u[q]);
-    y = cadd(y, v[q]);
-  }
-  dot = warp_sum2(x);
-  dr = warp_sum2(y);
+  __syncthreads();
+  dot = sh[66];
+  dr = sh[67];
 }
 
 __device__ __forceinline__ double2 cdotc_acc(double2 acc, double2 x, double2 y) {  // acc + conj(x) y
@@ -197,49 +194,15 @@ __device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // 
   return make_double2(w.x - (h.x * v.x - h.y * v.y), w.y - (h.x * v.y + h.y * v.x));
 }
 
-// One cross-CTA reduction: per-warp shuffle sums -> barrier -> warp 0 sums the
-// warps, publishes this CTA's partials, gathers all CTAs' -> barrier.  Two
-// block barriers per MGS step; the callers issue their next-step loads
-// before calling, so those loads overlap the cross-CTA wait.
-__device__ __forceinline__ void allreduce2(double2 acc, double2 dacc, bool with_drift,
-                                           double2* slot, int G, double2 (*wpart)[2],
-                                           double2* hcast, double2& h, double2& d) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  acc = warp_sum2(acc);
-  if (with_drift) dacc = warp_sum2(dacc);
-  if (lane == 0) {
-    wpart[warp][0] = acc;
-    wpart[warp][1] = dacc;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    double2 a = lane < kArnWarps ? wpart[lane][0] : make_double2(0.0, 0.0);
-    double2 b = lane < kArnWarps ? wpart[lane][1] : make_double2(0.0, 0.0);
-    a = warp_sum2(a);
-    b = warp_sum2(b);
-    if (lane == 0) publish(slot, G, a, b);
-    double2 hh, dd;
-    warp_gather(slot, G, with_drift, hh, dd);
-    if (lane == 0) {
-      hcast[0] = hh;
-      hcast[1] = dd;
-    }
-  }
-  __syncthreads();
-  h = hcast[0];
-  d = hcast[1];
-}
-
 // REG: unweighted, every CTA slice fits in registers (slice <= kArnThreads*kArnE):
-// w stays in registers for the whole kernel and the basis slice needed two
-// steps ahead is loaded into registers before each cross-CTA wait.
-// Otherwise: w and the basis are streamed from L2/HBM with a TMA bulk L2
-// prefetch of the slice needed two steps ahead.
+// w stays in registers for the whole kernel and the basis slice of step s+2
+// is loaded into registers right after publishing step s, so its latency
+// overlaps the barrier wait.  Otherwise: w and the basis are streamed from
+// L2/HBM with a TMA bulk L2 prefetch of the step s+2 slice.
 template <bool REG>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   extern __shared__ double2 col[];  // m+1, identical in every CTA
-  __shared__ double2 wpart[kArnWarps][2];
-  __shared__ double2 hcast[2];
+  __shared__ double2 red[68 + 2 * kMaxArnCTAs];
   const int G = gridDim.x;
   const int m = *a.iter + 1;
   const int64_t n = a.n;
@@ -252,48 +215,59 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const bool do_drift = a.check_drift && m >= 2;  // drift of V_{m-1} vs V_j, j < m-1
   const double2* dvm1 = (weighted ? a.DV : a.V) + (int64_t)(m - 1) * n;
   const int nsteps = 2 * m;
+  // slots of publication k (k = s+1 for step s; k = 0 for the initial dot)
+  auto slots = [&](int k) { return a.partials + (int64_t)k * 2 * G; };
   for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
-  // publication p carries the partial dot with X_p (X_t = V_{t mod m}, X_nsteps = w),
-  // plus the drift partial <X_p, DV_{m-1}> when p < m-1
-  auto slots = [&](int p) { return a.partials + (int64_t)p * 2 * G; };
+  // X_t = V_{t mod m} for t < nsteps; X_nsteps = w (the norm)
   auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n; };
 
   double2 W[kArnE], XN[kArnE], XNN[kArnE];
   double2* DM = col + (a.maxit + 1);  // drift vector slice in shared memory (REG path)
-  double2 h, d;
+  if constexpr (REG) {
+#pragma unroll
+    for (int k = 0; k < kArnE; ++k) {
+      const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+      const bool ok = i < hi;
+      W[k] = ok ? w[i] : make_double2(0.0, 0.0);
+      XN[k] = ok ? a.V[i] : make_double2(0.0, 0.0);
+      DM[threadIdx.x + k * kArnThreads] = (ok && do_drift) ? dvm1[i] : make_double2(0.0, 0.0);
+    }
+  } else if (threadIdx.x == 0) {
+    prefetch_l2(xvec(1) + lo, len * 16);
+  }
+  // iteration -1: dot with X_0 (+ drift of X_0 if 0 < m-1)
   {
     double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
     if constexpr (REG) {
 #pragma unroll
       for (int k = 0; k < kArnE; ++k) {
-        const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
-        const bool ok = i < hi;
-        W[k] = ok ? w[i] : make_double2(0.0, 0.0);
-        XN[k] = ok ? a.V[i] : make_double2(0.0, 0.0);
-        const double2 dm = (ok && do_drift) ? dvm1[i] : make_double2(0.0, 0.0);
-        DM[threadIdx.x + k * kArnThreads] = dm;
         acc = cdotc_acc(acc, XN[k], W[k]);
-        if (do_drift) dacc = cdotc_acc(dacc, XN[k], dm);
-      }
-      const double2* x1 = xvec(1);
-#pragma unroll
-      for (int k = 0; k < kArnE; ++k) {
-        const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
-        XNN[k] = i < hi ? x1[i] : make_double2(0.0, 0.0);
+        if (do_drift) dacc = cdotc_acc(dacc, XN[k], DM[threadIdx.x + k * kArnThreads]);
       }
     } else {
-      if (threadIdx.x == 0) prefetch_l2(xvec(1) + lo, len * 16);
       for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double2 x = a.V[i];
         acc = cdotc_acc(acc, x, dw[i]);
         if (do_drift) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
-    allreduce2(acc, dacc, do_drift && 0 < m - 1, slots(0), G, wpart, hcast, h, d);
+    block_sum2x2(acc, dacc, red);
+    if (threadIdx.x == 0) publish(slots(0), G, acc, dacc);
+    if constexpr (REG) {
+      const double2* x1 = xvec(1);
+#pragma unroll
+      for (int k = 0; k < kArnE; ++k) {
+        const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+        XNN[k] = i < hi ? x1[i] : make_double2(0.0, 0.0);
+      }
+    }
   }
   double dmax = 0.0;
   for (int s = 0; s < nsteps; ++s) {
     const int j = s % m;
+    double2 h, d;
+    // the drift slot carries data only in the first pass (s <= m-2)
+    gather_sum(slots(s), G, red, h, d, do_drift && s < m - 1);
     if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));  // drift term of X_s = V_s
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
@@ -311,14 +285,6 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         acc = cdotc_acc(acc, x, W[k]);
         if (drift_next) dacc = cdotc_acc(dacc, x, DM[threadIdx.x + k * kArnThreads]);
         XN[k] = XNN[k];
-      }
-      if (s + 2 < nsteps) {  // X_{s+2}: loads in flight across the cross-CTA wait
-        const double2* x2 = xvec(s + 2);
-#pragma unroll
-        for (int k = 0; k < kArnE; ++k) {
-          const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
-          XNN[k] = i < hi ? x2[i] : make_double2(0.0, 0.0);
-        }
       }
     } else {
       const double2* vj = a.V + (int64_t)j * n;
@@ -338,9 +304,23 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         if (drift_next) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
-    allreduce2(acc, dacc, drift_next, slots(s + 1), G, wpart, hcast, h, d);
+    block_sum2x2(acc, dacc, red);
+    if (threadIdx.x == 0) publish(slots(s + 1), G, acc, dacc);
+    if constexpr (REG) {
+      if (s + 2 < nsteps) {  // preload X_{s+2} while the other CTAs arrive
+        const double2* x2 = xvec(s + 2);
+#pragma unroll
+        for (int k = 0; k < kArnE; ++k) {
+          const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
+          XNN[k] = i < hi ? x2[i] : make_double2(0.0, 0.0);
+        }
+      }
+    }
   }
-  const double hlast = sqrt(fmax(h.x, 0.0));  // h of publication nsteps = Re vdot(w, dw)
+  double2 hn2, dummy;
+  gather_sum(slots(nsteps), G, red, hn2, dummy, false);
+  const double hlast = sqrt(fmax(hn2.x, 0.0));
+  __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
   __syncthreads();
   double cmax = 0.0;
@@ -653,12 +633,10 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
   const size_t part_elems = (size_t)(2 * maxit + 1) * 2 * G;
   DevBuf<double2> partials(part_elems);
-  int* hstatus = nullptr;
-  CK(cudaHostAlloc(&hstatus, sizeof(int) * 4, cudaHostAllocMapped));
-  struct StFree {
-    int* p;
-    ~StFree() { cudaFreeHost(p); }
-  } sf{hstatus};
+  // host-mapped status word, allocated once per context (cudaHostAlloc and
+  // cudaFreeHost are slow and cudaFreeHost synchronises the device)
+  if (!ctx->mapped_status) CK(cudaHostAlloc(&ctx->mapped_status, sizeof(int) * 4, cudaHostAllocMapped));
+  int* hstatus = ctx->mapped_status;
   int* hstatus_dev = nullptr;
   CK(cudaHostGetDevicePointer(&hstatus_dev, hstatus, 0));
 
@@ -731,6 +709,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (use_graph) {
     const int64_t l0 = ctx->launches;
     // device-side while loop: no host round trip per iteration
+    const auto tg0 = std::chrono::steady_clock::now();
     cudaGraph_t graph;
     CK(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle cond;
@@ -755,6 +734,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     body_launches = ctx->launches - l0;
     cudaGraphExec_t exec;
     CK(cudaGraphInstantiate(&exec, graph, 0));
+    ctx->timers[6] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count();
     CK(cudaGraphLaunch(exec, s));
     CK(cudaStreamSynchronize(s));
     cudaGraphExecDestroy(exec);

@@ -124,7 +124,8 @@ struct mdd_ctx {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   bool timing = false;
-  double timers[6] = {0, 0, 0, 0, 0, 0};
+  double timers[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int* mapped_status = nullptr;  // host-mapped GMRES status word
   // pinned staging used by host-pointer entry points
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
