@@ -299,33 +299,32 @@ __global__ void __launch_bounds__(256) k_fwd(const int4* __restrict__ tasks,
                                              const double2* __restrict__ fronts,
                                              const double2* __restrict__ bloc,
                                              double2* __restrict__ fpst, double2* __restrict__ uvec) {
-  extern __shared__ double2 fp[];
+  extern __shared__ double2 fp[];  // [np pivots | children's contributions to rows r0..r1)
   const int4 tk = tasks[blockIdx.x];
   const NodeDev nd = nodes[tk.x];
   const int r0 = tk.y, r1 = tk.z;
   const int np = nd.np, m = nd.m;
   const int64_t base = (int64_t)nd.mat_off + nd.pivb;
   const int32_t* ga = gmap_abs + nd.gmap_off;
-  for (int q = threadIdx.x; q < np; q += blockDim.x) {
-    double2 f = bloc[base + q];
+  double2* fu = fp + np;
+  // one prologue gathers both the pivot rhs and the children's contributions
+  // to this task's update rows (all 2-deep load chains in flight together)
+  const int nrow = r1 - r0;
+  for (int q = threadIdx.x; q < np + nrow; q += blockDim.x) {
+    const int pos = q < np ? q : np + r0 + (q - np);
+    double2 f = q < np ? bloc[base + q] : make_double2(0.0, 0.0);
     for (int ci = 0; ci < nd.nch; ++ci) {
-      const int g = ga[(int64_t)ci * m + q];
+      const int g = ga[(int64_t)ci * m + pos];
       if (g >= 0) f = cadd(f, uvec[g]);
     }
     fp[q] = f;
-    if (r0 == 0) fpst[base + q] = f;
+    if (q < np && r0 == 0) fpst[base + q] = f;
   }
   __syncthreads();
   if (r0 >= r1) return;
   const double2* TU = fronts + nd.front_off + (int64_t)np * m;  // row u of F_UP
-  gemv_rows_any(TU, m, r0, r1, np, fp, [&](int u, double2 acc) {
-    double2 fu = make_double2(0.0, 0.0);
-    for (int ci = 0; ci < nd.nch; ++ci) {
-      const int g = ga[(int64_t)ci * m + np + u];
-      if (g >= 0) fu = cadd(fu, uvec[g]);
-    }
-    uvec[nd.uvec_off + u] = csub(fu, acc);
-  });
+  gemv_rows_any(TU, m, r0, r1, np, fp,
+                [&](int u, double2 acc) { uvec[nd.uvec_off + u] = csub(fu[u - r0], acc); });
 }
 
 // backward: x_P = -(F_PP fp + F_PU x_U)
@@ -701,7 +700,7 @@ int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {
 }
 
 void FrontPlan::solve(cudaStream_t s) {
-  const size_t fsm = sizeof(double2) * std::max(1, max_np);
+  const size_t fsm = sizeof(double2) * (std::max(1, max_np) + 512);  // + task rows (<= 512)
   const size_t bsm = sizeof(double2) * std::max(1, max_m);
   for (int L = 0; L < nlevels; ++L) {
     const int64_t n = lev_fwd_off[L + 1] - lev_fwd_off[L];
