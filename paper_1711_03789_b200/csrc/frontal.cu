@@ -19,7 +19,8 @@
 namespace mdd {
 
 // ------------------------------------------------------------ kernels
-// warp per (node,row): F[row][:] = sum_children S_child[g(row)][g(:)]
+// warp per (node,row): F[row][:] = sum_children S_child[g(row)][g(:)], one
+// write per element (extend-add in gather form: no atomics)
 __global__ void __launch_bounds__(256) k_front_init(const int2* __restrict__ tasks, int64_t ntask,
                                                     const NodeDev* __restrict__ nodes,
                                                     const int32_t* __restrict__ children,
@@ -32,16 +33,37 @@ __global__ void __launch_bounds__(256) k_front_init(const int2* __restrict__ tas
   const NodeDev nd = nodes[tk.x];
   const int r = tk.y, m = nd.m;
   double2* row = fronts + nd.front_off + (int64_t)r * m;
-  for (int q = lane; q < m; q += 32) row[q] = make_double2(0.0, 0.0);
-  for (int ci = 0; ci < nd.nch; ++ci) {
-    const NodeDev ch = nodes[children[nd.child_off + ci]];
+  constexpr int kMaxCh = 4;
+  const double2* S[kMaxCh];
+  const int32_t* G[kMaxCh];
+  int nsrc = 0;
+  for (int ci = 0; ci < nd.nch && nsrc < kMaxCh; ++ci) {
     const int32_t* g = gmap + nd.gmap_off + (int64_t)ci * m;
     const int gr = g[r];
     if (gr < 0) continue;
-    const double2* S = fronts + ch.front_off + (int64_t)(ch.np + gr) * ch.m + ch.np;
+    const NodeDev ch = nodes[children[nd.child_off + ci]];
+    S[nsrc] = fronts + ch.front_off + (int64_t)(ch.np + gr) * ch.m + ch.np;
+    G[nsrc] = g;
+    ++nsrc;
+  }
+  for (int q = lane; q < m; q += 32) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < nsrc; ++k) {
+      const int gq = G[k][q];
+      if (gq >= 0) acc = cadd(acc, S[k][gq]);
+    }
+    row[q] = acc;
+  }
+  // children beyond kMaxCh (not produced by bisection; kept for generality)
+  for (int ci = kMaxCh; ci < nd.nch; ++ci) {
+    const int32_t* g = gmap + nd.gmap_off + (int64_t)ci * m;
+    const int gr = g[r];
+    if (gr < 0) continue;
+    const NodeDev ch = nodes[children[nd.child_off + ci]];
+    const double2* Sx = fronts + ch.front_off + (int64_t)(ch.np + gr) * ch.m + ch.np;
     for (int q = lane; q < m; q += 32) {
       const int gq = g[q];
-      if (gq >= 0) row[q] = cadd(row[q], S[gq]);
+      if (gq >= 0) row[q] = cadd(row[q], Sx[gq]);
     }
   }
 }
@@ -57,40 +79,54 @@ __global__ void k_front_scatter(int64_t n, const int64_t* __restrict__ pos,
 }
 
 // In-place Gauss-Jordan inverse of the kb x kb pivot block (no pivoting),
-// padded with the identity to 32x32; tracks pivot magnitudes.
-__global__ void __launch_bounds__(1024) k_invert(const NodeDev* __restrict__ nodes,
-                                                 const int32_t* __restrict__ act, int step,
-                                                 const double2* __restrict__ fronts,
-                                                 double2* __restrict__ pbuf,
-                                                 double* __restrict__ pivstat) {
-  __shared__ double2 P[kPB][kPB + 1];
-  const int node = act[blockIdx.x];
+// padded with the identity to 32x32; tracks pivot magnitudes.  One warp per
+// node (kInvWarps nodes per CTA), the block in shared memory, lane i owning
+// row i: per pivot, lane j scales column j of the pivot row, then every lane
+// eliminates its own row with the broadcast pivot row.  Warp-synchronous only.
+constexpr int kInvWarps = 4;
+__global__ void __launch_bounds__(32 * kInvWarps) k_invert(const NodeDev* __restrict__ nodes,
+                                                           const int32_t* __restrict__ act,
+                                                           int nact, int step,
+                                                           const double2* __restrict__ fronts,
+                                                           double2* __restrict__ pbuf,
+                                                           double* __restrict__ pivstat) {
+  extern __shared__ double2 invsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ai = blockIdx.x * kInvWarps + w;
+  if (ai >= nact) return;  // warp-uniform; no block barriers below
+  double2(*P)[kPB + 1] = reinterpret_cast<double2(*)[kPB + 1]>(invsm + w * kPB * (kPB + 1));
+  const int node = act[ai];
   const NodeDev nd = nodes[node];
   const int K0 = step * kPB;
   const int kb = min(kPB, nd.np - K0);
-  const int i = threadIdx.x >> 5, j = threadIdx.x & 31;
   const double2* T = fronts + nd.front_off;
-  P[i][j] = (i < kb && j < kb) ? T[(int64_t)(K0 + i) * nd.m + K0 + j]
-                               : make_double2(i == j ? 1.0 : 0.0, 0.0);
-  __syncthreads();
+  for (int r = 0; r < kPB; ++r)
+    P[r][lane] = (r < kb && lane < kb) ? T[(int64_t)(K0 + r) * nd.m + K0 + lane]
+                                       : make_double2(r == lane ? 1.0 : 0.0, 0.0);
+  __syncwarp();
   double pmin = INFINITY, pmax = 0.0;
   for (int p = 0; p < kb; ++p) {
     const double2 piv = P[p][p];
-    const double2 aip = P[i][p];
-    __syncthreads();
-    if (i == p) P[p][j] = cdiv(j == p ? make_double2(1.0, 0.0) : P[p][j], piv);
-    __syncthreads();
-    if (i != p) {
-      const double2 base = (j == p) ? make_double2(0.0, 0.0) : P[i][j];
-      P[i][j] = csub(base, cmul(aip, P[p][j]));
+    const double2 aip = P[lane][p];
+    const double2 np_ = cdiv(lane == p ? make_double2(1.0, 0.0) : P[p][lane], piv);
+    __syncwarp();
+    P[p][lane] = np_;
+    __syncwarp();
+    if (lane != p) {
+#pragma unroll 8
+      for (int j = 0; j < kPB; ++j) {
+        const double2 base = (j == p) ? make_double2(0.0, 0.0) : P[lane][j];
+        P[lane][j] = csub(base, cmul(aip, P[p][j]));
+      }
     }
-    const double a = hypot(piv.x, piv.y);
-    pmin = fmin(pmin, isfinite(a) ? a : 0.0);
-    pmax = fmax(pmax, isfinite(a) ? a : INFINITY);
-    __syncthreads();
+    const double am = hypot(piv.x, piv.y);
+    pmin = fmin(pmin, isfinite(am) ? am : 0.0);
+    pmax = fmax(pmax, isfinite(am) ? am : INFINITY);
+    __syncwarp();
   }
-  pbuf[(int64_t)blockIdx.x * kPB * kPB + i * kPB + j] = P[i][j];
-  if (threadIdx.x == 0) {
+  double2* out = pbuf + (int64_t)ai * kPB * kPB;
+  for (int r = 0; r < kPB; ++r) out[r * kPB + lane] = P[r][lane];
+  if (lane == 0) {
     pivstat[2 * node] = fmin(pivstat[2 * node], pmin);
     pivstat[2 * node + 1] = fmax(pivstat[2 * node + 1], pmax);
   }
@@ -160,7 +196,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 //   (re += Ar Br - Ai Bi, im += Ar Bi + Ai Br).
 // 8 warps, each owning a 16x32 sub-tile = 2x4 DMMA blocks; W (64 x kPB) and
 // the pivot row panel F[K][c0:c0+64] are staged in shared memory.
-__global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
+__global__ void __launch_bounds__(256, 2) k_update(const int4* __restrict__ tasks,
                                                 const NodeDev* __restrict__ nodes,
                                                 const int32_t* __restrict__ act,
                                                 const int64_t* __restrict__ woff, int step,
@@ -223,6 +259,23 @@ __global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
         dmma884(cim[i][j][0], cim[i][j][1], aim[i], bre[j]);
       }
   }
+  // epilogue: issue all 16 loads of the old values first (independent), then
+  // subtract and store; a lane's two columns are 32 contiguous bytes and the
+  // 4 lanes of a row cover 128 contiguous bytes
+  double2 old[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + wr + 8 * i + gid;
+    const bool rok = r < m && !(r >= K0 && r < K0 + kb);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + wc + 8 * j + 2 * tig + e;
+        const bool load = rok && c < m && !(c >= K0 && c < K0 + kb);
+        old[i][j][e] = load ? T[(int64_t)r * m + c] : make_double2(0.0, 0.0);
+      }
+  }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = r0 + wr + 8 * i + gid;
@@ -233,9 +286,8 @@ __global__ void __launch_bounds__(256) k_update(const int4* __restrict__ tasks,
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
         if (c >= m) continue;
-        double2* p = T + (int64_t)r * m + c;
-        const double2 old = (c >= K0 && c < K0 + kb) ? make_double2(0.0, 0.0) : *p;
-        *p = make_double2(old.x - cre[i][j][e], old.y - cim[i][j][e]);
+        T[(int64_t)r * m + c] =
+            make_double2(old[i][j][e].x - cre[i][j][e], old[i][j][e].y - cim[i][j][e]);
       }
   }
 }
@@ -623,6 +675,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
     CK(cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
     CK(cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
@@ -639,6 +693,7 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
   k_pivinit<<<gblocks(nnodes, 256, 1024), 256, 0, s>>>(pivstat.p, nnodes);
   CK_LAUNCH(ctx);
   const size_t upd_smem = sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1));
+  const size_t inv_smem = sizeof(double2) * kInvWarps * kPB * (kPB + 1);
   for (int L = 0; L < nlevels; ++L) {
     const int64_t ni = lev_init_off[L + 1] - lev_init_off[L];
     if (ni) {
@@ -658,8 +713,8 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
       const int64_t p0 = step_panel_off[si], npn = step_panel_off[si + 1] - p0;
       const int64_t t0 = step_tile_off[si], ntl = step_tile_off[si + 1] - t0;
       if (!na) continue;
-      k_invert<<<(unsigned)na, 1024, 0, s>>>(nodes.p, act_node.p + a0, st, fronts.p, pbuf.p,
-                                             pivstat.p);
+      k_invert<<<(unsigned)((na + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, inv_smem, s>>>(
+          nodes.p, act_node.p + a0, (int)na, st, fronts.p, pbuf.p, pivstat.p);
       CK_LAUNCH(ctx);
       k_panel<<<(unsigned)npn, kPanelCols, 0, s>>>(panel_tasks.p + p0, nodes.p, act_node.p + a0,
                                                    act_woff.p + a0, st, fronts.p, pbuf.p, wbuf.p);

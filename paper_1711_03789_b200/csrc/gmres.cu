@@ -146,6 +146,15 @@ __device__ __forceinline__ void publish(double2* slot_step, int G, double2 a, do
 
 __device__ __forceinline__ bool bad2(double2 v) { return isnan(v.x) || isnan(v.y); }
 
+// Relaxed gpu-scope load: always served coherently (L2), never hoisted out of
+// a polling loop (asm volatile), but NOT ordered like a volatile access, so
+// several polls of one thread are in flight together.
+__device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
 // Thread t < G waits for CTA t's slots of this step (the dot slot, and the
 // drift slot only when `with_drift`: both loads in flight together); warp 0
 // then sums them in CTA order (fixed order -> bitwise reproducible) and
@@ -156,12 +165,12 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, doub
   if ((int)threadIdx.x < G) {
     const int k = threadIdx.x;
     long long spins = 0;
-    double2 u = __ldcv(slot_step + k);
-    double2 v = with_drift ? __ldcv(slot_step + G + k) : make_double2(0.0, 0.0);
+    double2 u = ld_relaxed2(slot_step + k);
+    double2 v = with_drift ? ld_relaxed2(slot_step + G + k) : make_double2(0.0, 0.0);
     while (bad2(u) || bad2(v)) {
       if (++spins > (1ll << 28)) __trap();  // never hang the device
-      if (bad2(u)) u = __ldcv(slot_step + k);
-      if (bad2(v)) v = __ldcv(slot_step + G + k);
+      if (bad2(u)) u = ld_relaxed2(slot_step + k);
+      if (bad2(v)) v = ld_relaxed2(slot_step + G + k);
     }
     stage[k] = u;
     stage[G + k] = v;

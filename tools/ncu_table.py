@@ -12,7 +12,10 @@ for r in rows[hi + 1:]:
     if len(r) <= mi:
         continue
     d = L.setdefault((r[ii], r[ki].split('(')[0], r[gi]), {})
-    d[r[mn]] = float(r[mi].replace(',', '')) * U.get(r[ui], 1)
+    try:
+        d[r[mn]] = float(r[mi].replace(',', '')) * U.get(r[ui], 1)
+    except ValueError:
+        pass
 tt = tb = 0
 for (i, k, g), d in L.items():
     t = d.get('gpu__time_duration.sum', 0)
