@@ -582,6 +582,12 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   w_max = 0;
   max_act = 0;
   int64_t nsteps_total = 0;
+  // solve-task sizing (tunable: MDD_SOLVE_ELEMS factor entries per task,
+  // MDD_SOLVE_QUANT row granularity)
+  const char* env_e = getenv("MDD_SOLVE_ELEMS");
+  const char* env_q = getenv("MDD_SOLVE_QUANT");
+  const int task_elems = env_e ? std::max(256, atoi(env_e)) : kSolveTaskElems;
+  const int row_quant = env_q ? std::max(1, std::min(512, atoi(env_q))) : kSolveRows;
   for (int L = 0; L < nlevels; ++L) {
     h_epos.insert(h_epos.end(), epos[L].begin(), epos[L].end());
     h_esrc.insert(h_esrc.end(), esrc[L].begin(), esrc[L].end());
@@ -592,10 +598,10 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
       lnp = std::max(lnp, nd.np);
       // solve tasks: row ranges holding ~kSolveTaskElems factor entries
-      auto rows_for = [](int len) {
-        int r = len > 0 ? kSolveTaskElems / len : 512;
-        r = std::max(kSolveRows, std::min(512, r));
-        return (r / kSolveRows) * kSolveRows;
+      auto rows_for = [task_elems, row_quant](int len) {
+        int r = len > 0 ? task_elems / len : 512;
+        r = std::max(row_quant, std::min(512, r));
+        return (r / row_quant) * row_quant;
       };
       if (nd.nu == 0) h_fwd.push_back(make_int4(g, 0, 0, 0));
       for (int r = 0, step = rows_for(nd.np); r < nd.nu; r += step)

@@ -30,7 +30,7 @@ constexpr int kPB = 32;      // pivot block of the sweep
 constexpr int kTile = 64;    // update tile
 constexpr int kPanelCols = 128;
 constexpr int kSolveRows = 32;          // minimum rows per solve task
-constexpr int kSolveTaskElems = 3072;   // ~48 KB of factor data per solve task
+constexpr int kSolveTaskElems = 8192;   // ~128 KB of factor data per solve task (tuned)
 
 struct NodeDev {
   int64_t front_off;  // complex elements into the front storage

@@ -36,7 +36,7 @@ namespace mdd {
 
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 
-constexpr int kArnThreads = 512;
+constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
 
 struct ArnoldiArgs {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void reduce_step(const double2* p, int G, double2* sh
   dr = sh[67];
 }
 
-constexpr int kArnE = 6;  // vector elements per thread kept in registers (register path)
+constexpr int kArnE = 12;  // vector elements per thread kept in registers (register path)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;

@@ -612,7 +612,8 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
   c.local_kind = d->family == 2 ? 1 : 0;
   c.fine_space = d->space;
   const int64_t ndof = c.ndof;
-  const int leaf = d->leaf_size > 0 ? d->leaf_size : 64;
+  const char* env_leaf = getenv("MDD_ND_LEAF");
+  const int leaf = d->leaf_size > 0 ? d->leaf_size : (env_leaf ? std::max(4, atoi(env_leaf)) : 64);
   const mdd_pattern& AP = *d->A_prec->pat;
   // ---- size cap (linalg.py:80-84), checked in subdomain order
   for (int l = 0; l < d->nsub; ++l) {
