@@ -259,7 +259,15 @@ def run_mine(args, rank, world):
     spec = precond.PreconditionerSpec(c["family"], "two", c["corr"], xi_prec=c["xi"])
     prob = fem.assemble(space, coeffs)
     t1 = time.perf_counter()
-    st = precond.setup(prob, dec, spec, lu_cap=None)
+    if world > 1:
+        # strong scaling: each rank factorises/solves its block of subdomains; the
+        # one-level sum is completed by one ncclAllReduce per apply (distributed.py)
+        from paper_1711_03789_b200 import distributed
+
+        comm = distributed.Communicator(ctx)
+        st = distributed.setup_sharded(prob, dec, spec, comm=comm, lu_cap=None)
+    else:
+        st = precond.setup(prob, dec, spec, lu_cap=None)
     t_setup = time.perf_counter() - t1
     t_prep = time.perf_counter() - t0
     stats = st.stats()
@@ -346,14 +354,14 @@ def run_mine(args, rank, world):
     hist = rep.residual_history
     res = {
         "metric": METRIC,
-        "value": world * n / (ms_step / 1e3),
+        "value": n / (ms_step / 1e3),  # one solve per step, shared by all ranks
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic (seeded; BASELINE.json configs)",
@@ -363,7 +371,9 @@ def run_mine(args, rank, world):
                         f"{spec.label()}, right GMRES tol 1e-6 maxit 200",
             "ndof": n, "subdomains": len(dec.dofs), "iterations": its, "converged": bool(rep.converged),
             "final_rel_residual": float(hist[-1]),
-            "parallelism": "replicas" if world > 1 else "single-gpu",
+            "parallelism": (f"subdomains sharded over {world} GPUs (NCCL allreduce per apply), "
+                            "coarse + GMRES replicated") if world > 1 else "single-gpu",
+            "local_subdomains": int(len(st.dof_sets)),
             "l2": "working set (V basis, factors) >> 126 MB L2; no flush needed",
         },
         "iters_per_s": its / (ms_step / 1e3),
@@ -381,7 +391,7 @@ def run_mine(args, rank, world):
                      "unit": "GB/s", "frac": roof_all[dom]["frac"], "traffic": None,
                      "peak_source": peak["source"]},
         "roofline_all": roof_all,
-        "e2e": {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "s_per_step": e2e_s, "iterations": rep_e.iterations},
         "clocks": clk.summary(),
     }
@@ -426,7 +436,7 @@ def run_reference(args):
     return {
         "metric": METRIC, "impl": "reference", "value": n / t, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded; BASELINE.json configs)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded; BASELINE.json configs)",
         "config": {"workload": f"{c['name']} (same as the GPU arm)", "ndof": n, "iterations_assumed": its},
         "cpu_baseline": {"value": n / t, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"oracle restatement of the reference (numpy + SuperLU), bounded sample per step: "

@@ -33,6 +33,7 @@ typedef struct mdd_ctx mdd_ctx;     /* one device + stream + scratch            
 typedef struct mdd_csr mdd_csr;     /* device CSR (int32 indptr/indices)        */
 typedef struct mdd_space mdd_space; /* device mesh + edge space + CSR pattern   */
 typedef struct mdd_prec mdd_prec;   /* factorised Schwarz preconditioner        */
+typedef struct mdd_comm mdd_comm;   /* NCCL communicator (multi-GPU sharding)   */
 
 enum {
   MDD_OK = 0,
@@ -178,6 +179,19 @@ void mdd_prec_destroy(mdd_prec* P);
 int mdd_prec_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
 /* PreconditionerState.coarse_solve (precond.py:357-358): R0^T A0^{-1} R0 v */
 int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
+/* Multi-GPU sharding (the reference has no distributed code,
+ * SPEC.md:8).  Each rank builds its preconditioner over its own block of
+ * subdomains (coarse space replicated); attaching a communicator makes the
+ * one-level part of every apply a partial sum completed by an in-place NCCL
+ * allreduce.  NCCL is resolved with dlopen at first use.  id128 == NULL
+ * creates a one-rank communicator without NCCL (collectives are identities);
+ * with an id NCCL is initialised even for one rank. */
+int mdd_comm_unique_id(char* out128);
+int mdd_comm_create(mdd_ctx* ctx, int nranks, int rank, const char* id128, mdd_comm** out);
+void mdd_comm_destroy(mdd_comm* c);
+int mdd_comm_info(const mdd_comm* c, int* nranks, int* rank);
+int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm);
+
 /* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
  *              levels, sum_local_dofs, coarse_n] */
 int mdd_prec_stats(const mdd_prec* P, double* out8);

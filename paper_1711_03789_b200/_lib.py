@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdd.so")
+LIB_PATH = os.environ.get("MDD_LIB_PATH") or os.path.join(_HERE, "libmdd.so")
 
 MDD_OK, MDD_EINVAL, MDD_ESINGULAR, MDD_ECAP, MDD_ECUDA, MDD_ENCCL, MDD_ENOMEM, MDD_EDECOMP = range(8)
 
@@ -144,6 +144,11 @@ SIGNATURES = {
     "mdd_prec_apply": (C.c_int, [_P, _pz, _pz]),
     "mdd_prec_coarse_apply": (C.c_int, [_P, _pz, _pz]),
     "mdd_prec_stats": (C.c_int, [_P, _pd]),
+    "mdd_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "mdd_comm_create": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p, _PP]),
+    "mdd_comm_destroy": (None, [_P]),
+    "mdd_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "mdd_prec_set_comm": (C.c_int, [_P, _P]),
     "mdd_prec_refactor": (C.c_int, [_P, _P, C.POINTER(mdd_coeffs)]),
     "mdd_gmres": (
         C.c_int,

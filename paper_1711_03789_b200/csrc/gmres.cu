@@ -35,6 +35,7 @@ namespace cg = cooperative_groups;
 namespace mdd {
 
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
+bool prec_is_distributed(const mdd_prec* P);
 
 constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
@@ -713,7 +714,9 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   // MDD_NO_GRAPH=1: host-driven loop (profilers cannot see kernels inside
   // conditional graph nodes)
   static const bool no_graph = getenv("MDD_NO_GRAPH") != nullptr;
-  const bool use_graph = !ctx->timing && !op.host_ops() && !no_graph;
+  // sharded preconditioners issue an NCCL allreduce per apply: host-driven loop
+  // (NCCL kernels inside a conditional-node body are not relied upon)
+  const bool use_graph = !ctx->timing && !op.host_ops() && !no_graph && !prec_is_distributed(ops->P);
   int64_t body_launches = 0;
   if (use_graph) {
     const int64_t l0 = ctx->launches;

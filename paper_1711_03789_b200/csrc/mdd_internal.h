@@ -174,7 +174,19 @@ struct mdd_space {
   mdd::DevBuf<int32_t> inc_ptr, inc;
 };
 
+// NCCL communicator (comm.cu); `comm` is an ncclComm_t (NCCL is dlopen'ed)
+struct mdd_comm {
+  mdd_ctx* ctx = nullptr;
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
 namespace mdd {
+// in-place sum of a complex vector over the communicator (stream-ordered)
+void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s);
+// true when collectives go through NCCL (any rank count)
+inline bool comm_active(const mdd_comm* c) { return c && c->comm; }
+
 // element geometry + 6x6 stiffness / mass (fem.py:154-195); shared by the
 // global assembly, the impras local assembly and the coarse Galerkin kernel
 struct ElemMats {

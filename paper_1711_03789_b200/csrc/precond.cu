@@ -77,6 +77,7 @@ struct mdd_prec {
   std::shared_ptr<mdd::PrecCore> core;
   int family = 0, levels = 1, correction = 0;
   const mdd_csr* A_corr = nullptr;
+  mdd_comm* comm = nullptr;  // sharded: partial output summed over ranks
 };
 
 namespace mdd {
@@ -417,10 +418,26 @@ static void one_level_scatter(mdd_prec* P, const double2* add, double2* out, cud
   CK_LAUNCH(ctx);
 }
 
+bool prec_is_distributed(const mdd_prec* P) { return P && comm_active(P->comm); }
+
+// Scatter of the local solutions (+ add).  A sharded preconditioner holds a
+// subset of the subdomains (the coarse space is replicated): its scatter is a
+// partial sum that one in-place allreduce completes before `add` is applied.
+static void one_level_finish(mdd_prec* P, const double2* add, double2* out, cudaStream_t s) {
+  if (!prec_is_distributed(P)) {
+    one_level_scatter(P, add, out, s);
+    return;
+  }
+  const int64_t n = P->core->ndof;
+  one_level_scatter(P, nullptr, out, s);
+  comm_allreduce_z(P->comm, out, n, s);
+  if (add) vec_add(P->core->ctx, out, add, out, n, s);
+}
+
 static void one_level(mdd_prec* P, const double2* v, const double2* add, double2* out,
                       cudaStream_t s) {
   one_level_solve(P, v, s);
-  one_level_scatter(P, add, out, s);
+  one_level_finish(P, add, out, s);
 }
 
 // out = R0^T A0^{-1} R0 v   (precond.py:357-358)
@@ -448,7 +465,7 @@ void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s)
     CK(cudaEventRecord(c.ev_join, c.s2));
     one_level_solve(P, v, s);
     CK(cudaStreamWaitEvent(s, c.ev_join, 0));
-    one_level_scatter(P, gv, out, s);
+    one_level_finish(P, gv, out, s);
     return;
   }
   coarse_solve(P, v, gv, s);
@@ -974,6 +991,7 @@ int mdd_prec_variant(const mdd_prec* base, int family, int levels, int correctio
   P->levels = levels;
   P->correction = correction;
   P->A_corr = A_corr ? A_corr : base->A_corr;
+  P->comm = base->comm;
   *out = P.release();
   MDD_API_END
 }
@@ -1008,6 +1026,13 @@ int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out) {
   coarse_solve(P, dv.p, dout.p, ctx->stream);
   dout.download(reinterpret_cast<double2*>(out), n, ctx->stream);
   CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm) {
+  MDD_API_BEGIN
+  if (comm && comm->ctx != P->core->ctx) fail(MDD_EINVAL, "comm: different context");
+  P->comm = comm;
   MDD_API_END
 }
 

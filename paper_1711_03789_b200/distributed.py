@@ -1,0 +1,130 @@
+"""Multi-GPU sharding of the Schwarz preconditioner.
+
+The reference runs on one process (SPEC.md:8 puts MPI out of scope); the
+paper's production runs place one subdomain solve per processor
+(PAPER.md:1754).  Here one process drives one GPU and:
+
+* each rank factorises and solves a contiguous block of subdomains, balanced
+  by local DoF count (:func:`shard_bounds`);
+* the coarse space (a few thousand DoFs) is replicated, so every rank can
+  apply hybrid / ADEF1 corrections without further communication;
+* the one-level output is a partial sum that a single in-place
+  ``ncclAllReduce`` completes (libmdd ``mdd_prec_set_comm``);
+* SpMV and the MGS-GMRES recurrences are replicated: every rank holds the
+  same allreduced vectors, so the Krylov loop needs no further collective.
+
+The NCCL unique id travels over the caller's ``torch.distributed`` process
+group (any backend), NCCL itself is opened by libmdd with ``dlopen``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["Communicator", "Shard", "shard_bounds", "make_shard", "setup_sharded"]
+
+
+def shard_bounds(costs, nranks: int) -> np.ndarray:
+    """Split ``len(costs)`` ordered subdomains into ``nranks`` contiguous blocks.
+
+    Returns ``nranks + 1`` monotone boundaries; each block's summed cost is as
+    close as possible to ``total / nranks`` (prefix-sum cut points).  Every
+    rank receives at least one subdomain when there are enough of them.
+    """
+    costs = np.asarray(costs, dtype=np.float64)
+    nsub = len(costs)
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    if nsub < nranks:
+        raise ValueError(f"{nsub} subdomains cannot be shared by {nranks} ranks")
+    pref = np.concatenate([[0.0], np.cumsum(costs)])
+    total = pref[-1]
+    b = np.zeros(nranks + 1, dtype=np.int64)
+    b[-1] = nsub
+    for r in range(1, nranks):
+        target = total * r / nranks
+        cut = int(np.searchsorted(pref, target))
+        if cut > 0 and abs(pref[cut - 1] - target) <= abs(pref[min(cut, nsub)] - target):
+            cut -= 1
+        # keep at least one subdomain per rank on either side
+        b[r] = min(max(cut, b[r - 1] + 1), nsub - (nranks - r))
+    return b
+
+
+class Communicator:
+    """libmdd NCCL communicator for the ranks of a ``torch.distributed`` group.
+
+    ``force_nccl`` initialises NCCL even for a single rank (used by the tests
+    to exercise the allreduce path on one GPU)."""
+
+    def __init__(self, ctx=None, group=None, force_nccl: bool = False):
+        import torch.distributed as dist
+
+        self.ctx = ctx or _lib.get_context()
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.nranks = dist.get_world_size(group)
+        else:
+            self.rank, self.nranks = 0, 1
+        uid = None
+        if self.nranks > 1 or force_nccl:
+            uid = broadcast_unique_id(_new_unique_id if self.rank == 0 else None, group)
+        h = C.c_void_p()
+        _lib.check(_lib.lib.mdd_comm_create(self.ctx.handle, self.nranks, self.rank, uid, C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _lib.lib.mdd_comm_destroy(h)
+            self.handle = None
+
+
+def _new_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.lib.mdd_comm_unique_id(buf))
+    return buf.raw
+
+
+def broadcast_unique_id(make_id, group=None) -> bytes:
+    """Rank 0 calls ``make_id()``; the 128-byte id reaches every rank of ``group``."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return make_id()
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("NCCL unique id broadcast failed")
+    return bytes(uid)
+
+
+@dataclass(frozen=True)
+class Shard:
+    """The subdomains one rank owns and the communicator completing the sum."""
+
+    rank: int
+    nranks: int
+    subdomains: np.ndarray
+    comm: Communicator | None = None
+
+
+def make_shard(decomp, rank: int, nranks: int, comm: Communicator | None = None) -> Shard:
+    """Contiguous block of ``decomp``'s subdomains for ``rank`` (cost = local DoFs)."""
+    b = shard_bounds([len(d) for d in decomp.dofs], nranks)
+    return Shard(rank, nranks, np.arange(b[rank], b[rank + 1], dtype=np.int64), comm)
+
+
+def setup_sharded(problem, decomp, spec, comm: Communicator | None = None, **kw):
+    """:func:`precond.setup` over this rank's subdomains (all ranks call it)."""
+    from .precond import PreconditionerState
+
+    comm = comm or Communicator()
+    shard = make_shard(decomp, comm.rank, comm.nranks, comm)
+    return PreconditionerState(problem, decomp, spec, shard=shard, **kw)

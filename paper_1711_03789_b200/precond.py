@@ -101,8 +101,12 @@ class PreconditionerState:
     """Factorised Schwarz preconditioner; ``apply`` is a fixed linear map (reference precond.py:277-377)."""
 
     def __init__(self, problem: SystemBundle, decomp: Decomposition, spec: PreconditionerSpec,
-                 lu_cap=DEFAULT_LU_CAP, leaf_size: int = 0):
+                 lu_cap=DEFAULT_LU_CAP, leaf_size: int = 0, shard=None):
+        """``shard`` (a :class:`distributed.Shard`) restricts the local solves to a
+        subset of the subdomains and attaches the communicator whose allreduce
+        completes the one-level sum; the coarse space stays replicated."""
         self.spec = spec
+        self.shard = shard
         self.decomp = decomp
         self.ndof = problem.space.ndof
         space = problem.space
@@ -120,6 +124,13 @@ class PreconditionerState:
         else:
             self.dof_sets = impedance_dof_sets(space, decomp.elements)
             self.pou_weights = build_pou(self.dof_sets, self.ndof)
+        self._elements = decomp.elements
+        if shard is not None:
+            # PoU weights are global (computed over every subdomain) before the cut
+            sel = [int(i) for i in shard.subdomains]
+            self.dof_sets = [self.dof_sets[i] for i in sel]
+            self.pou_weights = [self.pou_weights[i] for i in sel]
+            self._elements = [decomp.elements[i] for i in sel]
         self.R0 = None
         if spec.levels == "two":
             if decomp.coarse is None:
@@ -129,6 +140,8 @@ class PreconditionerState:
         self.factors = _Factors(handle, prec.A._ctx)
         self._h = handle
         self.coarse_lu = self.factors if spec.levels == "two" else None
+        if shard is not None and shard.comm is not None:
+            _lib.check(_lib.lib.mdd_prec_set_comm(handle, shard.comm.handle))
         self.setup_time_s = time.perf_counter() - t0
 
     # ------------------------------------------------------------- setup
@@ -159,8 +172,8 @@ class PreconditionerState:
         keep += [cc, hold]
         d.prec_coeffs = C.pointer(cc)
         if spec.family == "impras":
-            tptr, tets = _concat(decomp.elements)
-            bfs = [subdomain_boundary_faces(space.mesh, e) for e in decomp.elements]
+            tptr, tets = _concat(self._elements)
+            bfs = [subdomain_boundary_faces(space.mesh, e) for e in self._elements]
             fptr = np.zeros(len(bfs) + 1, dtype=np.int64)
             fptr[1:] = np.cumsum([len(b) for b in bfs])
             fl = np.ascontiguousarray(np.concatenate(bfs) if bfs else np.zeros((0, 3)), dtype=np.int64)

@@ -1,0 +1,116 @@
+"""Sharded (multi-GPU) preconditioner: host logic on CPU with gloo, world_size 2.
+
+The device path (libmdd ``mdd_prec_set_comm``) completes each rank's partial
+one-level sum with one allreduce and applies the replicated coarse terms
+afterwards; these tests check that decomposition of the work on the oracle:
+the per-rank partial sums, allreduced over gloo, reproduce the full
+one-level, additive, hybrid and ADEF1 applications.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import mesh_dict, rel
+from oracle import maxwell_oracle as O
+from paper_1711_03789_b200 import decomp, fem, mesh
+from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, shard_bounds
+
+
+def test_shard_bounds_cover_and_balance():
+    rng = np.random.default_rng(1)
+    for nsub, nranks in [(64, 1), (64, 2), (64, 8), (27, 4), (8, 8), (5, 3)]:
+        costs = rng.uniform(1.0, 3.0, nsub)
+        b = shard_bounds(costs, nranks)
+        assert b[0] == 0 and b[-1] == nsub and len(b) == nranks + 1
+        assert np.all(np.diff(b) >= 1)
+        loads = np.add.reduceat(costs, b[:-1])
+        assert loads.max() - loads.min() <= 2 * costs.max() + 1e-12
+    assert list(shard_bounds(np.ones(64), 4)) == [0, 16, 32, 48, 64]
+    with pytest.raises(ValueError):
+        shard_bounds(np.ones(3), 4)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    s = fem.build_edge_space(mesh.build_cube_mesh(4), "pec")
+    d = decomp.build_decomposition(s, 2, 1, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(2), "pec"))
+    a = O.assemble(mesh_dict(s.mesh), s.edge_to_dof, s.ndof, 3.0, 9.0)["A"]
+    return s, d, a
+
+
+def _allreduce_z(x):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(x).view(np.float64).copy())
+    dist.all_reduce(t)
+    return t.numpy().view(np.complex128)
+
+
+def _worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        s, d, a = _problem()
+        # unique-id broadcast (stub id: NCCL is not needed on CPU)
+        uid = broadcast_unique_id((lambda: bytes(range(128))) if rank == 0 else None)
+        assert uid == bytes(range(128))
+        sh = make_shard(d, rank, world)
+        sizes = [None] * world
+        dist.all_gather_object(sizes, [int(i) for i in sh.subdomains])
+        flat = sorted(i for blk in sizes for i in blk)
+        assert flat == list(range(d.n_subdomains)), flat
+        r0 = d.coarse.R0
+        a0 = (r0 @ a @ r0.T).tocsr()
+        v = np.random.default_rng(7).standard_normal(s.ndof) * (1 + 0.5j)
+        for fam in ("as", "ras"):
+            sel = list(sh.subdomains)
+            local = O.Schwarz([d.dofs[i] for i in sel], [d.pou[i] for i in sel],
+                              O.minors(a, [d.dofs[i] for i in sel]), fam, "two", "additive",
+                              R0=r0, A0=a0, A_corr=a, ndof=s.ndof, solver="dense")
+            for cor in ("additive", "hybrid", "adef1"):
+                full = O.Schwarz(d.dofs, d.pou, O.minors(a, d.dofs), fam, "two", cor, R0=r0, A0=a0,
+                                 A_corr=a, ndof=s.ndof, solver="dense")
+                one = lambda x: _allreduce_z(local.one_level(x))  # noqa: E731
+                gv = local.coarse_solve(v)  # replicated coarse space
+                if cor == "additive":
+                    got = one(v) + gv
+                elif cor == "adef1":
+                    got = one(v - a @ gv) + gv
+                else:
+                    y = one(v - a @ gv)
+                    got = y - local.coarse_solve(a @ y) + gv
+                err = rel(got, full.apply(v))
+                assert err < 1e-12, (fam, cor, err)
+            assert rel(_allreduce_z(local.one_level(v)), full.one_level(v)) < 1e-12
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as e:  # report to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_gloo_two_ranks_partial_sums():
+    world = 2
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
