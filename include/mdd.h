@@ -179,6 +179,10 @@ void mdd_prec_destroy(mdd_prec* P);
 int mdd_prec_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
 /* PreconditionerState.coarse_solve (precond.py:357-358): R0^T A0^{-1} R0 v */
 int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
+/* Diagnostics: device-timed applies (inputs resident, CUDA events on the
+ * context stream).  which: 0 full apply, 1 restriction + subdomain solves,
+ * 2 coarse solve.  No reference counterpart (bench.py / tools only). */
+int mdd_prec_apply_bench(mdd_prec* P, int which, int reps, double* ms_per_call);
 /* Multi-GPU sharding (the reference has no distributed code,
  * SPEC.md:8).  Each rank builds its preconditioner over its own block of
  * subdomains (coarse space replicated); attaching a communicator makes the

@@ -1,5 +1,5 @@
-// Batched multifrontal factorisation (block Gauss-Jordan sweeps) and
-// forward/backward solves.  See frontal.h for the algebra.
+// Batched multifrontal factorisation (block Gauss-Jordan sweeps); the
+// forward/backward solves are in solve.cu.  See frontal.h for the algebra.
 //
 // Replaces linalg.DenseLU (zgetrf, reference linalg.py:73-101) and
 // DenseLU.solve (zgetrs, linalg.py:103-107) as used per subdomain and for
@@ -300,105 +300,6 @@ __global__ void k_pivinit(double* p, int64_t n) {
   }
 }
 
-// Row-block GEMV of a front: rows [r0, r0+kSolveRows) of the row-major block
-// T (leading dimension ld), each dotted with z[0..len) held in shared memory.
-// A group of TPR lanes owns one row (TPR matched to the row length so short
-// rows do not waste a full warp reduction); each lane keeps 4 streaming loads
-// in flight.  emit(row, value) is called by the group's first lane.
-template <int TPR, typename Emit>
-__device__ __forceinline__ void gemv_rows(const double2* __restrict__ T, int64_t ld, int r0, int rend,
-                                          int len, const double2* __restrict__ z, Emit emit) {
-  constexpr int kGroups = 256 / TPR;
-  const int grp = threadIdx.x / TPR, lig = threadIdx.x % TPR;
-  for (int r = r0 + grp; r < rend; r += kGroups) {
-    const double2* row = T + (int64_t)r * ld;
-    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
-    int q = lig;
-    for (; q + 3 * TPR < len; q += 4 * TPR) {
-      const double2 t0 = __ldcs(row + q), t1 = __ldcs(row + q + TPR);
-      const double2 t2 = __ldcs(row + q + 2 * TPR), t3 = __ldcs(row + q + 3 * TPR);
-      a0 = cfma(t0, z[q], a0);
-      a1 = cfma(t1, z[q + TPR], a1);
-      a2 = cfma(t2, z[q + 2 * TPR], a2);
-      a3 = cfma(t3, z[q + 3 * TPR], a3);
-    }
-    for (; q < len; q += TPR) a0 = cfma(__ldcs(row + q), z[q], a0);
-    double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
-#pragma unroll
-    for (int o = TPR / 2; o > 0; o >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, TPR);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, TPR);
-    }
-    if (lig == 0) emit(r, acc);
-  }
-}
-
-template <typename Emit>
-__device__ __forceinline__ void gemv_rows_any(const double2* T, int64_t ld, int r0, int rend, int len,
-                                              const double2* z, Emit emit) {
-  if (len <= 48) gemv_rows<4>(T, ld, r0, rend, len, z, emit);
-  else if (len <= 160) gemv_rows<8>(T, ld, r0, rend, len, z, emit);
-  else if (len <= 512) gemv_rows<16>(T, ld, r0, rend, len, z, emit);
-  else gemv_rows<32>(T, ld, r0, rend, len, z, emit);
-}
-
-// forward: fp = b_P + children contributions ; uvec = (children contributions)_U - F_UP fp
-// gmap_abs holds, per child, the absolute uvec index feeding each front
-// position (or -1), so each contribution is a 2-deep load chain.
-__global__ void __launch_bounds__(256) k_fwd(const int4* __restrict__ tasks,
-                                             const NodeDev* __restrict__ nodes,
-                                             const int32_t* __restrict__ gmap_abs,
-                                             const double2* __restrict__ fronts,
-                                             const double2* __restrict__ bloc,
-                                             double2* __restrict__ fpst, double2* __restrict__ uvec) {
-  extern __shared__ double2 fp[];  // [np pivots | children's contributions to rows r0..r1)
-  const int4 tk = tasks[blockIdx.x];
-  const NodeDev nd = nodes[tk.x];
-  const int r0 = tk.y, r1 = tk.z;
-  const int np = nd.np, m = nd.m;
-  const int64_t base = (int64_t)nd.mat_off + nd.pivb;
-  const int32_t* ga = gmap_abs + nd.gmap_off;
-  double2* fu = fp + np;
-  // one prologue gathers both the pivot rhs and the children's contributions
-  // to this task's update rows (all 2-deep load chains in flight together)
-  const int nrow = r1 - r0;
-  for (int q = threadIdx.x; q < np + nrow; q += blockDim.x) {
-    const int pos = q < np ? q : np + r0 + (q - np);
-    double2 f = q < np ? bloc[base + q] : make_double2(0.0, 0.0);
-    for (int ci = 0; ci < nd.nch; ++ci) {
-      const int g = ga[(int64_t)ci * m + pos];
-      if (g >= 0) f = cadd(f, uvec[g]);
-    }
-    fp[q] = f;
-    if (q < np && r0 == 0) fpst[base + q] = f;
-  }
-  __syncthreads();
-  if (r0 >= r1) return;
-  const double2* TU = fronts + nd.front_off + (int64_t)np * m;  // row u of F_UP
-  gemv_rows_any(TU, m, r0, r1, np, fp,
-                [&](int u, double2 acc) { uvec[nd.uvec_off + u] = csub(fu[u - r0], acc); });
-}
-
-// backward: x_P = -(F_PP fp + F_PU x_U)
-__global__ void __launch_bounds__(256) k_bwd(const int4* __restrict__ tasks,
-                                             const NodeDev* __restrict__ nodes,
-                                             const int32_t* __restrict__ upd,
-                                             const double2* __restrict__ fronts,
-                                             const double2* __restrict__ fpst,
-                                             double2* __restrict__ xloc) {
-  extern __shared__ double2 z[];
-  const int4 tk = tasks[blockIdx.x];
-  const NodeDev nd = nodes[tk.x];
-  const int r0 = tk.y, r1 = tk.z;
-  const int np = nd.np, m = nd.m;
-  const int64_t base = (int64_t)nd.mat_off + nd.pivb;
-  for (int q = threadIdx.x; q < m; q += blockDim.x)
-    z[q] = q < np ? fpst[base + q] : xloc[(int64_t)nd.mat_off + upd[nd.upd_off + q - np]];
-  __syncthreads();
-  gemv_rows_any(fronts + nd.front_off, m, r0, r1, m, z,
-                [&](int i, double2 acc) { xloc[base + i] = cneg(acc); });
-}
-
 // ------------------------------------------------------------- host plan
 template <typename F>
 static void par_for(int64_t n, F&& f) {
@@ -494,6 +395,21 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       factor_flops += 8.0 * nd.np * (double)nd.m * nd.m;
       factor_entries += (double)nd.m * nd.m - (double)nd.nu * nd.nu;
     }
+  // packed F_UP rows for the solve kernels live after the fronts
+  upk_total = 0;
+  std::vector<int32_t> h_parent(nn, -1);
+  std::vector<int2> h_pack;
+  for (int i = 0; i < nmat; ++i)
+    for (size_t k = 0; k < sym[i].nodes.size(); ++k) {
+      const int64_t g = node_base[i] + (int64_t)k;
+      NodeDev& nd = h_nodes[g];
+      nd.upk_off = front_total + upk_total;
+      upk_total += (int64_t)nd.nu * nd.np;
+      if (sym[i].nodes[k].parent >= 0) h_parent[g] = node_base[i] + sym[i].nodes[k].parent;
+      if (nd.np > 0)
+        for (int u = 0; u < nd.nu; ++u) h_pack.push_back(make_int2((int)g, u));
+    }
+  npack = (int64_t)h_pack.size();
   std::vector<int32_t> h_upd(upd_total), h_gmap(gm_total, -1);
   // upd lists + gather maps
   par_for(nmat, [&](int64_t i) {
@@ -566,14 +482,11 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int64_t> h_epos;
   std::vector<int32_t> h_esrc;
   std::vector<int2> h_init, h_panel;
-  std::vector<int4> h_fwd, h_bwd;
   std::vector<int4> h_tile;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
   lev_ent_off.assign(1, 0);
   lev_init_off.assign(1, 0);
-  lev_fwd_off.assign(1, 0);
-  lev_bwd_off.assign(1, 0);
   lev_steps.assign(nlevels, 0);
   lev_step_base.assign(nlevels, 0);
   step_act_off.assign(1, 0);
@@ -582,12 +495,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   w_max = 0;
   max_act = 0;
   int64_t nsteps_total = 0;
-  // solve-task sizing (tunable: MDD_SOLVE_ELEMS factor entries per task,
-  // MDD_SOLVE_QUANT row granularity)
-  const char* env_e = getenv("MDD_SOLVE_ELEMS");
-  const char* env_q = getenv("MDD_SOLVE_QUANT");
-  const int task_elems = env_e ? std::max(256, atoi(env_e)) : kSolveTaskElems;
-  const int row_quant = env_q ? std::max(1, std::min(512, atoi(env_q))) : kSolveRows;
   for (int L = 0; L < nlevels; ++L) {
     h_epos.insert(h_epos.end(), epos[L].begin(), epos[L].end());
     h_esrc.insert(h_esrc.end(), esrc[L].begin(), esrc[L].end());
@@ -597,21 +504,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       const NodeDev& nd = h_nodes[g];
       for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
       lnp = std::max(lnp, nd.np);
-      // solve tasks: row ranges holding ~kSolveTaskElems factor entries
-      auto rows_for = [task_elems, row_quant](int len) {
-        int r = len > 0 ? task_elems / len : 512;
-        r = std::max(row_quant, std::min(512, r));
-        return (r / row_quant) * row_quant;
-      };
-      if (nd.nu == 0) h_fwd.push_back(make_int4(g, 0, 0, 0));
-      for (int r = 0, step = rows_for(nd.np); r < nd.nu; r += step)
-        h_fwd.push_back(make_int4(g, r, std::min(nd.nu, r + step), 0));
-      for (int r = 0, step = rows_for(nd.m); r < nd.np; r += step)
-        h_bwd.push_back(make_int4(g, r, std::min(nd.np, r + step), 0));
     }
     lev_init_off.push_back((int64_t)h_init.size());
-    lev_fwd_off.push_back((int64_t)h_fwd.size());
-    lev_bwd_off.push_back((int64_t)h_bwd.size());
     const int nst = (lnp + kPB - 1) / kPB;
     lev_steps[L] = nst;
     lev_step_base[L] = nsteps_total;
@@ -666,9 +560,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   tile_tasks.upload(h_tile, s);
   act_node.upload(h_act, s);
   act_woff.upload(h_woff, s);
-  fwd_tasks.upload(h_fwd, s);
-  bwd_tasks.upload(h_bwd, s);
-  fronts.alloc(front_total);
+  fronts.alloc(front_total + upk_total);
+  pack_tasks.upload(h_pack, s);
   uvec.alloc(std::max<int64_t>(1, uvec_total));
   pbuf.alloc(std::max<int64_t>(1, (int64_t)max_act * kPB * kPB));
   wbuf.alloc(std::max<int64_t>(1, w_max));
@@ -680,19 +573,18 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
-    CK(cudaFuncSetAttribute(k_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
-    CK(cudaFuncSetAttribute(k_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
-  if ((int64_t)max_m * 16 > 200 * 1024) fail(MDD_EINVAL, "front larger than the solve kernels support");
+  build_solve(lev);
   CK(cudaStreamSynchronize(s));
 }
 
 static unsigned gblocks(int64_t n, int bs, int cap) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, cap));
 }
+
 
 void FrontPlan::factor(const double2* vals, cudaStream_t s) {
   if (nnodes == 0) return;
@@ -732,6 +624,7 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
       }
     }
   }
+  pack(s);
 }
 
 int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {
@@ -758,25 +651,6 @@ int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {
     }
   }
   return -1;
-}
-
-void FrontPlan::solve(cudaStream_t s) {
-  const size_t fsm = sizeof(double2) * (std::max(1, max_np) + 512);  // + task rows (<= 512)
-  const size_t bsm = sizeof(double2) * std::max(1, max_m);
-  for (int L = 0; L < nlevels; ++L) {
-    const int64_t n = lev_fwd_off[L + 1] - lev_fwd_off[L];
-    if (!n) continue;
-    k_fwd<<<(unsigned)n, 256, fsm, s>>>(fwd_tasks.p + lev_fwd_off[L], nodes.p, gmap_abs.p,
-                                        fronts.p, bloc.p, fpst.p, uvec.p);
-    CK_LAUNCH(ctx);
-  }
-  for (int L = nlevels - 1; L >= 0; --L) {
-    const int64_t n = lev_bwd_off[L + 1] - lev_bwd_off[L];
-    if (!n) continue;
-    k_bwd<<<(unsigned)n, 256, bsm, s>>>(bwd_tasks.p + lev_bwd_off[L], nodes.p, upd.p, fronts.p,
-                                        fpst.p, xloc.p);
-    CK_LAUNCH(ctx);
-  }
 }
 
 }  // namespace mdd

@@ -29,8 +29,6 @@ namespace mdd {
 constexpr int kPB = 32;      // pivot block of the sweep
 constexpr int kTile = 64;    // update tile
 constexpr int kPanelCols = 128;
-constexpr int kSolveRows = 32;          // minimum rows per solve task
-constexpr int kSolveTaskElems = 8192;   // ~128 KB of factor data per solve task (tuned)
 
 struct NodeDev {
   int64_t front_off;  // complex elements into the front storage
@@ -40,7 +38,19 @@ struct NodeDev {
   int32_t m, np, nu, pivb;
   int32_t mat_off;    // offset of the node's matrix in the local vector space
   int32_t nch, child_off, mat;
+  int64_t upk_off;    // packed F_UP rows (solve.cu), elements into the front storage
 };
+
+// one solve task (solve.cu): rows [r0, r0+nrow) of a front block of row length len
+struct LvlTask {
+  int64_t off;      // factor rows (elements into the front storage)
+  int64_t out_off;  // forward: uvec index of row r0; backward: xloc index of row r0
+  int64_t aux_off;  // forward: gather map (gmap_abs); backward: update list (upd)
+  int64_t base;     // local vector index of the node's first pivot
+  int32_t mat_off, r0, nrow, len, np, m, nch, pad;
+};
+constexpr int kTSolveTaskElems = 2048;  // factor entries per solve task (32 KB)
+constexpr int kTSolvePrefetch = 500;    // L2 prefetch distance (tasks)
 
 struct MatrixInput {
   int32_t n = 0;
@@ -75,9 +85,7 @@ struct FrontPlan {
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
-  DevBuf<int4> fwd_tasks, bwd_tasks;  // {node, row0, row1, 0}
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
-  std::vector<int64_t> lev_fwd_off, lev_bwd_off;
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
   double factor_flops = 0, factor_entries = 0;
@@ -87,6 +95,13 @@ struct FrontPlan {
   // solve workspace (local vectors)
   DevBuf<double2> bloc, fpst, xloc;
   float factor_ms = 0;
+  // solve (solve.cu): packed F_UP rows, per-level task lists
+  int64_t npack = 0, upk_total = 0;
+  DevBuf<int2> pack_tasks;
+  DevBuf<LvlTask> ltasks;
+  std::vector<int64_t> lvl_off, lvl_dcap, lvl_zcap;  // forward levels ascending, then backward descending
+  void build_solve(const std::vector<std::vector<int32_t>>& lev);
+  void pack(cudaStream_t s);
 
   // build from analysed matrices
   void build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf);
@@ -94,8 +109,9 @@ struct FrontPlan {
   void factor(const double2* vals, cudaStream_t s);
   // per-matrix pivot ratio check; returns index of the first failing matrix or -1
   int check_pivots(std::string& msg, cudaStream_t s);
-  // solve in place: bloc (ND-ordered local rhs) -> xloc
-  void solve(cudaStream_t s);
+  // solve: bloc (ND-ordered local rhs) -> xloc; with v/gidx the local rhs is
+  // gathered as v[gidx[i]] inside the solve (fused restriction)
+  void solve(cudaStream_t s, const double2* v = nullptr, const int32_t* gidx = nullptr);
 };
 
 }  // namespace mdd

@@ -83,13 +83,6 @@ struct mdd_prec {
 namespace mdd {
 
 // ---------------------------------------------------------------- kernels
-__global__ void k_gather(int64_t n, const int32_t* __restrict__ gidx, const double2* __restrict__ v,
-                         double2* __restrict__ out) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = v[gidx[t]];
-}
-
 // out[i] = (sum_k w_k x[own_idx[k]]) (+ add[i])
 __global__ void k_scatter_owner(int64_t ndof, const int32_t* __restrict__ ptr,
                                 const int32_t* __restrict__ idx, const double* __restrict__ w,
@@ -402,9 +395,7 @@ static void one_level_solve(mdd_prec* P, const double2* v, cudaStream_t s) {
   PrecCore& c = *P->core;
   const int64_t nl = c.sub.nloc;
   if (nl) {
-    k_gather<<<gsb(c.ctx, nl), 256, 0, s>>>(nl, c.gidx.p, v, c.sub.bloc.p);
-    CK_LAUNCH(c.ctx);
-    c.sub.solve(s);
+    c.sub.solve(s, v, c.gidx.p);  // restriction v[I_l] fused into the solve
   }
 }
 
@@ -1026,6 +1017,37 @@ int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out) {
   coarse_solve(P, dv.p, dout.p, ctx->stream);
   dout.download(reinterpret_cast<double2*>(out), n, ctx->stream);
   CK(cudaStreamSynchronize(ctx->stream));
+  MDD_API_END
+}
+
+// Device-timed applies (CUDA events on the context stream, inputs resident):
+// which = 0 full apply, 1 subdomain solves only (restriction + solves), 2 coarse solve only.
+int mdd_prec_apply_bench(mdd_prec* P, int which, int reps, double* ms_per_call) {
+  MDD_API_BEGIN
+  mdd_ctx* ctx = P->core->ctx;
+  CK(cudaSetDevice(ctx->device));
+  if (which == 2 && !P->core->have_coarse) fail(MDD_EINVAL, "preconditioner has no coarse level");
+  const int64_t n = P->core->ndof;
+  DevBuf<double2> dv(n), dout(n);
+  CK(cudaMemsetAsync(dv.p, 0, sizeof(double2) * n, ctx->stream));
+  auto one = [&]() {
+    if (which == 0) prec_apply_dev(P, dv.p, dout.p, ctx->stream);
+    else if (which == 1) one_level_solve(P, dv.p, ctx->stream);
+    else coarse_solve(P, dv.p, dout.p, ctx->stream);
+  };
+  for (int i = 0; i < 3; ++i) one();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  for (int i = 0; i < reps; ++i) one();
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_per_call = reps > 0 ? ms / reps : 0.0;
   MDD_API_END
 }
 
