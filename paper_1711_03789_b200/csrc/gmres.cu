@@ -64,6 +64,7 @@ struct ArnoldiArgs {
   volatile int* hstatus; // host-mapped copy (host loop) or nullptr
   cudaGraphConditionalHandle cond;
   int use_cond;
+  int64_t wcap;  // STREAM path: w elements of the slice held in shared memory
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -204,13 +205,19 @@ __device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // 
   return make_double2(w.x - (h.x * v.x - h.y * v.y), w.y - (h.x * v.y + h.y * v.x));
 }
 
-// REG: unweighted, every CTA slice fits in registers (slice <= kArnThreads*kArnE):
-// w stays in registers for the whole kernel and the basis slice of step s+2
-// is loaded into registers right after publishing step s, so its latency
-// overlaps the barrier wait.  Otherwise: w and the basis are streamed from
-// L2/HBM with a TMA bulk L2 prefetch of the step s+2 slice.
-template <bool REG>
+// MODE 1 (REG): unweighted, every CTA slice fits in registers (slice <=
+// kArnThreads*kArnE): w stays in registers for the whole kernel and the basis
+// slice of step s+2 is loaded into registers right after publishing step s,
+// so its latency overlaps the barrier wait.
+// MODE 2 (STREAM): unweighted, larger slices (cfg3/cfg4 on one GPU): the
+// first wcap elements of the CTA's w slice live in shared memory (the rest in
+// L2-cached global memory); the basis is streamed with 4-way unrolled
+// L2-cached loads, the step s+2 slice bulk-prefetched into L2, so each basis
+// vector comes from HBM once per step and its second use hits L2.
+// MODE 0: the general (weighted) path, w and D w streamed from memory.
+template <int MODE>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
+  constexpr bool REG = MODE == 1, STR = MODE == 2;
   extern __shared__ double2 col[];  // m+1, identical in every CTA
   __shared__ double2 red[68 + 2 * kMaxArnCTAs];
   const int G = gridDim.x;
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const int64_t lo = (int64_t)blockIdx.x * a.slice;
   const int64_t hi = min(n, lo + a.slice);
   const int64_t len = hi > lo ? hi - lo : 0;
-  const bool weighted = !REG && a.DV != nullptr;
+  const bool weighted = MODE == 0 && a.DV != nullptr;
   double2* w = a.w;
   double2* dw = weighted ? a.dw : a.w;
   const bool do_drift = a.check_drift && m >= 2;  // drift of V_{m-1} vs V_j, j < m-1
@@ -233,6 +240,14 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
 
   double2 W[kArnE], XN[kArnE], XNN[kArnE];
   double2* DM = col + (a.maxit + 1);  // drift vector slice in shared memory (REG path)
+  double2* WS = col + (a.maxit + 1);  // w slice head in shared memory (STREAM path)
+  const int64_t ws = STR ? min(len, a.wcap) : 0;
+  auto wld = [&](int64_t i) { return i - lo < ws ? WS[i - lo] : __ldcg(w + i); };
+  if constexpr (STR) {
+    for (int64_t k = threadIdx.x; k < ws; k += blockDim.x) WS[k] = w[lo + k];
+    __syncthreads();
+    if (threadIdx.x == 0) prefetch_l2(xvec(1) + lo, len * 16);
+  }
   if constexpr (REG) {
 #pragma unroll
     for (int k = 0; k < kArnE; ++k) {
@@ -257,7 +272,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     } else {
       for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double2 x = a.V[i];
-        acc = cdotc_acc(acc, x, dw[i]);
+        acc = cdotc_acc(acc, x, STR ? wld(i) : dw[i]);
         if (do_drift) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
@@ -295,6 +310,35 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         acc = cdotc_acc(acc, x, W[k]);
         if (drift_next) dacc = cdotc_acc(dacc, x, DM[threadIdx.x + k * kArnThreads]);
         XN[k] = XNN[k];
+      }
+    } else if constexpr (STR) {
+      const double2* vj = a.V + (int64_t)j * n;
+      const double2* vn = xvec(last ? 0 : s + 1);
+      constexpr int U = 4;
+      const double2 zero = make_double2(0.0, 0.0);
+      for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += U * kArnThreads) {
+        double2 xv[U], xn[U], wv[U], dm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + (int64_t)u * kArnThreads;
+          const bool ok = i < hi;
+          xv[u] = ok ? __ldcg(vj + i) : zero;
+          xn[u] = (ok && !last) ? __ldcg(vn + i) : zero;
+          wv[u] = ok ? wld(i) : zero;
+          dm[u] = (ok && drift_next) ? __ldcg(dvm1 + i) : zero;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + (int64_t)u * kArnThreads;
+          if (i < hi) {
+            const double2 wi = caxmy(wv[u], h, xv[u]);
+            if (i - lo < ws) WS[i - lo] = wi;
+            else __stcg(w + i, wi);
+            const double2 x = last ? wi : xn[u];
+            acc = cdotc_acc(acc, x, wi);
+            if (drift_next) dacc = cdotc_acc(dacc, x, dm[u]);
+          }
+        }
       }
     } else {
       const double2* vj = a.V + (int64_t)j * n;
@@ -351,7 +395,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     } else {
       double2* dvm = weighted ? a.DV + (int64_t)m * n : nullptr;
       for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double2 wi = w[i];
+        const double2 wi = STR ? wld(i) : w[i];
         const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
         vm[i] = q;
         a.vin[i] = q;
@@ -633,9 +677,21 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nsm, (n + 255) / 256));
   const int64_t slice = (n + G - 1) / G;
   G = (int)((n + slice - 1) / slice);
-  const size_t shmem = sizeof(double2) * ((size_t)maxit + 1 + (size_t)kArnThreads * kArnE);
   const bool reg_path = !weighted && slice <= (int64_t)kArnThreads * kArnE;
-  auto kfn = reg_path ? k_arnoldi<true> : k_arnoldi<false>;
+  int mode = weighted ? 0 : reg_path ? 1 : 2;
+  // test hook: force the STREAM path (2) or the general path (0) of an
+  // unweighted solve; MDD_ARNOLDI_WCAP shrinks the shared-memory w head
+  if (const char* e = getenv("MDD_ARNOLDI_MODE"))
+    if (!weighted && (atoi(e) == 0 || atoi(e) == 2)) mode = atoi(e);
+  // STREAM: as much of the w slice in shared memory as fits beside col and the
+  // static reduction scratch (227 KB per CTA)
+  int64_t wcap = std::max<int64_t>(
+      0, (int64_t)(227 * 1024 - 16 * (68 + 2 * kMaxArnCTAs) - 1024) / 16 - (maxit + 1));
+  if (const char* e = getenv("MDD_ARNOLDI_WCAP")) wcap = std::min<int64_t>(wcap, std::max(0, atoi(e)));
+  const size_t shmem = sizeof(double2) * ((size_t)maxit + 1 +
+                                          (mode == 1 ? (size_t)kArnThreads * kArnE
+                                                     : mode == 2 ? (size_t)std::min<int64_t>(slice, wcap) : 0));
+  auto kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi<2> : k_arnoldi<0>;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
@@ -671,6 +727,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.check_drift = cfg->check_drift;
   aa.iter = diter.p;
   aa.dstatus = dstat.p;
+  aa.wcap = wcap;
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
     // NaN-fill the publication slots (0xFF bytes are a NaN pattern)

@@ -174,3 +174,30 @@ def test_translation_invariance_and_determinism(gpu):
     assert rel(r2.x, alpha * r1.x) <= 1e-12
     r3 = gmres(a, b, config=KrylovConfig(tol=1e-9))
     assert np.array_equal(r1.x, r3.x)  # fixed reduction order: bitwise reruns
+
+
+@pytest.mark.parametrize("mode,wcap", [("2", None), ("2", "40"), ("0", None)])
+def test_arnoldi_paths_match_reference(gpu, gg, monkeypatch, mode, wcap):
+    """The device Arnoldi kernel has three data paths (register-resident slices,
+    the shared-memory/streaming path used for large n, the general weighted
+    path).  Forcing each one on the golden AS2 case gives the reference's
+    iteration count and solution (north_star tolerances) and the same history
+    as the default path."""
+    from paper_1711_03789_b200 import decomp, fem, mesh, precond
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(4), "pec")
+    prob = fem.assemble(s, fem.Coefficients(k=3.0, xi=9.0), source=fem.gaussian_source)
+    d = decomp.build_decomposition(s, 2, 1, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(2), "pec"))
+    st = precond.setup(prob, d, precond.PreconditionerSpec("as", "two", "additive", xi_prec=9.0))
+    cfg = KrylovConfig(tol=1e-8, maxit=200)
+    base = gmres(prob.A, prob.rhs, precond=st, config=cfg)
+    monkeypatch.setenv("MDD_ARNOLDI_MODE", mode)
+    if wcap:
+        monkeypatch.setenv("MDD_ARNOLDI_WCAP", wcap)
+    r = gmres(prob.A, prob.rhs, precond=st, config=cfg)
+    tag = "as_two_additive_right_id"
+    assert r.converged and abs(r.iterations - int(gg[f"{tag}_it"])) <= 1
+    assert rel(r.x, gg[f"{tag}_x"]) <= 1e-8
+    assert r.iterations == base.iterations
+    assert np.allclose(r.residual_history, base.residual_history, rtol=1e-10, atol=1e-15)
