@@ -337,20 +337,33 @@ def run_mine(args, rank, world):
     sum_loc = stats["sum_local_dofs"]
     r0nnz = dec.coarse.R0.nnz
     b_prec = 16 * fe + 40 * sum_loc + 40 * r0nnz + 48 * n
-    b_arn = sum((32 * m + 16 * m + 64) * n for m in range(1, its + 1))  # 2 MGS passes + drift pass + w
+    # two MGS passes stream V_0..V_{m-1} once each; the drift rides along the first pass; + w in, V_m out
+    b_arn = sum((32 * m + 64) * n for m in range(1, its + 1))
     b_spmv = (20 * prob.A.nnz + 36 * n) * its
     peak = read_peaks()
+    # kernel families per GMRES iteration: one preconditioner apply, one SpMV,
+    # one Arnoldi launch (bytes: SURVEY.md §8d formulas)
     cands = {
-        "precond_apply(k_fwd/k_bwd/k_gather/k_scatter_owner)": (b_prec * its, t_prec),
-        "k_arnoldi": (b_arn, t_arn),
-        "k_spmv": (b_spmv, t_op),
+        "precond_apply": (b_prec, t_prec / its, "k_solve_tma fwd/bwd levels + k_scatter_owner + coarse R0/R0^T "
+                                                  "SpMV and coarse solve, one apply"),
+        "k_arnoldi": (b_arn / its, t_arn / its, "one k_arnoldi launch (MGS2 + drift + Givens), mean over the "
+                                                 "solve's iterations"),
+        "k_spmv": (b_spmv / its, t_op / its, "one complex CSR SpMV"),
     }
     dom = max(cands, key=lambda k: cands[k][1])
+    traffic = read_traffic(c["name"])
     roof_all = {}
-    for k, (b, t) in cands.items():
+    for k, (b, t, what) in cands.items():
         ach = b / (t / 1e3) / 1e9 if t > 0 else 0.0
-        roof_all[k] = {"achieved": ach, "frac": ach / peak["hbm_gbs"], "ms_per_step": t,
-                       "bytes_per_step": b}
+        roof_all[k] = {"achieved": ach, "frac": ach / peak["hbm_gbs"], "ms_per_launch": t,
+                       "algorithmic_bytes_per_launch": b, "ms_per_step": t * its, "launch": what,
+                       "traffic": traffic.get(k)}
+    fpk = read_fp64_peak()
+    f_ach = stats["factor_flops"] / (stats["factor_ms"] / 1e3) / 1e12 if stats["factor_ms"] > 0 else 0.0
+    roof_factor = {"bound": "tensor", "kernel": "numeric factorisation (k_front_init/k_invert/k_panel/"
+                                                "k_update DMMA), subdomains + coarse",
+                   "achieved": f_ach, "peak": fpk["tflops"], "unit": "TFLOP/s", "frac": f_ach / fpk["tflops"],
+                   "flops": stats["factor_flops"], "ms": stats["factor_ms"], "peak_source": fpk["source"]}
     hist = rep.residual_history
     res = {
         "metric": METRIC,
@@ -388,9 +401,13 @@ def run_mine(args, rank, world):
         "factor": {k: stats[k] for k in ("n_fronts", "max_front", "factor_entries", "factor_flops", "factor_ms")},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": roof_all[dom]["achieved"], "peak": peak["hbm_gbs"],
-                     "unit": "GB/s", "frac": roof_all[dom]["frac"], "traffic": None,
-                     "peak_source": peak["source"]},
+                     "unit": "GB/s", "frac": roof_all[dom]["frac"], "traffic": roof_all[dom]["traffic"],
+                     "algorithmic_bytes_per_launch": roof_all[dom]["algorithmic_bytes_per_launch"],
+                     "launch": roof_all[dom]["launch"], "peak_source": peak["source"],
+                     "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                       "(profiles/traffic.json)" if roof_all[dom]["traffic"] else None},
         "roofline_all": roof_all,
+        "roofline_factor": roof_factor,
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "s_per_step": e2e_s, "iterations": rep_e.iterations},
         "clocks": clk.summary(),
@@ -406,6 +423,24 @@ def run_mine(args, rank, world):
                                          f"est. {t_cpu:.0f}s per solve)",
                                "est_s_per_solve": t_cpu}
     return res
+
+
+def read_traffic(cfg_name):
+    """Measured DRAM bytes per launch of each kernel family (ncu launch list of
+    one bench step, tools/traffic_from_ncu.py -> profiles/traffic.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return d.get(cfg_name, {})
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def read_fp64_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return {"tflops": float(d["fp64_tflops"]), "source": "measured DMMA peak (profiles/fp64_peak.json)"}
+    except Exception:  # noqa: BLE001
+        return {"tflops": 40.0, "source": "nominal B200 FP64 tensor peak (no measurement found)"}
 
 
 def read_peaks():
