@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256, 2) k_update(const int4* __restrict__ task
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
-        const bool load = rok && c < m && !(c >= K0 && c < K0 + kb);
+        const bool load = rok && c < m && !(c >= K0 && c < K0 + kb) && !(r >= nd.np && c >= nd.np);
         old[i][j][e] = load ? T[(int64_t)r * m + c] : make_double2(0.0, 0.0);
       }
   }
@@ -285,9 +285,121 @@ __global__ void __launch_bounds__(256, 2) k_update(const int4* __restrict__ task
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
-        if (c >= m) continue;
+        if (c >= m || (r >= nd.np && c >= nd.np)) continue;  // F_UU: deferred Schur GEMM
         T[(int64_t)r * m + c] =
             make_double2(old[i][j][e].x - cre[i][j][e], old[i][j][e].y - cim[i][j][e]);
+      }
+  }
+}
+
+// Deferred Schur complement of one 64x64 tile of F_UU on the FP64 tensor
+// cores:  F_UU -= C_orig F_PU  (K = np), with C_orig the F_UP block saved
+// before the sweeps (the sweeps skip F_UU) and F_PU = F_PP^{-1} F_PU after
+// them.  One GEMM with K = np replaces np/32 rank-32 passes over F_UU.
+// K is consumed in chunks of kSchurKC through a 2-stage cp.async pipeline;
+// padded shared-memory rows keep the DMMA fragment loads conflict-free.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__global__ void __launch_bounds__(256, 2) k_schur(const int4* __restrict__ tasks, const NodeDev* __restrict__ nodes,
+                                               double2* __restrict__ fronts) {
+  extern __shared__ double2 sm[];
+  constexpr int LA = kSchurKC + 4, LB = kTile + 2;  // padded leading dimensions
+  const int4 tk = tasks[blockIdx.x];
+  const NodeDev nd = nodes[tk.x];
+  const int m = nd.m, np = nd.np, nu = nd.nu;
+  const int r0 = tk.y * kTile, c0 = tk.z * kTile;
+  const double2* Cg = fronts + nd.upk_off;                         // nu x np, ld np
+  const double2* Bg = fronts + nd.front_off + np;                  // np x nu, ld m
+  double2* Dg = fronts + nd.front_off + (int64_t)np * m + np;      // nu x nu, ld m
+  auto As = [&](int st) { return sm + st * (kTile * LA + kSchurKC * LB); };
+  auto Bs = [&](int st) { return sm + st * (kTile * LA + kSchurKC * LB) + kTile * LA; };
+  auto load = [&](int st, int k0) {
+    double2* A = As(st);
+    double2* B = Bs(st);
+    for (int t = threadIdx.x; t < kTile * kSchurKC; t += 256) {
+      const int rr = t / kSchurKC, kk = t % kSchurKC;
+      const bool ok = r0 + rr < nu && k0 + kk < np;
+      cp_async16(A + rr * LA + kk, ok ? Cg + (int64_t)(r0 + rr) * np + k0 + kk : Cg, ok);
+    }
+    for (int t = threadIdx.x; t < kSchurKC * kTile; t += 256) {
+      const int kk = t / kTile, cc = t % kTile;
+      const bool ok = k0 + kk < np && c0 + cc < nu;
+      cp_async16(B + kk * LB + cc, ok ? Bg + (int64_t)(k0 + kk) * m + c0 + cc : Bg, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+  double cre[2][4][2], cim[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
+  const int nk = (np + kSchurKC - 1) / kSchurKC;
+  load(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      load((kc + 1) & 1, (kc + 1) * kSchurKC);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double2* A = As(kc & 1);
+    const double2* B = Bs(kc & 1);
+#pragma unroll
+    for (int kk = 0; kk < kSchurKC / 4; ++kk) {
+      double are[2], aim[2], naim[2], bre[4], bim[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double2 v = A[(wr + 8 * i + gid) * LA + 4 * kk + tig];
+        are[i] = v.x;
+        aim[i] = v.y;
+        naim[i] = -v.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 v = B[(4 * kk + tig) * LB + wc + 8 * j + gid];
+        bre[j] = v.x;
+        bim[j] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma884(cre[i][j][0], cre[i][j][1], are[i], bre[j]);
+          dmma884(cre[i][j][0], cre[i][j][1], naim[i], bim[j]);
+          dmma884(cim[i][j][0], cim[i][j][1], are[i], bim[j]);
+          dmma884(cim[i][j][0], cim[i][j][1], aim[i], bre[j]);
+        }
+    }
+    __syncthreads();  // stage kc&1 is refilled by the next iteration's load
+  }
+  double2 old[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + wr + 8 * i + gid;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + wc + 8 * j + 2 * tig + e;
+        old[i][j][e] = (r < nu && c < nu) ? Dg[(int64_t)r * m + c] : make_double2(0.0, 0.0);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + wr + 8 * i + gid;
+    if (r >= nu) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + wc + 8 * j + 2 * tig + e;
+        if (c < nu) Dg[(int64_t)r * m + c] = make_double2(old[i][j][e].x - cre[i][j][e], old[i][j][e].y - cim[i][j][e]);
       }
   }
 }
@@ -398,7 +510,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   // packed F_UP rows for the solve kernels live after the fronts
   upk_total = 0;
   std::vector<int32_t> h_parent(nn, -1);
-  std::vector<int2> h_pack;
   for (int i = 0; i < nmat; ++i)
     for (size_t k = 0; k < sym[i].nodes.size(); ++k) {
       const int64_t g = node_base[i] + (int64_t)k;
@@ -406,10 +517,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       nd.upk_off = front_total + upk_total;
       upk_total += (int64_t)nd.nu * nd.np;
       if (sym[i].nodes[k].parent >= 0) h_parent[g] = node_base[i] + sym[i].nodes[k].parent;
-      if (nd.np > 0)
-        for (int u = 0; u < nd.nu; ++u) h_pack.push_back(make_int2((int)g, u));
     }
-  npack = (int64_t)h_pack.size();
   std::vector<int32_t> h_upd(upd_total), h_gmap(gm_total, -1);
   // upd lists + gather maps
   par_for(nmat, [&](int64_t i) {
@@ -482,7 +590,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int64_t> h_epos;
   std::vector<int32_t> h_esrc;
   std::vector<int2> h_init, h_panel;
-  std::vector<int4> h_tile;
+  std::vector<int4> h_tile, h_schur;
+  std::vector<int2> h_pack;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
   lev_ent_off.assign(1, 0);
@@ -492,6 +601,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   step_act_off.assign(1, 0);
   step_panel_off.assign(1, 0);
   step_tile_off.assign(1, 0);
+  lev_pack_off.assign(1, 0);
+  lev_schur_off.assign(1, 0);
   w_max = 0;
   max_act = 0;
   int64_t nsteps_total = 0;
@@ -504,8 +615,18 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       const NodeDev& nd = h_nodes[g];
       for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
       lnp = std::max(lnp, nd.np);
+      if (nd.np > 0 && nd.nu > 0) {
+        // F_UP rows (pack: the original block before the sweeps, F_UP after)
+        for (int u = 0; u < nd.nu; ++u) h_pack.push_back(make_int2((int)g, u));
+        // deferred Schur complement F_UU -= C_orig F_PU, 64x64 tiles
+        const int nt = (nd.nu + kTile - 1) / kTile;
+        for (int tr = 0; tr < nt; ++tr)
+          for (int tc = 0; tc < nt; ++tc) h_schur.push_back(make_int4(g, tr, tc, 0));
+      }
     }
     lev_init_off.push_back((int64_t)h_init.size());
+    lev_pack_off.push_back((int64_t)h_pack.size());
+    lev_schur_off.push_back((int64_t)h_schur.size());
     const int nst = (lnp + kPB - 1) / kPB;
     lev_steps[L] = nst;
     lev_step_base[L] = nsteps_total;
@@ -525,7 +646,10 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
         for (int tr = 0; tr < nt; ++tr) {
           const int rb = tr * kTile, re = std::min(nd.m, rb + kTile);
           if (rb >= K0 && re <= K0 + kb) continue;  // tile rows all pivots
-          for (int tc = 0; tc < nt; ++tc) h_tile.push_back(make_int4(ai, tr, tc, 0));
+          for (int tc = 0; tc < nt; ++tc) {
+            if (rb >= nd.np && tc * kTile >= nd.np) continue;  // inside F_UU: deferred Schur GEMM
+            h_tile.push_back(make_int4(ai, tr, tc, 0));
+          }
         }
       }
       w_max = std::max(w_max, wo);
@@ -558,6 +682,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   init_tasks.upload(h_init, s);
   panel_tasks.upload(h_panel, s);
   tile_tasks.upload(h_tile, s);
+  schur_tasks.upload(h_schur, s);
+  npack = (int64_t)h_pack.size();
   act_node.upload(h_act, s);
   act_woff.upload(h_woff, s);
   fronts.alloc(front_total + upk_total);
@@ -573,6 +699,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
+    CK(cudaFuncSetAttribute(k_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
     CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
     attr_set = true;
@@ -605,6 +732,12 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
           ne, ent_pos.p + lev_ent_off[L], ent_src.p + lev_ent_off[L], vals, fronts.p);
       CK_LAUNCH(ctx);
     }
+    // C_orig = F_UP before the sweeps (the packed F_UP region is free until pack())
+    const int64_t pk0 = lev_pack_off[L], npk = lev_pack_off[L + 1] - pk0;
+    if (npk) {
+      k_pack_up<<<(unsigned)((npk + 7) / 8), 256, 0, s>>>(pack_tasks.p + pk0, npk, nodes.p, fronts.p);
+      CK_LAUNCH(ctx);
+    }
     for (int st = 0; st < lev_steps[L]; ++st) {
       const int64_t si = lev_step_base[L] + st;
       const int64_t a0 = step_act_off[si], na = step_act_off[si + 1] - a0;
@@ -622,6 +755,11 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
                                                       act_woff.p + a0, st, fronts.p, wbuf.p);
         CK_LAUNCH(ctx);
       }
+    }
+    const int64_t sc0 = lev_schur_off[L], nsc = lev_schur_off[L + 1] - sc0;
+    if (nsc) {
+      k_schur<<<(unsigned)nsc, 256, kSchurSmem, s>>>(schur_tasks.p + sc0, nodes.p, fronts.p);
+      CK_LAUNCH(ctx);
     }
   }
   pack(s);

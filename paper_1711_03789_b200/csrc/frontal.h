@@ -29,6 +29,8 @@ namespace mdd {
 constexpr int kPB = 32;      // pivot block of the sweep
 constexpr int kTile = 64;    // update tile
 constexpr int kPanelCols = 128;
+constexpr int kSchurKC = 16;  // K chunk of the deferred Schur GEMM
+constexpr size_t kSchurSmem = 2 * sizeof(double2) * (kTile * (kSchurKC + 4) + kSchurKC * (kTile + 2));
 
 struct NodeDev {
   int64_t front_off;  // complex elements into the front storage
@@ -85,6 +87,8 @@ struct FrontPlan {
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
+  DevBuf<int4> schur_tasks;                  // {node, tile row, tile col} over F_UU
+  std::vector<int64_t> lev_pack_off, lev_schur_off;
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
@@ -113,5 +117,9 @@ struct FrontPlan {
   // gathered as v[gidx[i]] inside the solve (fused restriction)
   void solve(cudaStream_t s, const double2* v = nullptr, const int32_t* gidx = nullptr);
 };
+
+// F_UP rows of the listed (node, row) pairs -> packed row-contiguous blocks (solve.cu)
+__global__ void k_pack_up(const int2* __restrict__ tasks, int64_t ntask, const NodeDev* __restrict__ nodes,
+                          double2* __restrict__ fronts);
 
 }  // namespace mdd
