@@ -216,6 +216,11 @@ typedef struct {
   int32_t check_drift;   /* 1: compute the orthogonality drift (krylov.py:152) */
   int32_t keep_basis;
   int32_t device_io;     /* 1: b, x0, x are device pointers (no H2D/D2H)      */
+  int32_t ortho;         /* 0: MGS2 (reference krylov.py:137-143, default);
+                            1: CGS2 (classical Gram-Schmidt + one
+                            reorthogonalisation pass; with a sharded
+                            preconditioner the Krylov vectors are sharded by
+                            row blocks over the ranks)                        */
 } mdd_gmres_cfg;
 
 typedef struct {

@@ -78,6 +78,7 @@ class mdd_gmres_cfg(C.Structure):
         ("check_drift", C.c_int32),
         ("keep_basis", C.c_int32),
         ("device_io", C.c_int32),
+        ("ortho", C.c_int32),
     ]
 
 

@@ -3,11 +3,12 @@
 //
 // Sharding: each rank factorises and solves only its block of
 // subdomains (the small coarse space is replicated); the one-level output is
-// a partial sum that one in-place ncclAllReduce completes (mdd_prec_set_comm).  The Krylov vectors are replicated: SpMV and
-// the MGS-GMRES recurrences run identically on every rank (allreduce results
-// are identical on all ranks), so GMRES needs no further collective.  A
-// per-MGS-step cross-GPU reduction would cost more latency than the
-// single-GPU step it replaces at the BASELINE sizes.
+// a partial sum that one in-place ncclAllReduce completes (mdd_prec_set_comm).
+// GMRES either replicates the Krylov vectors (MGS, no further collective) or
+// shards them by contiguous row blocks (CGS2, gmres.cu): an allgather of the
+// new basis vector feeds the preconditioner and the row-block SpMV, and three
+// small allreduces per iteration complete the Gram-Schmidt coefficients and
+// the norm.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -25,6 +26,7 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
@@ -42,11 +44,12 @@ NcclApi& nccl() {
     api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
     api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(api.h, "ncclCommInitRank"));
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(api.h, "ncclAllReduce"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(api.h, "ncclAllGather"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.h, "ncclCommDestroy"));
     api.getErrorString =
         reinterpret_cast<decltype(api.getErrorString)>(dlsym(api.h, "ncclGetErrorString"));
   });
-  if (!api.h || !api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+  if (!api.h || !api.getUniqueId || !api.commInitRank || !api.allReduce || !api.allGather || !api.commDestroy)
     fail(MDD_ENCCL, "NCCL (libnccl.so.2) is not available");
   return api;
 }
@@ -68,6 +71,15 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
   nccl_check(nccl().allReduce(buf, buf, (size_t)(2 * n), ncclFloat64, ncclSum,
                               static_cast<ncclComm_t>(c->comm), s),
              "ncclAllReduce");
+}
+void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s) {
+  if (!c || !c->comm) {
+    if (send != recv)
+      CK(cudaMemcpyAsync(recv, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  nccl_check(nccl().allGather(send, recv, (size_t)(2 * per_rank), ncclFloat64, static_cast<ncclComm_t>(c->comm), s),
+             "ncclAllGather");
 }
 }  // namespace mdd
 

@@ -183,6 +183,34 @@ void spmv_dev_axpby(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y
     launch_spmv_t<4>(ctx, A, x, y, alpha, beta, z, s);
 }
 
+void spmv_rows_dev(mdd_ctx* ctx, const mdd_csr* A, int64_t row0, int64_t nrow, const double2* x, double2* y,
+                   cudaStream_t s) {
+  if (nrow <= 0) return;
+  if (row0 < 0 || row0 + nrow > A->nrow()) fail(MDD_EINVAL, "spmv: row block out of range");
+  // rowptr entries are absolute offsets into cols/vals: a shifted rowptr is the row block
+  const double avg = A->nrow() ? (double)A->nnz() / (double)A->nrow() : 0.0;
+  const int tpr = avg > 48 ? 32 : avg > 12 ? 8 : 4;
+  const int64_t grid = (nrow * tpr + 255) / 256;
+  const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
+  const int32_t* rp = A->pat->rowptr.p + row0;
+#define MDD_SPMV_ROWS(T)                                                                                   \
+  if (A->is_complex)                                                                                     \
+    k_spmv<true, T><<<(unsigned)grid, 256, 0, s>>>(nrow, rp, A->pat->cols.p, A->vals.p, x, y, one, zero,  \
+                                                   nullptr);                                             \
+  else                                                                                                   \
+    k_spmv<false, T><<<(unsigned)grid, 256, 0, s>>>(nrow, rp, A->pat->cols.p, A->vals.p, x, y, one, zero, \
+                                                    nullptr);
+  if (tpr == 32) {
+    MDD_SPMV_ROWS(32)
+  } else if (tpr == 8) {
+    MDD_SPMV_ROWS(8)
+  } else {
+    MDD_SPMV_ROWS(4)
+  }
+#undef MDD_SPMV_ROWS
+  CK_LAUNCH(ctx);
+}
+
 void spmv_dev(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y, cudaStream_t s) {
   spmv_dev_axpby(ctx, A, x, y, make_double2(1.0, 0.0), make_double2(0.0, 0.0), nullptr, s);
 }

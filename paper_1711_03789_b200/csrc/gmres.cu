@@ -36,6 +36,7 @@ namespace mdd {
 
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 bool prec_is_distributed(const mdd_prec* P);
+mdd_comm* prec_comm(const mdd_prec* P);
 
 constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
@@ -203,6 +204,55 @@ __device__ __forceinline__ double2 cdotc_acc(double2 acc, double2 x, double2 y) 
 }
 __device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // w - h v
   return make_double2(w.x - (h.x * v.x - h.y * v.y), w.y - (h.x * v.y + h.y * v.x));
+}
+
+// Complex Givens update of Hessenberg column m-1 (krylov.py:162-187), residual
+// history clamp and loop status; one thread.  col[0..m] holds the new column.
+__device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool breakdown) {
+  for (int j = 0; j < m - 1; ++j) {
+    const double2 csj = a.cs[j], snj = a.sn[j];
+    const double2 t = cadd(cmul(csj, col[j]), cmul(snj, col[j + 1]));
+    col[j + 1] = cadd(cmul(cneg(cconj(snj)), col[j]), cmul(csj, col[j + 1]));
+    col[j] = t;
+  }
+  const double am1 = hypot(col[m - 1].x, col[m - 1].y);
+  const double am = hypot(col[m].x, col[m].y);
+  const double denom = hypot(am1, am);
+  double2 csm, snm;
+  if (denom == 0.0) {
+    csm = make_double2(1.0, 0.0);
+    snm = make_double2(0.0, 0.0);
+  } else {
+    csm = make_double2(am1 / denom, 0.0);
+    const double2 phase = am1 > 0 ? make_double2(col[m - 1].x / am1, col[m - 1].y / am1)
+                                  : make_double2(1.0, 0.0);
+    const double2 p = cmul(phase, cconj(col[m]));
+    snm = make_double2(p.x / denom, p.y / denom);
+  }
+  a.cs[m - 1] = csm;
+  a.sn[m - 1] = snm;
+  double2* Hc = a.H + (int64_t)(m - 1) * (a.maxit + 1);
+  for (int j = 0; j <= m; ++j) Hc[j] = col[j];
+  Hc[m - 1] = cadd(cmul(csm, col[m - 1]), cmul(snm, col[m]));
+  Hc[m] = make_double2(0.0, 0.0);
+  const double2 gm1 = a.g[m - 1];
+  a.g[m] = cmul(cneg(cconj(snm)), gm1);
+  a.g[m - 1] = cmul(csm, gm1);
+  const double rel = fmin(hypot(a.g[m].x, a.g[m].y) / *a.beta, a.hist[m - 1]);
+  a.hist[m] = rel;
+  const int done = (breakdown || rel <= a.tol) ? 1 : 0;
+  *a.iter = m;
+  a.dstatus[0] = done;
+  a.dstatus[1] = breakdown ? 1 : 0;
+  a.dstatus[2] = m;
+  if (a.hstatus) {
+    a.hstatus[1] = breakdown ? 1 : 0;
+    a.hstatus[2] = m;
+    __threadfence_system();
+    a.hstatus[0] = done;
+    __threadfence_system();
+  }
+  if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
 }
 
 // MODE 1 (REG): unweighted, every CTA slice fits in registers (slice <=
@@ -407,52 +457,8 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     }
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  // ---- Givens (CTA 0, one thread) ----
   if (do_drift) a.drift[m - 1] = dmax;
-  for (int j = 0; j < m - 1; ++j) {
-    const double2 csj = a.cs[j], snj = a.sn[j];
-    const double2 t = cadd(cmul(csj, col[j]), cmul(snj, col[j + 1]));
-    col[j + 1] = cadd(cmul(cneg(cconj(snj)), col[j]), cmul(csj, col[j + 1]));
-    col[j] = t;
-  }
-  const double am1 = hypot(col[m - 1].x, col[m - 1].y);
-  const double am = hypot(col[m].x, col[m].y);
-  const double denom = hypot(am1, am);
-  double2 csm, snm;
-  if (denom == 0.0) {
-    csm = make_double2(1.0, 0.0);
-    snm = make_double2(0.0, 0.0);
-  } else {
-    csm = make_double2(am1 / denom, 0.0);
-    const double2 phase = am1 > 0 ? make_double2(col[m - 1].x / am1, col[m - 1].y / am1)
-                                  : make_double2(1.0, 0.0);
-    const double2 p = cmul(phase, cconj(col[m]));
-    snm = make_double2(p.x / denom, p.y / denom);
-  }
-  a.cs[m - 1] = csm;
-  a.sn[m - 1] = snm;
-  double2* Hc = a.H + (int64_t)(m - 1) * (a.maxit + 1);
-  for (int j = 0; j <= m; ++j) Hc[j] = col[j];
-  Hc[m - 1] = cadd(cmul(csm, col[m - 1]), cmul(snm, col[m]));
-  Hc[m] = make_double2(0.0, 0.0);
-  const double2 gm1 = a.g[m - 1];
-  a.g[m] = cmul(cneg(cconj(snm)), gm1);
-  a.g[m - 1] = cmul(csm, gm1);
-  const double rel = fmin(hypot(a.g[m].x, a.g[m].y) / *a.beta, a.hist[m - 1]);
-  a.hist[m] = rel;
-  const int done = (breakdown || rel <= a.tol) ? 1 : 0;
-  *a.iter = m;
-  a.dstatus[0] = done;
-  a.dstatus[1] = breakdown ? 1 : 0;
-  a.dstatus[2] = m;
-  if (a.hstatus) {
-    a.hstatus[1] = breakdown ? 1 : 0;
-    a.hstatus[2] = m;
-    __threadfence_system();
-    a.hstatus[0] = done;
-    __threadfence_system();
-  }
-  if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
+  arnoldi_tail(a, col, m, breakdown);
 }
 
 // drift of the final basis vector V_m: |vdot(V_j, DV_m)| for j < m (one CTA per j)
@@ -540,6 +546,112 @@ __global__ void k_axpy_out(int64_t n, const double2* x0, const double2* u, doubl
     x[e] = x0 ? cadd(x0[e], u[e]) : u[e];
 }
 
+// ------------------------------------------------------------ CGS2 path
+// Classical Gram-Schmidt with one reorthogonalisation pass: per iteration two
+// block projections h = V^H w, w -= V h (each one sweep over the basis) and a
+// norm, i.e. three reductions whatever m is.  This is the Krylov loop of the
+// sharded multi-GPU solve (vectors split in row blocks, each reduction one
+// small ncclAllReduce); on one GPU it is available through
+// KrylovConfig.orthogonalization = "cgs2".  The default stays MGS2 as in the
+// reference (krylov.py:137-143).  Partial sums are combined in a fixed order.
+
+// partial[k*G + cta] = sum over the CTA's chunk of conj(X_k) y_k, where job k < nv
+// is (V_k, y) and job nv + j (j < nd) is (V_j, d); one warp per job at a time
+__global__ void __launch_bounds__(256) k_mdot(int64_t nl, int64_t ldv, const double2* __restrict__ V, int nv,
+                                              const double2* __restrict__ y, const double2* __restrict__ d,
+                                              int nd, double2* __restrict__ partial) {
+  const int G = gridDim.x;
+  const int64_t chunk = (nl + G - 1) / G;
+  const int64_t i0 = (int64_t)blockIdx.x * chunk, i1 = min(nl, i0 + chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < nv + nd; k += blockDim.x >> 5) {
+    const double2* x = V + (int64_t)(k < nv ? k : k - nv) * ldv;
+    const double2* yy = k < nv ? y : d;
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+    int64_t i = i0 + lane;
+    for (; i + 96 < i1; i += 128) {
+      a0 = cdotc_acc(a0, __ldcs(x + i), __ldg(yy + i));
+      a1 = cdotc_acc(a1, __ldcs(x + i + 32), __ldg(yy + i + 32));
+      a2 = cdotc_acc(a2, __ldcs(x + i + 64), __ldg(yy + i + 64));
+      a3 = cdotc_acc(a3, __ldcs(x + i + 96), __ldg(yy + i + 96));
+    }
+    for (; i < i1; i += 32) a0 = cdotc_acc(a0, __ldcs(x + i), __ldg(yy + i));
+    double2 acc = warp_sum2(cadd(cadd(a0, a1), cadd(a2, a3)));
+    if (lane == 0) partial[(int64_t)k * G + blockIdx.x] = acc;
+  }
+}
+
+// out[k] = sum_c partial[k*G + c] in CTA order; one warp per k
+__global__ void k_colsum(const double2* __restrict__ partial, int G, int nk, double2* __restrict__ out) {
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= nk) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int c = lane; c < G; c += 32) acc = cadd(acc, partial[(int64_t)k * G + c]);
+  acc = warp_sum2(acc);
+  if (lane == 0) out[k] = acc;
+}
+
+// w[i] -= sum_{j < nv} h[j] V_j[i]
+__global__ void __launch_bounds__(256) k_maxpy(int64_t nl, int64_t ldv, const double2* __restrict__ V, int nv,
+                                               const double2* __restrict__ h, double2* __restrict__ w) {
+  extern __shared__ double2 hs[];
+  for (int j = threadIdx.x; j < nv; j += blockDim.x) hs[j] = h[j];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 wi = w[i];
+    int j = 0;
+    for (; j + 3 < nv; j += 4) {
+      const double2 v0 = __ldcs(V + (int64_t)j * ldv + i), v1 = __ldcs(V + (int64_t)(j + 1) * ldv + i);
+      const double2 v2 = __ldcs(V + (int64_t)(j + 2) * ldv + i), v3 = __ldcs(V + (int64_t)(j + 3) * ldv + i);
+      wi = caxmy(wi, hs[j], v0);
+      wi = caxmy(wi, hs[j + 1], v1);
+      wi = caxmy(wi, hs[j + 2], v2);
+      wi = caxmy(wi, hs[j + 3], v3);
+    }
+    for (; j < nv; ++j) wi = caxmy(wi, hs[j], __ldcs(V + (int64_t)j * ldv + i));
+    w[i] = wi;
+  }
+}
+
+// Column m-1 of H from the two projections and the norm, drift of V_{m-1},
+// breakdown test, Givens update (arnoldi_tail).  One thread.  scal[0] = hlast,
+// scal[1] = 1 on breakdown (k_vscale then leaves V_m alone).
+__global__ void k_cgs_tail(ArnoldiArgs a, const double2* h1, const double2* h2, const double2* nrm,
+                           const double2* dr, int do_drift, double2* col, double* scal) {
+  if (threadIdx.x || blockIdx.x) return;
+  const int m = *a.iter + 1;
+  for (int j = 0; j < m; ++j) col[j] = cadd(h1[j], h2[j]);
+  const double hlast = sqrt(fmax(nrm[0].x, 0.0));
+  col[m] = make_double2(hlast, 0.0);
+  double cmax = 0.0;
+  for (int j = 0; j <= m; ++j) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  const bool breakdown = hlast <= 1e-13 * cmax;
+  if (do_drift && m >= 2) {
+    double dmax = 0.0;
+    for (int j = 0; j < m - 1; ++j) dmax = fmax(dmax, hypot(dr[j].x, dr[j].y));
+    a.drift[m - 1] = dmax;
+  }
+  scal[0] = hlast;
+  scal[1] = breakdown ? 1.0 : 0.0;
+  arnoldi_tail(a, col, m, breakdown);
+}
+
+__global__ void k_vscale(int64_t nl, const double2* __restrict__ w, const double* __restrict__ scal,
+                         double2* __restrict__ vm) {
+  if (scal[1] != 0.0) return;
+  const double hl = scal[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 x = w[i];
+    vm[i] = make_double2(x.x / hl, x.y / hl);
+  }
+}
+
+// y = x[off .. off+n) ; zero-filled beyond `valid`
+__global__ void k_slice(int64_t n, int64_t valid, const double2* __restrict__ x, double2* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = i < valid ? x[i] : make_double2(0.0, 0.0);
+}
+
 struct OpRunner {
   mdd_ctx* ctx;
   const mdd_gmres_ops* ops;
@@ -571,6 +683,210 @@ static unsigned gs_grid(int64_t n) {
   return std::max<unsigned>(1, (unsigned)std::min<int64_t>((n + 255) / 256, 8192));
 }
 
+// CGS2 GMRES over row-block-sharded Krylov vectors (one block when the
+// preconditioner is not sharded).  Same recurrences and outputs as the MGS
+// path: breakdown test, Givens, history clamp, drift (arnoldi_tail).
+static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const mdd_complex* b,
+                      const mdd_complex* x0, const mdd_gmres_cfg* cfg, mdd_complex* x, double* history,
+                      double* drift, int32_t* iterations, int32_t* converged) {
+  cudaStream_t s = ctx->stream;
+  if (!ops->A) fail(MDD_EINVAL, "CGS2 GMRES needs the operator as a matrix");
+  if (ops->a_fn || ops->m_fn) fail(MDD_EINVAL, "CGS2 GMRES does not take host callables");
+  if (ops->D) fail(MDD_EINVAL, "CGS2 GMRES: weighted inner products are not supported");
+  if (cfg->keep_basis) fail(MDD_EINVAL, "CGS2 GMRES: keep_basis is not supported");
+  mdd_comm* comm = ops->P ? prec_comm(ops->P) : nullptr;
+  const bool dist = comm_active(comm);
+  const int N = dist ? comm->nranks : 1, rank = dist ? comm->rank : 0;
+  const int64_t chunk = (n + N - 1) / N;
+  const int64_t lo = std::min<int64_t>(n, (int64_t)rank * chunk);
+  const int64_t nl = std::min<int64_t>(chunk, n - lo);
+  const int maxit = cfg->maxit;
+  const bool right = cfg->side == 0, dio = cfg->device_io != 0;
+  const bool hasM = ops->P || ops->Mcsr;
+  auto allreduce = [&](double2* buf, int64_t k) {
+    if (dist) comm_allreduce_z(comm, buf, k, s);
+  };
+  DevBuf<double2> V((size_t)(maxit + 1) * chunk), w(chunk), t(chunk), full((size_t)N * chunk), z(n), bfull,
+      x0full, u(chunk);
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->nsm, (nl + 511) / 512));
+  DevBuf<double2> partial((size_t)(2 * maxit + 2) * G), hb(2 * maxit + 2), h2(maxit + 1), nrm(1),
+      col(maxit + 2);
+  DevBuf<double2> H((size_t)(maxit + 1) * maxit), cs(maxit), sn(maxit), g(maxit + 1), y(maxit);
+  DevBuf<double> hist(maxit + 1), dbeta(1), ddrift(maxit + 1), scal(2);
+  DevBuf<int> diter(1), dstat(4);
+  H.zero(s);
+  cs.zero(s);
+  sn.zero(s);
+  g.zero(s);
+  diter.zero(s);
+  dstat.zero(s);
+  V.zero(s);  // padding rows of the last block stay zero
+  {
+    std::vector<double> nanv(maxit + 1, NAN);
+    ddrift.upload(nanv, s);
+  }
+  const double2* bdev;
+  if (dio) {
+    bdev = reinterpret_cast<const double2*>(b);
+  } else {
+    bfull.upload(reinterpret_cast<const double2*>(b), n, s);
+    bdev = bfull.p;
+  }
+  const double2* x0dev = nullptr;
+  if (x0) {
+    if (dio) {
+      x0dev = reinterpret_cast<const double2*>(x0);
+    } else {
+      x0full.upload(reinterpret_cast<const double2*>(x0), n, s);
+      x0dev = x0full.p;
+    }
+  }
+  auto slice = [&](const double2* src_full, double2* dst) {
+    k_slice<<<gs_grid(chunk), 256, 0, s>>>(chunk, nl, src_full + lo, dst);
+    CK_LAUNCH(ctx);
+  };
+  auto applyM = [&](const double2* in_full, double2* out_full) {
+    if (ops->P) prec_apply_dev(ops->P, in_full, out_full, s);
+    else spmv_dev(ctx, ops->Mcsr, in_full, out_full, s);
+  };
+  // local rows of the (preconditioned) operator applied to a full vector
+  auto op = [&](const double2* vfull, double2* wl) {
+    if (right) {
+      const double2* in = vfull;
+      if (hasM) {
+        applyM(vfull, z.p);
+        in = z.p;
+      }
+      spmv_rows_dev(ctx, ops->A, lo, nl, in, wl, s);
+    } else {
+      spmv_rows_dev(ctx, ops->A, lo, nl, vfull, t.p, s);
+      if (hasM) {
+        comm_allgather_z(dist ? comm : nullptr, t.p, full.p, chunk, s);
+        applyM(full.p, z.p);
+        slice(z.p, wl);
+      } else {
+        CK(cudaMemcpyAsync(wl, t.p, sizeof(double2) * chunk, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  };
+  auto dots = [&](const double2* Vb, int nv, const double2* yv, const double2* d, int nd, double2* out) {
+    k_mdot<<<G, 256, 0, s>>>(nl, chunk, Vb, nv, yv, d, nd, partial.p);
+    CK_LAUNCH(ctx);
+    k_colsum<<<(unsigned)((nv + nd + 7) / 8), 256, 0, s>>>(partial.p, G, nv + nd, out);
+    CK_LAUNCH(ctx);
+    allreduce(out, nv + nd);
+  };
+  // r0 (krylov.py:94-106), local rows
+  double2* r = w.p;
+  slice(bdev, r);
+  if (x0dev) {
+    spmv_rows_dev(ctx, ops->A, lo, nl, x0dev, t.p, s);
+    vec_sub(ctx, r, t.p, r, chunk, s);
+  }
+  if (!right && hasM) {
+    comm_allgather_z(dist ? comm : nullptr, r, full.p, chunk, s);
+    applyM(full.p, z.p);
+    slice(z.p, r);
+  }
+  dots(r, 1, r, nullptr, 0, nrm.p);
+  std::vector<double2> hn(1);
+  nrm.download(hn.data(), 1, s);
+  CK(cudaStreamSynchronize(s));
+  const double beta = std::sqrt(std::max(hn[0].x, 0.0));
+  double2* xout_dev = nullptr;
+  DevBuf<double2> xo(dio ? 0 : n);
+  xout_dev = dio ? reinterpret_cast<double2*>(x) : xo.p;
+  if (beta == 0.0) {  // zero residual: 0 iterations (krylov.py:110-118)
+    if (x0dev) CK(cudaMemcpyAsync(xout_dev, x0dev, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+    else CK(cudaMemsetAsync(xout_dev, 0, sizeof(double2) * n, s));
+    if (!dio) xo.download(reinterpret_cast<double2*>(x), n, s);
+    CK(cudaStreamSynchronize(s));
+    history[0] = 0.0;
+    *iterations = 0;
+    *converged = 1;
+    return;
+  }
+  {
+    const double h0[2] = {beta, 0.0};
+    scal.upload(h0, 2, s);
+    const double one = 1.0;
+    hist.upload(&one, 1, s);
+    const double2 g0 = make_double2(beta, 0.0);
+    g.upload(&g0, 1, s);
+    dbeta.upload(&beta, 1, s);
+  }
+  k_vscale<<<gs_grid(chunk), 256, 0, s>>>(chunk, r, scal.p, V.p);
+  CK_LAUNCH(ctx);
+  ArnoldiArgs aa{};
+  aa.maxit = maxit;
+  aa.H = H.p;
+  aa.cs = cs.p;
+  aa.sn = sn.p;
+  aa.g = g.p;
+  aa.hist = hist.p;
+  aa.drift = ddrift.p;
+  aa.beta = dbeta.p;
+  aa.tol = cfg->tol;
+  aa.check_drift = cfg->check_drift;
+  aa.iter = diter.p;
+  aa.dstatus = dstat.p;
+  int st[4] = {0, 0, 0, 0};
+  for (int it = 1; it <= maxit; ++it) {
+    const int m = it - 1;  // newest basis vector
+    double2* vm = V.p + (int64_t)m * chunk;
+    comm_allgather_z(dist ? comm : nullptr, vm, full.p, chunk, s);
+    op(full.p, w.p);
+    const int nd = (cfg->check_drift && m >= 1) ? m : 0;
+    dots(V.p, m + 1, w.p, vm, nd, hb.p);  // pass 1 (+ drift of V_m)
+    k_maxpy<<<gs_grid(chunk), 256, sizeof(double2) * (m + 1), s>>>(nl, chunk, V.p, m + 1, hb.p, w.p);
+    CK_LAUNCH(ctx);
+    dots(V.p, m + 1, w.p, nullptr, 0, h2.p);  // pass 2
+    k_maxpy<<<gs_grid(chunk), 256, sizeof(double2) * (m + 1), s>>>(nl, chunk, V.p, m + 1, h2.p, w.p);
+    CK_LAUNCH(ctx);
+    dots(w.p, 1, w.p, nullptr, 0, nrm.p);
+    k_cgs_tail<<<1, 32, 0, s>>>(aa, hb.p, h2.p, nrm.p, hb.p + m + 1, nd > 0 ? 1 : 0, col.p, scal.p);
+    CK_LAUNCH(ctx);
+    k_vscale<<<gs_grid(chunk), 256, 0, s>>>(chunk, w.p, scal.p, V.p + (int64_t)(m + 1) * chunk);
+    CK_LAUNCH(ctx);
+    dstat.download(st, 4, s);
+    CK(cudaStreamSynchronize(s));
+    if (st[0]) break;
+  }
+  const int m = st[2];
+  const bool done = st[0] != 0;
+  const bool breakdown = done && st[1];
+  if (m < 1) fail(MDD_ECUDA, "gmres: no iteration completed");
+  double final_drift = NAN;
+  if (cfg->check_drift && !breakdown) {  // drift of the final vector V_m (krylov.py:152-160)
+    dots(V.p, m, V.p + (int64_t)m * chunk, nullptr, 0, hb.p);
+    std::vector<double2> hv(m);
+    hb.download(hv.data(), m, s);
+    CK(cudaStreamSynchronize(s));
+    final_drift = 0.0;
+    for (int j = 0; j < m; ++j) final_drift = std::max(final_drift, std::hypot(hv[j].x, hv[j].y));
+  }
+  // solution (krylov.py:189-198): x = x0 + M (V y) (right) or x0 + V y (left)
+  k_backsub<<<1, 32, 0, s>>>(m, maxit, H.p, g.p, y.p);
+  CK_LAUNCH(ctx);
+  k_combine_basis<<<gs_grid(chunk), 256, 0, s>>>(chunk, m, V.p, y.p, u.p);
+  CK_LAUNCH(ctx);
+  comm_allgather_z(dist ? comm : nullptr, u.p, full.p, chunk, s);
+  const double2* upd = full.p;
+  if (right && hasM) {
+    applyM(full.p, z.p);
+    upd = z.p;
+  }
+  k_axpy_out<<<gs_grid(n), 256, 0, s>>>(n, x0dev, upd, xout_dev);
+  CK_LAUNCH(ctx);
+  if (!dio) xo.download(reinterpret_cast<double2*>(x), n, s);
+  hist.download(history, m + 1, s);
+  if (drift) ddrift.download(drift, m + 1, s);
+  CK(cudaStreamSynchronize(s));
+  if (drift && !std::isnan(final_drift)) drift[m] = final_drift;
+  *iterations = m;
+  *converged = done ? (breakdown ? 2 : 1) : 0;
+}
+
 }  // namespace mdd
 
 using namespace mdd;
@@ -589,6 +905,12 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (!ops->A && !ops->a_fn) fail(MDD_EINVAL, "gmres: no operator");
   if (ops->A && (ops->A->nrow() != n || ops->A->ncol() != n))
     fail(MDD_EINVAL, "gmres: operator dimension mismatch");
+  if (cfg->ortho == 1) {
+    gmres_cgs(ctx, ops, n, b, x0, cfg, x, history, drift, iterations, converged);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return MDD_OK;
+  }
+  if (cfg->ortho != 0) fail(MDD_EINVAL, "gmres: unknown orthogonalisation");
   OpRunner op{ctx, ops, n, s};
   if (op.host_ops()) {
     CK(cudaMallocHost(&op.hin, sizeof(double2) * (n ? n : 1)));

@@ -184,6 +184,8 @@ struct mdd_comm {
 namespace mdd {
 // in-place sum of a complex vector over the communicator (stream-ordered)
 void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s);
+// recv[r*per_rank ...] = send of rank r (stream-ordered); one rank: copy
+void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s);
 // true when collectives go through NCCL (any rank count)
 inline bool comm_active(const mdd_comm* c) { return c && c->comm; }
 
@@ -198,6 +200,9 @@ struct ElemMats {
 // kernels shared across units ------------------------------------------
 // y = A x (x, y device complex)
 void spmv_dev(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y, cudaStream_t s);
+// y[0..nrow) = A[row0:row0+nrow, :] x  (row block of a CSR, x full length)
+void spmv_rows_dev(mdd_ctx* ctx, const mdd_csr* A, int64_t row0, int64_t nrow, const double2* x, double2* y,
+                   cudaStream_t s);
 // y = beta*y + alpha*A x on device; variants used by the preconditioner
 void spmv_dev_axpby(mdd_ctx* ctx, const mdd_csr* A, const double2* x, double2* y,
                     double2 alpha, double2 beta, const double2* z, cudaStream_t s);

@@ -410,6 +410,7 @@ static void one_level_scatter(mdd_prec* P, const double2* add, double2* out, cud
 }
 
 bool prec_is_distributed(const mdd_prec* P) { return P && comm_active(P->comm); }
+mdd_comm* prec_comm(const mdd_prec* P) { return P ? P->comm : nullptr; }
 
 // Scatter of the local solutions (+ add).  A sharded preconditioner holds a
 // subset of the subdomains (the coarse space is replicated): its scatter is a

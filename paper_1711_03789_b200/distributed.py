@@ -10,8 +10,14 @@ paper's production runs place one subdomain solve per processor
   apply hybrid / ADEF1 corrections without further communication;
 * the one-level output is a partial sum that a single in-place
   ``ncclAllReduce`` completes (libmdd ``mdd_prec_set_comm``);
-* SpMV and the MGS-GMRES recurrences are replicated: every rank holds the
-  same allreduced vectors, so the Krylov loop needs no further collective.
+* GMRES either replicates the Krylov vectors (``orthogonalization="mgs"``,
+  the reference's MGS2: every rank runs the same recurrences on the same
+  allreduced vectors) or shards them (``"cgs2"``, the default of the
+  multi-GPU benchmark): rank r owns the contiguous row block
+  :func:`row_block` of every basis vector; per iteration one ncclAllGather
+  assembles the newest basis vector for the preconditioner and the row-block
+  SpMV, and three small ncclAllReduce calls complete the two classical
+  Gram-Schmidt projections and the norm (libmdd gmres.cu, ``gmres_cgs``).
 
 The NCCL unique id travels over the caller's ``torch.distributed`` process
 group (any backend), NCCL itself is opened by libmdd with ``dlopen``.
@@ -26,7 +32,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["Communicator", "Shard", "shard_bounds", "make_shard", "setup_sharded"]
+__all__ = ["Communicator", "Shard", "shard_bounds", "make_shard", "setup_sharded", "row_block"]
 
 
 def shard_bounds(costs, nranks: int) -> np.ndarray:
@@ -54,6 +60,18 @@ def shard_bounds(costs, nranks: int) -> np.ndarray:
         # keep at least one subdomain per rank on either side
         b[r] = min(max(cut, b[r - 1] + 1), nsub - (nranks - r))
     return b
+
+
+def row_block(n: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Rows ``[lo, hi)`` of the Krylov vectors owned by ``rank`` in the sharded
+    CGS2 loop: blocks of ``ceil(n / nranks)`` rows (the last one shorter), the
+    layout ncclAllGather needs (equal per-rank counts, zero padding).  Mirrors
+    ``gmres_cgs`` in csrc/gmres.cu."""
+    if nranks < 1 or not 0 <= rank < nranks:
+        raise ValueError("bad rank / world size")
+    chunk = -(-n // nranks)
+    lo = min(n, rank * chunk)
+    return lo, min(n, lo + chunk)
 
 
 class Communicator:

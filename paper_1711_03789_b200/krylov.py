@@ -27,7 +27,16 @@ __all__ = ["KrylovConfig", "KrylovReport", "gmres"]
 
 @dataclass(frozen=True)
 class KrylovConfig:
-    """Reference krylov.py:25-43 (+ ``check_orthogonality``, default on as in the reference)."""
+    """Reference krylov.py:25-43 (+ ``check_orthogonality``, default on as in the reference).
+
+    ``orthogonalization`` (extension, not in the reference): ``"mgs"`` — the
+    reference's modified Gram-Schmidt with one reorthogonalisation pass
+    (krylov.py:137-143), the default — or ``"cgs2"``: classical Gram-Schmidt
+    with one reorthogonalisation pass, three reductions per iteration whatever
+    the basis size.  With a sharded preconditioner (:mod:`.distributed`)
+    ``"cgs2"`` also shards the Krylov vectors over the ranks by row blocks.
+    Unweighted inner products only.
+    """
 
     tol: float = 1e-6
     maxit: int = 200
@@ -37,6 +46,7 @@ class KrylovConfig:
     seed: int = 0
     keep_basis: bool = False
     check_orthogonality: bool = True
+    orthogonalization: str = "mgs"
 
     def __post_init__(self):
         if self.tol <= 0:
@@ -47,6 +57,8 @@ class KrylovConfig:
             raise ValueError(f"side must be 'left' or 'right', got {self.side!r}")
         if self.initial_guess not in ("zero", "random"):
             raise ValueError(f"unknown initial guess {self.initial_guess!r}")
+        if self.orthogonalization not in ("mgs", "cgs2"):
+            raise ValueError(f"orthogonalization must be 'mgs' or 'cgs2', got {self.orthogonalization!r}")
 
 
 @dataclass
@@ -184,6 +196,7 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, ou
     c.check_drift = 1 if cfg.check_orthogonality else 0
     c.keep_basis = 1 if cfg.keep_basis else 0
     c.device_io = 1 if dio else 0
+    c.ortho = 1 if cfg.orthogonalization == "cgs2" else 0
     x = out if dio else np.empty(n, dtype=np.complex128)
     hist = np.empty(cfg.maxit + 1, dtype=np.float64)
     drift = np.full(cfg.maxit + 1, np.nan)

@@ -1,10 +1,15 @@
-"""Sharded (multi-GPU) preconditioner: host logic on CPU with gloo, world_size 2.
+"""Sharded (multi-GPU) preconditioner and Krylov loop: host logic on CPU with
+gloo, world_size 2.
 
 The device path (libmdd ``mdd_prec_set_comm``) completes each rank's partial
 one-level sum with one allreduce and applies the replicated coarse terms
 afterwards; these tests check that decomposition of the work on the oracle:
 the per-rank partial sums, allreduced over gloo, reproduce the full
-one-level, additive, hybrid and ADEF1 applications.
+one-level, additive, hybrid and ADEF1 applications.  The sharded CGS2 GMRES
+of csrc/gmres.cu (``gmres_cgs``: row blocks of ``distributed.row_block``,
+allgather of each new basis vector, allreduced projections and norms) is
+restated step by step on gloo and must reproduce the oracle's MGS2 solve
+(iterations +-1, solution <= 1e-8).
 """
 
 import os
@@ -18,7 +23,7 @@ import torch.multiprocessing as mp
 from conftest import mesh_dict, rel
 from oracle import maxwell_oracle as O
 from paper_1711_03789_b200 import decomp, fem, mesh
-from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, shard_bounds
+from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, row_block, shard_bounds
 
 
 def test_shard_bounds_cover_and_balance():
@@ -105,6 +110,111 @@ def test_gloo_two_ranks_partial_sums():
     errq = ctx.SimpleQueue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def test_row_blocks_tile_the_vector():
+    for n, w in [(10, 1), (10, 3), (433720, 8), (7, 8), (64, 4)]:
+        blocks = [row_block(n, w, r) for r in range(w)]
+        assert blocks[0][0] == 0 and blocks[-1][1] == n
+        assert all(blocks[r][1] == blocks[r + 1][0] for r in range(w - 1))
+        assert all(0 <= hi - lo <= -(-n // w) for lo, hi in blocks)
+
+
+def _allgather_z(xl, n, world):
+    """ncclAllGather of equal-size zero-padded blocks -> the first n entries."""
+    import torch
+
+    chunk = -(-n // world)
+    pad = np.zeros(chunk, dtype=np.complex128)
+    pad[: len(xl)] = xl
+    t = torch.from_numpy(pad.view(np.float64).copy())
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return np.concatenate([p.numpy().view(np.complex128) for p in parts])[:n]
+
+
+def _cgs2_sharded(a, b, prec, tol, maxit, rank, world):
+    """Restatement of gmres_cgs (csrc/gmres.cu) on this rank's row block."""
+    n = len(b)
+    lo, hi = row_block(n, world, rank)
+    rows = a[lo:hi]
+    dots = lambda X, y: _allreduce_z(np.array([np.vdot(x, y) for x in X]))  # noqa: E731
+    r = b[lo:hi].copy()
+    beta = np.sqrt(_allreduce_z(np.array([np.vdot(r, r)]))[0].real)
+    V = [r / beta]
+    H = np.zeros((maxit + 1, maxit), dtype=complex)
+    g = np.zeros(maxit + 1, dtype=complex)
+    g[0] = beta
+    cs, sn = np.zeros(maxit, dtype=complex), np.zeros(maxit, dtype=complex)
+    hist = [1.0]
+    m = 0
+    for j in range(maxit):
+        w = rows @ prec(_allgather_z(V[j], n, world))
+        h1 = dots(V, w)
+        w = w - sum(h * v for h, v in zip(h1, V))
+        h2 = dots(V, w)
+        w = w - sum(h * v for h, v in zip(h2, V))
+        col = np.zeros(j + 2, dtype=complex)
+        col[: j + 1] = h1 + h2
+        col[j + 1] = np.sqrt(_allreduce_z(np.array([np.vdot(w, w)]))[0].real)
+        for i in range(j):  # krylov.py:162-187
+            t = cs[i] * col[i] + sn[i] * col[i + 1]
+            col[i + 1] = -np.conj(sn[i]) * col[i] + cs[i] * col[i + 1]
+            col[i] = t
+        am1, am = abs(col[j]), abs(col[j + 1])
+        den = np.hypot(am1, am)
+        cs[j] = am1 / den
+        sn[j] = (col[j] / am1 if am1 > 0 else 1.0) * np.conj(col[j + 1]) / den
+        H[: j + 2, j] = col
+        H[j, j] = cs[j] * col[j] + sn[j] * col[j + 1]
+        H[j + 1, j] = 0.0
+        g[j + 1] = -np.conj(sn[j]) * g[j]
+        g[j] = cs[j] * g[j]
+        hist.append(min(abs(g[j + 1]) / beta, hist[-1]))
+        m = j + 1
+        V.append(w / np.sqrt(_allreduce_z(np.array([np.vdot(w, w)]))[0].real))
+        if hist[-1] <= tol:
+            break
+    y = np.linalg.solve(np.triu(H[:m, :m]), g[:m])
+    u = sum(yi * v for yi, v in zip(y, V[:m]))
+    return prec(_allgather_z(u, n, world)), m
+
+
+def _cgs_worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        s, d, a = _problem()
+        r0 = d.coarse.R0
+        full = O.Schwarz(d.dofs, d.pou, O.minors(a, d.dofs), "as", "two", "additive", R0=r0,
+                         A0=(r0 @ a @ r0.T).tocsr(), A_corr=a, ndof=s.ndof, solver="dense")
+        b = np.random.default_rng(11).standard_normal(s.ndof) * (1 - 1j)
+        x, it = _cgs2_sharded(a, b, full.apply, 1e-8, 200, rank, world)
+        xr, _, itr, conv = O.gmres(a, b, full, tol=1e-8, maxit=200)
+        assert conv and abs(it - itr) <= 1, (it, itr)
+        assert rel(x, xr) <= 1e-8, rel(x, xr)
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as e:  # report to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_gloo_two_ranks_sharded_cgs2_gmres():
+    world = 2
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cgs_worker, args=(r, world, port, errq)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

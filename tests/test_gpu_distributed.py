@@ -60,3 +60,27 @@ def test_one_rank_nccl_bitwise(gpu, case, fam, cor):
     assert r1.iterations == r2.iterations and r1.converged
     assert np.array_equal(r1.residual_history, r2.residual_history)
     assert np.array_equal(r1.x, r2.x)
+
+
+@pytest.mark.parametrize("fam,cor", [("as", "additive"), ("ras", "hybrid")])
+def test_one_rank_nccl_sharded_cgs2(gpu, case, fam, cor):
+    """The sharded-vector CGS2 loop (ncclAllGather of each new basis vector,
+    row-block SpMV, ncclAllReduce of the projections) on a one-rank NCCL
+    communicator reproduces the unsharded CGS2 run bit for bit, and matches
+    the MGS2 run to the north_star tolerances."""
+    from paper_1711_03789_b200 import KrylovConfig, gmres, precond
+    from paper_1711_03789_b200.distributed import Communicator, setup_sharded
+
+    prob, d = case
+    spec = precond.PreconditionerSpec(fam, "two", cor, xi_prec=4.0)
+    ref = precond.setup(prob, d, spec)
+    st = setup_sharded(prob, d, spec, comm=Communicator(force_nccl=True))
+    cg = KrylovConfig(tol=1e-8, maxit=80, orthogonalization="cgs2")
+    r1 = gmres(prob.A, prob.rhs, precond=ref, config=cg)
+    r2 = gmres(prob.A, prob.rhs, precond=st, config=cg)
+    assert r1.converged and r1.iterations == r2.iterations
+    assert np.array_equal(r1.residual_history, r2.residual_history)
+    assert np.array_equal(r1.x, r2.x)
+    rm = gmres(prob.A, prob.rhs, precond=ref, config=KrylovConfig(tol=1e-8, maxit=80))
+    assert abs(rm.iterations - r1.iterations) <= 1
+    assert rel(r1.x, rm.x) <= 1e-8

@@ -201,3 +201,38 @@ def test_arnoldi_paths_match_reference(gpu, gg, monkeypatch, mode, wcap):
     assert rel(r.x, gg[f"{tag}_x"]) <= 1e-8
     assert r.iterations == base.iterations
     assert np.allclose(r.residual_history, base.residual_history, rtol=1e-10, atol=1e-15)
+
+
+@pytest.mark.parametrize("side", ["right", "left"])
+def test_cgs2_matches_reference(gpu, gg, side):
+    """CGS2 (the sharded multi-GPU Krylov loop; KrylovConfig extension) against
+    the reference's MGS2 golden runs: iterations +-1, solution <= 1e-8."""
+    from paper_1711_03789_b200 import decomp, fem, mesh, precond
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(4), "pec")
+    prob = fem.assemble(s, fem.Coefficients(k=3.0, xi=9.0), source=fem.gaussian_source)
+    d = decomp.build_decomposition(s, 2, 1, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(2), "pec"))
+    fam, cor = ("as", "additive") if side == "right" else ("ras", "hybrid")
+    st = precond.setup(prob, d, precond.PreconditionerSpec(fam, "two", cor, xi_prec=9.0, side=side))
+    r = gmres(prob.A, prob.rhs, precond=st,
+              config=KrylovConfig(tol=1e-8, maxit=200, side=side, orthogonalization="cgs2"))
+    tag = f"{fam}_two_{cor}_{side}_id"
+    assert r.converged and abs(r.iterations - int(gg[f"{tag}_it"])) <= 1
+    assert rel(r.x, gg[f"{tag}_x"]) <= 1e-8
+    assert not r.ortho_warning
+
+
+def test_cgs2_dense_and_random_guess(gpu, gg):
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    r = gmres(gg["dense_a"], gg["dense_b"], config=KrylovConfig(tol=1e-12, maxit=120, orthogonalization="cgs2"))
+    assert r.converged and abs(r.iterations - int(gg["dense_it"])) <= 1
+    assert rel(r.x, gg["dense_x"]) <= 1e-10
+    rng = np.random.default_rng(5)
+    a, b = _random_system(rng, 40)
+    r = gmres(a, b, config=KrylovConfig(tol=1e-10, initial_guess="random", seed=3, orthogonalization="cgs2"))
+    assert r.converged
+    assert np.linalg.norm(b - a @ r.x) / np.linalg.norm(b) <= 1e-9
+    z = gmres(a, np.zeros(40), config=KrylovConfig(orthogonalization="cgs2"))
+    assert z.converged and z.iterations == 0
