@@ -126,6 +126,7 @@ __device__ __forceinline__ void reduce_step(const double2* p, int G, double2* sh
 }
 
 constexpr int kArnE = 12;  // vector elements per thread kept in registers (register path)
+constexpr int kArnPf = 4;  // REG path: L2 prefetch distance in MGS steps
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -299,6 +300,8 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     if (threadIdx.x == 0) prefetch_l2(xvec(1) + lo, len * 16);
   }
   if constexpr (REG) {
+    if (threadIdx.x == 0)
+      for (int t = 2; t < kArnPf && t < nsteps; ++t) prefetch_l2(xvec(t) + lo, len * 16);
 #pragma unroll
     for (int k = 0; k < kArnE; ++k) {
       const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
@@ -347,6 +350,9 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
       if (!REG && s + 2 < nsteps) prefetch_l2(xvec(s + 2) + lo, len * 16);
+      // REG: the register preload of X_{s+2} happens after this step's publish;
+      // an L2 bulk prefetch kArnPf steps ahead makes that preload an L2 hit
+      if (REG && s + kArnPf < nsteps) prefetch_l2(xvec(s + kArnPf) + lo, len * 16);
     }
     const bool last = (s + 1 == nsteps);
     const bool drift_next = do_drift && s + 1 < m - 1;
