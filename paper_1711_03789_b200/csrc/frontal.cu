@@ -475,6 +475,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   front_total = 0;
   uvec_total = 0;
   factor_flops = 0;
+  schur_flops = 0;
   factor_entries = 0;
   max_np = 0;
   max_m = 0;
@@ -505,6 +506,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       max_np = std::max(max_np, nd.np);
       max_m = std::max(max_m, nd.m);
       factor_flops += 8.0 * nd.np * (double)nd.m * nd.m;
+      schur_flops += 8.0 * nd.np * (double)nd.nu * nd.nu;
       factor_entries += (double)nd.m * nd.m - (double)nd.nu * nd.nu;
     }
   // packed F_UP rows for the solve kernels live after the fronts
@@ -705,6 +707,22 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     attr_set = true;
   }
   build_solve(lev);
+  if (getenv("MDD_PLAN_STATS")) {
+    // per-level histogram: nodes, sum np, max m, GJ flops, Schur flops
+    for (int L = 0; L < nlevels; ++L) {
+      double gj = 0, sc = 0, sm = 0;
+      int mx = 0;
+      for (int32_t g : lev[L]) {
+        const NodeDev& nd = h_nodes[g];
+        sc += 8.0 * nd.np * (double)nd.nu * nd.nu;
+        gj += 8.0 * nd.np * ((double)nd.m * nd.m - (double)nd.nu * nd.nu);
+        sm += nd.np;
+        mx = std::max(mx, nd.m);
+      }
+      fprintf(stderr, "[plan] L%d nodes=%zu sum_np=%.0f max_m=%d gj_flops=%.3e schur_flops=%.3e\n", L,
+              lev[L].size(), sm, mx, gj, sc);
+    }
+  }
   CK(cudaStreamSynchronize(s));
 }
 

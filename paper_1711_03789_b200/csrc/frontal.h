@@ -92,7 +92,7 @@ struct FrontPlan {
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
-  double factor_flops = 0, factor_entries = 0;
+  double factor_flops = 0, factor_entries = 0, schur_flops = 0;
   // numeric storage
   DevBuf<double2> fronts, uvec, pbuf, wbuf;
   DevBuf<double> pivstat;  // per node: [min |pivot|, max |pivot|]
