@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(kPanelCols) k_panel(const int2* __restrict__ t
     P[t / kPB][t % kPB] = pbuf[(int64_t)ai * kPB * kPB + t];
   __syncthreads();
   double2* T = fronts + nd.front_off;
+  const int np = nd.np;
   const int c = chunk * kPanelCols + threadIdx.x;
-  if (c < m) {
+  if (c < np) {  // the sweeps work on the pivot block only (F_PU, F_UP, F_UU: GEMMs)
     if (c >= K0 && c < K0 + kb) {
       for (int r = 0; r < kb; ++r) T[(int64_t)(K0 + r) * m + c] = cneg(P[r][c - K0]);
     } else {
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kPanelCols) k_panel(const int2* __restrict__ t
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int rr = wid; rr < kPanelCols; rr += kPanelCols / 32) {
     const int r = chunk * kPanelCols + rr;
-    if (r >= m) break;
+    if (r >= np) break;
     const bool inK = r >= K0 && r < K0 + kb;
     W[(int64_t)r * kPB + lane] =
         (inK || lane >= kb) ? make_double2(0.0, 0.0) : T[(int64_t)r * m + K0 + lane];
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(256, 2) k_update(const int4* __restrict__ task
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
-        const bool load = rok && c < m && !(c >= K0 && c < K0 + kb) && !(r >= nd.np && c >= nd.np);
+        const bool load = rok && c < nd.np && !(c >= K0 && c < K0 + kb) && r < nd.np;
         old[i][j][e] = load ? T[(int64_t)r * m + c] : make_double2(0.0, 0.0);
       }
   }
@@ -285,48 +286,51 @@ __global__ void __launch_bounds__(256, 2) k_update(const int4* __restrict__ task
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
-        if (c >= m || (r >= nd.np && c >= nd.np)) continue;  // F_UU: deferred Schur GEMM
+        if (c >= nd.np || r >= nd.np) continue;  // outside the pivot block: k_gemm
         T[(int64_t)r * m + c] =
             make_double2(old[i][j][e].x - cre[i][j][e], old[i][j][e].y - cim[i][j][e]);
       }
   }
 }
 
-// Deferred Schur complement of one 64x64 tile of F_UU on the FP64 tensor
-// cores:  F_UU -= C_orig F_PU  (K = np), with C_orig the F_UP block saved
-// before the sweeps (the sweeps skip F_UU) and F_PU = F_PP^{-1} F_PU after
-// them.  One GEMM with K = np replaces np/32 rank-32 passes over F_UU.
-// K is consumed in chunks of kSchurKC through a 2-stage cp.async pipeline;
-// padded shared-memory rows keep the DMMA fragment loads conflict-free.
+// Batched complex GEMM tiles on the FP64 tensor cores (DMMA), used for the
+// parts of each front the pivot-block sweeps leave out (A = F_PP, with
+// -A^{-1} in place after the sweeps; B_orig / C_orig the original F_PU / F_UP):
+//   F_PU = A^{-1} B_orig = -(-A^{-1}) B_orig          (mode 0)
+//   F_UP = C_orig A^{-1} = -C_orig (-A^{-1})          (mode 0)
+//   F_UU -= C_orig F_PU   (deferred Schur complement) (mode 1)
+// Each is one GEMM with K = np instead of np/32 rank-32 passes.  One 64x64
+// output tile per CTA, 8 warps of 16x32, complex product = 4 real DMMA
+// products; K is consumed in chunks of kGemmKC through a 2-stage cp.async
+// pipeline; padded shared-memory rows keep the fragment loads conflict-free.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
-__global__ void __launch_bounds__(256, 2) k_schur(const int4* __restrict__ tasks, const NodeDev* __restrict__ nodes,
-                                               double2* __restrict__ fronts) {
+__global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ tasks, double2* __restrict__ fronts,
+                                                 const double2* __restrict__ bbuf) {
   extern __shared__ double2 sm[];
-  constexpr int LA = kSchurKC + 4, LB = kTile + 2;  // padded leading dimensions
-  const int4 tk = tasks[blockIdx.x];
-  const NodeDev nd = nodes[tk.x];
-  const int m = nd.m, np = nd.np, nu = nd.nu;
-  const int r0 = tk.y * kTile, c0 = tk.z * kTile;
-  const double2* Cg = fronts + nd.upk_off;                         // nu x np, ld np
-  const double2* Bg = fronts + nd.front_off + np;                  // np x nu, ld m
-  double2* Dg = fronts + nd.front_off + (int64_t)np * m + np;      // nu x nu, ld m
-  auto As = [&](int st) { return sm + st * (kTile * LA + kSchurKC * LB); };
-  auto Bs = [&](int st) { return sm + st * (kTile * LA + kSchurKC * LB) + kTile * LA; };
+  constexpr int LA = kGemmKC + 4, LB = kTile + 2;  // padded leading dimensions
+  const GemmTask tk = tasks[blockIdx.x];
+  const int M = tk.M, N = tk.N, K = tk.K, r0 = tk.r0, c0 = tk.c0;
+  const double2* Xg = fronts + tk.xo;
+  const double2* Wg = (tk.wsel ? bbuf : fronts) + tk.wo;
+  double2* Og = fronts + tk.oo;
+  const int ldx = tk.ldx, ldw = tk.ldw, ldo = tk.ldo;
+  auto As = [&](int st) { return sm + st * (kTile * LA + kGemmKC * LB); };
+  auto Bs = [&](int st) { return sm + st * (kTile * LA + kGemmKC * LB) + kTile * LA; };
   auto load = [&](int st, int k0) {
     double2* A = As(st);
     double2* B = Bs(st);
-    for (int t = threadIdx.x; t < kTile * kSchurKC; t += 256) {
-      const int rr = t / kSchurKC, kk = t % kSchurKC;
-      const bool ok = r0 + rr < nu && k0 + kk < np;
-      cp_async16(A + rr * LA + kk, ok ? Cg + (int64_t)(r0 + rr) * np + k0 + kk : Cg, ok);
+    for (int t = threadIdx.x; t < kTile * kGemmKC; t += 256) {
+      const int rr = t / kGemmKC, kk = t % kGemmKC;
+      const bool ok = r0 + rr < M && k0 + kk < K;
+      cp_async16(A + rr * LA + kk, ok ? Xg + (int64_t)(r0 + rr) * ldx + k0 + kk : Xg, ok);
     }
-    for (int t = threadIdx.x; t < kSchurKC * kTile; t += 256) {
+    for (int t = threadIdx.x; t < kGemmKC * kTile; t += 256) {
       const int kk = t / kTile, cc = t % kTile;
-      const bool ok = k0 + kk < np && c0 + cc < nu;
-      cp_async16(B + kk * LB + cc, ok ? Bg + (int64_t)(k0 + kk) * m + c0 + cc : Bg, ok);
+      const bool ok = k0 + kk < K && c0 + cc < N;
+      cp_async16(B + kk * LB + cc, ok ? Wg + (int64_t)(k0 + kk) * ldw + c0 + cc : Wg, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -338,11 +342,11 @@ __global__ void __launch_bounds__(256, 2) k_schur(const int4* __restrict__ tasks
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
-  const int nk = (np + kSchurKC - 1) / kSchurKC;
+  const int nk = (K + kGemmKC - 1) / kGemmKC;
   load(0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) {
-      load((kc + 1) & 1, (kc + 1) * kSchurKC);
+      load((kc + 1) & 1, (kc + 1) * kGemmKC);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) k_schur(const int4* __restrict__ tasks
     const double2* A = As(kc & 1);
     const double2* B = Bs(kc & 1);
 #pragma unroll
-    for (int kk = 0; kk < kSchurKC / 4; ++kk) {
+    for (int kk = 0; kk < kGemmKC / 4; ++kk) {
       double are[2], aim[2], naim[2], bre[4], bim[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -378,30 +382,36 @@ __global__ void __launch_bounds__(256, 2) k_schur(const int4* __restrict__ tasks
     }
     __syncthreads();  // stage kc&1 is refilled by the next iteration's load
   }
-  double2 old[2][4][2];
+  const bool acc = tk.mode == 1;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = r0 + wr + 8 * i + gid;
+    if (r >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = c0 + wc + 8 * j + 2 * tig + e;
-        old[i][j][e] = (r < nu && c < nu) ? Dg[(int64_t)r * m + c] : make_double2(0.0, 0.0);
+        if (c >= N) continue;
+        double2* o = Og + (int64_t)r * ldo + c;
+        const double2 old = acc ? *o : make_double2(0.0, 0.0);
+        *o = make_double2(old.x - cre[i][j][e], old.y - cim[i][j][e]);
       }
   }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int r = r0 + wr + 8 * i + gid;
-    if (r >= nu) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = c0 + wc + 8 * j + 2 * tig + e;
-        if (c < nu) Dg[(int64_t)r * m + c] = make_double2(old[i][j][e].x - cre[i][j][e], old[i][j][e].y - cim[i][j][e]);
-      }
-  }
+}
+
+// B_orig rows: front row r (< np), columns np..m -> bbuf (np x nu, row-major)
+__global__ void __launch_bounds__(256) k_copy_b(const int2* __restrict__ tasks, int64_t ntask,
+                                                const NodeDev* __restrict__ nodes,
+                                                const double2* __restrict__ fronts, double2* __restrict__ bbuf) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ntask) return;
+  const int2 tk = tasks[w];
+  const NodeDev nd = nodes[tk.x];
+  const double2* src = fronts + nd.front_off + (int64_t)tk.y * nd.m + nd.np;
+  double2* dst = bbuf + nd.bb_off + (int64_t)tk.y * nd.nu;
+  for (int q = lane; q < nd.nu; q += 32) dst[q] = src[q];
 }
 
 __global__ void k_pivinit(double* p, int64_t n) {
@@ -592,8 +602,9 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int64_t> h_epos;
   std::vector<int32_t> h_esrc;
   std::vector<int2> h_init, h_panel;
-  std::vector<int4> h_tile, h_schur;
-  std::vector<int2> h_pack;
+  std::vector<int4> h_tile;
+  std::vector<int2> h_pack, h_copyb;
+  std::vector<GemmTask> h_yz, h_s;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
   lev_ent_off.assign(1, 0);
@@ -604,7 +615,10 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   step_panel_off.assign(1, 0);
   step_tile_off.assign(1, 0);
   lev_pack_off.assign(1, 0);
-  lev_schur_off.assign(1, 0);
+  lev_copyb_off.assign(1, 0);
+  lev_yz_off.assign(1, 0);
+  lev_s_off.assign(1, 0);
+  int64_t bb_max = 0;
   w_max = 0;
   max_act = 0;
   int64_t nsteps_total = 0;
@@ -613,22 +627,41 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     h_esrc.insert(h_esrc.end(), esrc[L].begin(), esrc[L].end());
     lev_ent_off.push_back((int64_t)h_epos.size());
     int32_t lnp = 0;
+    int64_t bb = 0;  // B_orig workspace of this level
     for (int32_t g : lev[L]) {
-      const NodeDev& nd = h_nodes[g];
+      NodeDev& nd = h_nodes[g];
       for (int r = 0; r < nd.m; ++r) h_init.push_back(make_int2(g, r));
       lnp = std::max(lnp, nd.np);
+      nd.bb_off = bb;
       if (nd.np > 0 && nd.nu > 0) {
-        // F_UP rows (pack: the original block before the sweeps, F_UP after)
+        bb += (int64_t)nd.np * nd.nu;
+        // C_orig (pack before the sweeps; the final F_UP is packed after all levels)
         for (int u = 0; u < nd.nu; ++u) h_pack.push_back(make_int2((int)g, u));
-        // deferred Schur complement F_UU -= C_orig F_PU, 64x64 tiles
-        const int nt = (nd.nu + kTile - 1) / kTile;
-        for (int tr = 0; tr < nt; ++tr)
-          for (int tc = 0; tc < nt; ++tc) h_schur.push_back(make_int4(g, tr, tc, 0));
+        for (int r = 0; r < nd.np; ++r) h_copyb.push_back(make_int2((int)g, r));
+        const int np = nd.np, nu = nd.nu, m = nd.m;
+        const int64_t A = nd.front_off, B = nd.front_off + np, C = nd.front_off + (int64_t)np * m,
+                      D = C + np;
+        auto tiles = [&](std::vector<GemmTask>& out, int64_t xo, int ldx, int64_t wo, int ldw, int wsel,
+                         int64_t oo, int M, int N, int mode) {
+          for (int r0 = 0; r0 < M; r0 += kTile)
+            for (int c0 = 0; c0 < N; c0 += kTile) {
+              GemmTask t{};
+              t.xo = xo; t.ldx = ldx; t.wo = wo; t.ldw = ldw; t.wsel = wsel; t.oo = oo; t.ldo = m;
+              t.M = M; t.N = N; t.K = np; t.r0 = r0; t.c0 = c0; t.mode = mode;
+              out.push_back(t);
+            }
+        };
+        tiles(h_yz, A, m, nd.bb_off, nu, 1, B, np, nu, 0);    // F_PU = -(-A^-1) B_orig
+        tiles(h_yz, nd.upk_off, np, A, m, 0, C, nu, np, 0);   // F_UP = -C_orig (-A^-1)
+        tiles(h_s, nd.upk_off, np, B, m, 0, D, nu, nu, 1);    // F_UU -= C_orig F_PU
       }
     }
+    bb_max = std::max(bb_max, bb);
     lev_init_off.push_back((int64_t)h_init.size());
     lev_pack_off.push_back((int64_t)h_pack.size());
-    lev_schur_off.push_back((int64_t)h_schur.size());
+    lev_copyb_off.push_back((int64_t)h_copyb.size());
+    lev_yz_off.push_back((int64_t)h_yz.size());
+    lev_s_off.push_back((int64_t)h_s.size());
     const int nst = (lnp + kPB - 1) / kPB;
     lev_steps[L] = nst;
     lev_step_base[L] = nsteps_total;
@@ -642,16 +675,14 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
         h_act.push_back(g);
         h_woff.push_back(wo);
         wo += (int64_t)nd.m * kPB;
-        for (int ch = 0; ch * kPanelCols < nd.m; ++ch) h_panel.push_back(make_int2(ai, ch));
+        // sweeps over the pivot block A only (F_PU, F_UP, F_UU: k_gemm)
+        for (int ch = 0; ch * kPanelCols < nd.np; ++ch) h_panel.push_back(make_int2(ai, ch));
         const int K0 = st * kPB, kb = std::min(kPB, nd.np - K0);
-        const int nt = (nd.m + kTile - 1) / kTile;
+        const int nt = (nd.np + kTile - 1) / kTile;
         for (int tr = 0; tr < nt; ++tr) {
-          const int rb = tr * kTile, re = std::min(nd.m, rb + kTile);
+          const int rb = tr * kTile, re = std::min(nd.np, rb + kTile);
           if (rb >= K0 && re <= K0 + kb) continue;  // tile rows all pivots
-          for (int tc = 0; tc < nt; ++tc) {
-            if (rb >= nd.np && tc * kTile >= nd.np) continue;  // inside F_UU: deferred Schur GEMM
-            h_tile.push_back(make_int4(ai, tr, tc, 0));
-          }
+          for (int tc = 0; tc < nt; ++tc) h_tile.push_back(make_int4(ai, tr, tc, 0));
         }
       }
       w_max = std::max(w_max, wo);
@@ -684,8 +715,16 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   init_tasks.upload(h_init, s);
   panel_tasks.upload(h_panel, s);
   tile_tasks.upload(h_tile, s);
-  schur_tasks.upload(h_schur, s);
   npack = (int64_t)h_pack.size();
+  copyb_tasks.upload(h_copyb, s);
+  // one task list: the YZ tiles of every level, then the Schur tiles of every level
+  {
+    const int64_t nyz = (int64_t)h_yz.size();
+    for (auto& o : lev_s_off) o += nyz;
+    h_yz.insert(h_yz.end(), h_s.begin(), h_s.end());
+    gemm_tasks.upload(h_yz, s);
+  }
+  bbuf.alloc(std::max<int64_t>(1, bb_max));
   act_node.upload(h_act, s);
   act_woff.upload(h_woff, s);
   fronts.alloc(front_total + upk_total);
@@ -701,7 +740,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
-    CK(cudaFuncSetAttribute(k_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSchurSmem));
+    CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
     CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
     attr_set = true;
@@ -756,6 +795,11 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
       k_pack_up<<<(unsigned)((npk + 7) / 8), 256, 0, s>>>(pack_tasks.p + pk0, npk, nodes.p, fronts.p);
       CK_LAUNCH(ctx);
     }
+    const int64_t cb0 = lev_copyb_off[L], ncb = lev_copyb_off[L + 1] - cb0;
+    if (ncb) {  // B_orig = F_PU before the sweeps
+      k_copy_b<<<(unsigned)((ncb + 7) / 8), 256, 0, s>>>(copyb_tasks.p + cb0, ncb, nodes.p, fronts.p, bbuf.p);
+      CK_LAUNCH(ctx);
+    }
     for (int st = 0; st < lev_steps[L]; ++st) {
       const int64_t si = lev_step_base[L] + st;
       const int64_t a0 = step_act_off[si], na = step_act_off[si + 1] - a0;
@@ -774,9 +818,14 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
         CK_LAUNCH(ctx);
       }
     }
-    const int64_t sc0 = lev_schur_off[L], nsc = lev_schur_off[L + 1] - sc0;
-    if (nsc) {
-      k_schur<<<(unsigned)nsc, 256, kSchurSmem, s>>>(schur_tasks.p + sc0, nodes.p, fronts.p);
+    const int64_t y0 = lev_yz_off[L], ny = lev_yz_off[L + 1] - y0;
+    if (ny) {  // F_PU and F_UP from -A^{-1}
+      k_gemm<<<(unsigned)ny, 256, kGemmSmem, s>>>(gemm_tasks.p + y0, fronts.p, bbuf.p);
+      CK_LAUNCH(ctx);
+    }
+    const int64_t s0 = lev_s_off[L], nsg = lev_s_off[L + 1] - s0;
+    if (nsg) {  // deferred Schur complement
+      k_gemm<<<(unsigned)nsg, 256, kGemmSmem, s>>>(gemm_tasks.p + s0, fronts.p, bbuf.p);
       CK_LAUNCH(ctx);
     }
   }

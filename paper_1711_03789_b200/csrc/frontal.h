@@ -29,8 +29,8 @@ namespace mdd {
 constexpr int kPB = 32;      // pivot block of the sweep
 constexpr int kTile = 64;    // update tile
 constexpr int kPanelCols = 128;
-constexpr int kSchurKC = 16;  // K chunk of the deferred Schur GEMM
-constexpr size_t kSchurSmem = 2 * sizeof(double2) * (kTile * (kSchurKC + 4) + kSchurKC * (kTile + 2));
+constexpr int kGemmKC = 16;  // K chunk of the front GEMMs (k_gemm)
+constexpr size_t kGemmSmem = 2 * sizeof(double2) * (kTile * (kGemmKC + 4) + kGemmKC * (kTile + 2));
 
 struct NodeDev {
   int64_t front_off;  // complex elements into the front storage
@@ -41,6 +41,16 @@ struct NodeDev {
   int32_t mat_off;    // offset of the node's matrix in the local vector space
   int32_t nch, child_off, mat;
   int64_t upk_off;    // packed F_UP rows (solve.cu), elements into the front storage
+  int64_t bb_off;     // B_orig workspace (np x nu) of the node's level, elements into bbuf
+};
+
+// One 64x64 output tile of a batched complex GEMM on the fronts (k_gemm):
+//   mode 0: O = -X W     mode 1: O -= X W
+// X (M x K, ld ldx), W (K x N, ld ldw), O (M x N, ld ldo) as element offsets
+// into the front storage (wsel bit 0: W lives in the B_orig workspace).
+struct GemmTask {
+  int64_t xo, wo, oo;
+  int32_t ldx, ldw, ldo, M, N, K, r0, c0, mode, wsel;
 };
 
 // one solve task (solve.cu): rows [r0, r0+nrow) of a front block of row length len
@@ -87,8 +97,12 @@ struct FrontPlan {
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
-  DevBuf<int4> schur_tasks;                  // {node, tile row, tile col} over F_UU
-  std::vector<int64_t> lev_pack_off, lev_schur_off;
+  // per level: C_orig pack tasks, B_orig copy tasks, GEMM tiles for
+  // F_PU = A^-1 B and F_UP = C A^-1 (one launch) and the Schur update (next launch)
+  DevBuf<int2> copyb_tasks;
+  DevBuf<GemmTask> gemm_tasks;
+  DevBuf<double2> bbuf;
+  std::vector<int64_t> lev_pack_off, lev_copyb_off, lev_yz_off, lev_s_off;
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
