@@ -285,6 +285,7 @@ def run_mine(args, rank, world):
         p = fem.assemble(space, coeffs)
         ctx.record(1)
         a_prec = fem.assemble(space, prec_coeffs).A
+        ctx.record(4)
         st.refactor(a_prec, prec_coeffs)
         ctx.record(2)
         if device_io:
@@ -310,7 +311,7 @@ def run_mine(args, rank, world):
             ctx.record(3)
             ms = ctx.elapsed_ms(0, 3)
             ms_steps.append(ms)
-            phases.append((ctx.elapsed_ms(0, 1), ctx.elapsed_ms(1, 2), ctx.elapsed_ms(2, 3)))
+            phases.append((ctx.elapsed_ms(0, 1), ctx.elapsed_ms(1, 2), ctx.elapsed_ms(2, 3), ctx.elapsed_ms(4, 2)))
             host += np.array(ctx.timers()[3:7])
             reps.append(rep)
     ctx.synchronize()
@@ -363,11 +364,12 @@ def run_mine(args, rank, world):
                        "algorithmic_bytes_per_launch": b, "ms_per_step": t * its, "launch": what,
                        "traffic": traffic.get(k)}
     fpk = read_fp64_peak()
-    f_ach = stats["factor_flops"] / (stats["factor_ms"] / 1e3) / 1e12 if stats["factor_ms"] > 0 else 0.0
+    fac_ms = float(np.mean([p[3] for p in phases]))  # numeric refactorisation inside the timed steps
+    f_ach = stats["factor_flops"] / (fac_ms / 1e3) / 1e12 if fac_ms > 0 else 0.0
     roof_factor = {"bound": "tensor", "kernel": "numeric factorisation (k_front_init/k_invert/k_panel/"
                                                 "k_update DMMA), subdomains + coarse",
                    "achieved": f_ach, "peak": fpk["tflops"], "unit": "TFLOP/s", "frac": f_ach / fpk["tflops"],
-                   "flops": stats["factor_flops"], "ms": stats["factor_ms"], "peak_source": fpk["source"]}
+                   "flops": stats["factor_flops"], "ms": fac_ms, "peak_source": fpk["source"]}
     hist = rep.residual_history
     res = {
         "metric": METRIC,
@@ -401,6 +403,7 @@ def run_mine(args, rank, world):
         "phases_ms": {"assemble_A": float(np.mean([p[0] for p in phases])),
                       "assemble_Aprec_factor": float(np.mean([p[1] for p in phases])),
                       "gmres": float(np.mean([p[2] for p in phases])),
+                      "factor": float(np.mean([p[3] for p in phases])),
                       "gmres_spmv": t_op, "gmres_precond": t_prec, "gmres_arnoldi": t_arn,
                       "gmres_host_setup": h_setup, "gmres_host_loop": h_loop, "gmres_host_final": h_final,
                       "gmres_graph_build": h_graph},

@@ -603,7 +603,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int32_t> h_esrc;
   std::vector<int2> h_init, h_panel;
   std::vector<int4> h_tile;
-  std::vector<int2> h_pack, h_copyb;
+  std::vector<int2> h_copyb;
   std::vector<GemmTask> h_yz, h_s;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
@@ -614,7 +614,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   step_act_off.assign(1, 0);
   step_panel_off.assign(1, 0);
   step_tile_off.assign(1, 0);
-  lev_pack_off.assign(1, 0);
   lev_copyb_off.assign(1, 0);
   lev_yz_off.assign(1, 0);
   lev_s_off.assign(1, 0);
@@ -635,30 +634,29 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       nd.bb_off = bb;
       if (nd.np > 0 && nd.nu > 0) {
         bb += (int64_t)nd.np * nd.nu;
-        // C_orig (pack before the sweeps; the final F_UP is packed after all levels)
-        for (int u = 0; u < nd.nu; ++u) h_pack.push_back(make_int2((int)g, u));
+        // the front's F_UP block keeps C_orig (the sweeps do not touch it); the
+        // F_UP GEMM writes the final values straight into the packed solve layout
         for (int r = 0; r < nd.np; ++r) h_copyb.push_back(make_int2((int)g, r));
         const int np = nd.np, nu = nd.nu, m = nd.m;
         const int64_t A = nd.front_off, B = nd.front_off + np, C = nd.front_off + (int64_t)np * m,
                       D = C + np;
         auto tiles = [&](std::vector<GemmTask>& out, int64_t xo, int ldx, int64_t wo, int ldw, int wsel,
-                         int64_t oo, int M, int N, int mode) {
+                         int64_t oo, int ldo, int M, int N, int mode) {
           for (int r0 = 0; r0 < M; r0 += kTile)
             for (int c0 = 0; c0 < N; c0 += kTile) {
               GemmTask t{};
-              t.xo = xo; t.ldx = ldx; t.wo = wo; t.ldw = ldw; t.wsel = wsel; t.oo = oo; t.ldo = m;
+              t.xo = xo; t.ldx = ldx; t.wo = wo; t.ldw = ldw; t.wsel = wsel; t.oo = oo; t.ldo = ldo;
               t.M = M; t.N = N; t.K = np; t.r0 = r0; t.c0 = c0; t.mode = mode;
               out.push_back(t);
             }
         };
-        tiles(h_yz, A, m, nd.bb_off, nu, 1, B, np, nu, 0);    // F_PU = -(-A^-1) B_orig
-        tiles(h_yz, nd.upk_off, np, A, m, 0, C, nu, np, 0);   // F_UP = -C_orig (-A^-1)
-        tiles(h_s, nd.upk_off, np, B, m, 0, D, nu, nu, 1);    // F_UU -= C_orig F_PU
+        tiles(h_yz, A, m, nd.bb_off, nu, 1, B, m, np, nu, 0);            // F_PU = -(-A^-1) B_orig
+        tiles(h_yz, C, m, A, m, 0, nd.upk_off, np, nu, np, 0);           // F_UP = -C_orig (-A^-1), packed
+        tiles(h_s, C, m, B, m, 0, D, m, nu, nu, 1);                      // F_UU -= C_orig F_PU
       }
     }
     bb_max = std::max(bb_max, bb);
     lev_init_off.push_back((int64_t)h_init.size());
-    lev_pack_off.push_back((int64_t)h_pack.size());
     lev_copyb_off.push_back((int64_t)h_copyb.size());
     lev_yz_off.push_back((int64_t)h_yz.size());
     lev_s_off.push_back((int64_t)h_s.size());
@@ -715,7 +713,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   init_tasks.upload(h_init, s);
   panel_tasks.upload(h_panel, s);
   tile_tasks.upload(h_tile, s);
-  npack = (int64_t)h_pack.size();
   copyb_tasks.upload(h_copyb, s);
   // one task list: the YZ tiles of every level, then the Schur tiles of every level
   {
@@ -728,7 +725,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   act_node.upload(h_act, s);
   act_woff.upload(h_woff, s);
   fronts.alloc(front_total + upk_total);
-  pack_tasks.upload(h_pack, s);
   uvec.alloc(std::max<int64_t>(1, uvec_total));
   pbuf.alloc(std::max<int64_t>(1, (int64_t)max_act * kPB * kPB));
   wbuf.alloc(std::max<int64_t>(1, w_max));
@@ -789,12 +785,6 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
           ne, ent_pos.p + lev_ent_off[L], ent_src.p + lev_ent_off[L], vals, fronts.p);
       CK_LAUNCH(ctx);
     }
-    // C_orig = F_UP before the sweeps (the packed F_UP region is free until pack())
-    const int64_t pk0 = lev_pack_off[L], npk = lev_pack_off[L + 1] - pk0;
-    if (npk) {
-      k_pack_up<<<(unsigned)((npk + 7) / 8), 256, 0, s>>>(pack_tasks.p + pk0, npk, nodes.p, fronts.p);
-      CK_LAUNCH(ctx);
-    }
     const int64_t cb0 = lev_copyb_off[L], ncb = lev_copyb_off[L + 1] - cb0;
     if (ncb) {  // B_orig = F_PU before the sweeps
       k_copy_b<<<(unsigned)((ncb + 7) / 8), 256, 0, s>>>(copyb_tasks.p + cb0, ncb, nodes.p, fronts.p, bbuf.p);
@@ -829,7 +819,6 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
       CK_LAUNCH(ctx);
     }
   }
-  pack(s);
 }
 
 int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {

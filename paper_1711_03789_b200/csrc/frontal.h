@@ -97,12 +97,12 @@ struct FrontPlan {
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
-  // per level: C_orig pack tasks, B_orig copy tasks, GEMM tiles for
-  // F_PU = A^-1 B and F_UP = C A^-1 (one launch) and the Schur update (next launch)
+  // per level: B_orig copy tasks, GEMM tiles for F_PU = A^-1 B and
+  // F_UP = C A^-1 (one launch) and the Schur update (next launch)
   DevBuf<int2> copyb_tasks;
   DevBuf<GemmTask> gemm_tasks;
   DevBuf<double2> bbuf;
-  std::vector<int64_t> lev_pack_off, lev_copyb_off, lev_yz_off, lev_s_off;
+  std::vector<int64_t> lev_copyb_off, lev_yz_off, lev_s_off;
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
@@ -113,13 +113,11 @@ struct FrontPlan {
   // solve workspace (local vectors)
   DevBuf<double2> bloc, fpst, xloc;
   float factor_ms = 0;
-  // solve (solve.cu): packed F_UP rows, per-level task lists
-  int64_t npack = 0, upk_total = 0;
-  DevBuf<int2> pack_tasks;
+  // solve (solve.cu): per-level task lists over the fronts and the packed F_UP rows
+  int64_t upk_total = 0;
   DevBuf<LvlTask> ltasks;
   std::vector<int64_t> lvl_off, lvl_dcap, lvl_zcap;  // forward levels ascending, then backward descending
   void build_solve(const std::vector<std::vector<int32_t>>& lev);
-  void pack(cudaStream_t s);
 
   // build from analysed matrices
   void build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf);
@@ -131,9 +129,5 @@ struct FrontPlan {
   // gathered as v[gidx[i]] inside the solve (fused restriction)
   void solve(cudaStream_t s, const double2* v = nullptr, const int32_t* gidx = nullptr);
 };
-
-// F_UP rows of the listed (node, row) pairs -> packed row-contiguous blocks (solve.cu)
-__global__ void k_pack_up(const int2* __restrict__ tasks, int64_t ntask, const NodeDev* __restrict__ nodes,
-                          double2* __restrict__ fronts);
 
 }  // namespace mdd

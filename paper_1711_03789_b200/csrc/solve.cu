@@ -8,8 +8,8 @@
 //                      backward x_P  = -(F_PP r_P + F_PU x_U)   (root -> leaves)
 // One launch per tree level, one CTA per task.  A task is a row range of one
 // front block holding ~32 KB of factor data: [F_PP F_PU] rows are contiguous
-// in the row-major front, and F_UP rows are packed row-contiguous after each
-// factorisation (k_pack_up), so every task is one contiguous byte range that
+// in the row-major front, and F_UP rows are written row-contiguous by the
+// factorisation's F_UP GEMM (frontal.cu), so every task is one contiguous byte range that
 // thread 0 moves into shared memory with a single TMA bulk copy
 // (cp.async.bulk + mbarrier complete_tx) while the block gathers the task's
 // vector; the GEMV then runs out of shared memory.  Thread 0 also issues an
@@ -62,20 +62,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // -------------------------------------------------------------- kernels
-// F_UP rows (front rows np..m, columns 0..np) -> packed row-contiguous block
-__global__ void __launch_bounds__(256) k_pack_up(const int2* __restrict__ tasks, int64_t ntask,
-                                                 const NodeDev* __restrict__ nodes,
-                                                 double2* __restrict__ fronts) {
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= ntask) return;
-  const int2 tk = tasks[w];
-  const NodeDev nd = nodes[tk.x];
-  const double2* src = fronts + nd.front_off + (int64_t)(nd.np + tk.y) * nd.m;
-  double2* dst = fronts + nd.upk_off + (int64_t)tk.y * nd.np;
-  for (int q = lane; q < nd.np; q += 32) dst[q] = src[q];
-}
-
 // GEMV of R rows (row-major, row length len, in shared memory) with the
 // vector z (shared memory): a group of tpr threads per row, tpr chosen from
 // the row count so all 256 threads work; groups wider than a warp combine
@@ -250,12 +236,6 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
     CK(cudaFuncSetAttribute(k_solve_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
-}
-
-void FrontPlan::pack(cudaStream_t s) {
-  if (npack == 0) return;
-  k_pack_up<<<(unsigned)((npack + 7) / 8), 256, 0, s>>>(pack_tasks.p, npack, nodes.p, fronts.p);
-  CK_LAUNCH(ctx);
 }
 
 void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
