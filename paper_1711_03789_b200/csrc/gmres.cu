@@ -39,7 +39,7 @@ bool prec_is_distributed(const mdd_prec* P);
 mdd_comm* prec_comm(const mdd_prec* P);
 
 constexpr int kArnThreads = 256;
-constexpr int kMaxArnCTAs = 256;  // grid <= #SMs (148 on B200)
+constexpr int kMaxArnCTAs = 160;  // grid <= #SMs (148 on B200)
 
 struct ArnoldiArgs {
   int64_t n;
@@ -198,6 +198,28 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, doub
   dr = sh[67];
 }
 
+// Block sum of (a, b) delivered to thread 0 only (it publishes): one block
+// barrier.  `sh` is double-buffered by step parity: a buffer is rewritten two
+// steps later, after thread 0 has passed the next step's barrier.
+__device__ __forceinline__ void block_sum_t0(double2& a, double2& b, double2* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  a = warp_sum2(a);
+  b = warp_sum2(b);
+  if (lane == 0) {
+    sh[2 * wid] = a;
+    sh[2 * wid + 1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = sh[0];
+    b = sh[1];
+    for (int k = 1; k < nw; ++k) {
+      a = cadd(a, sh[2 * k]);
+      b = cadd(b, sh[2 * k + 1]);
+    }
+  }
+}
+
 __device__ __forceinline__ double2 cdotc_acc(double2 acc, double2 x, double2 y) {  // acc + conj(x) y
   acc.x += x.x * y.x + x.y * y.y;
   acc.y += x.x * y.y - x.y * y.x;
@@ -270,7 +292,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   constexpr bool REG = MODE == 1, STR = MODE == 2;
   extern __shared__ double2 col[];  // m+1, identical in every CTA
-  __shared__ double2 red[68 + 2 * kMaxArnCTAs];
+  __shared__ double2 red[68 + 2 * kMaxArnCTAs + 32];
   const int G = gridDim.x;
   const int m = *a.iter + 1;
   const int64_t n = a.n;
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         if (do_drift) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
-    block_sum2x2(acc, dacc, red);
+    block_sum_t0(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16);
     if (threadIdx.x == 0) publish(slots(0), G, acc, dacc);
     if constexpr (REG) {
       const double2* x1 = xvec(1);
@@ -414,7 +436,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         if (drift_next) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
-    block_sum2x2(acc, dacc, red);
+    block_sum_t0(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16 * (s & 1));
     if (threadIdx.x == 0) publish(slots(s + 1), G, acc, dacc);
     if constexpr (REG) {
       if (s + 2 < nsteps) {  // preload X_{s+2} while the other CTAs arrive
