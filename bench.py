@@ -39,6 +39,10 @@ CONFIGS = {
             rhs=("gauss", 100.0)),
     1: dict(name="cfg1", N=40, k=20.0, xi=20.0, p=4, layers=2, nc=10, family="as", corr="additive",
             rhs=("random", 0)),
+    # second-order Nedelec fine space (extension: the reference has Whitney elements only),
+    # lowest-order coarse space nested in its Whitney part; Gaussian source as cfg0
+    2: dict(name="cfg2", N=30, k=20.0, xi=20.0, p=3, layers=1, nc=8, family="as", corr="additive",
+            rhs=("gauss", 100.0), order=2),
     3: dict(name="cfg3", N=60, k=30.0, xi=math.sqrt(30.0), p=4, layers=2, nc=15, family="impras",
             corr="hybrid", rhs=("random", 0)),  # ImpHRAS: the paper's coarse combination for ImpRAS
     4: dict(name="cfg4", N=80, k=40.0, xi=0.0, p=8, layers=2, nc=20, family="as", corr="additive",
@@ -57,7 +61,7 @@ def build_problem(c, seed=0):
     from paper_1711_03789_b200 import decomp, fem, mesh
 
     m = mesh.build_cube_mesh(c["N"])
-    space = fem.build_edge_space(m, "pec")
+    space = fem.build_edge_space(m, "pec", order=c.get("order", 1))
     nt = m.n_tets
     if c.get("hetero"):
         # eps_r per 4x4x4 block ~ U[1,4]; absorption per block ~ U[k/2, 2k] carried by
@@ -77,7 +81,7 @@ def build_problem(c, seed=0):
         rhs = fem.assemble_rhs(space, fem.GaussianSource(alpha=c["rhs"][1], direction=(0.0, 0.0, 1.0)))
     coarse = fem.build_edge_space(mesh.build_cube_mesh(c["nc"]), "pec")
     t0 = time.perf_counter()
-    dec = decomp.build_decomposition(space, c["p"], c["layers"], coarse_space=coarse)
+    dec = decomp.build_decomposition(space, c["p"], c["layers"], coarse_space=coarse, allow_nonnested=True)
     t_dec = time.perf_counter() - t0
     return space, coeffs, np.ascontiguousarray(rhs), dec, t_dec
 
@@ -171,8 +175,14 @@ def cpu_sample(c, space, coeffs, rhs, dec, budget_s=12.0, workers=None):
     md = {k: getattr(space.mesh, k) for k in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs",
                                               "boundary_faces")}
     t0 = time.perf_counter()
-    sysm = O.assemble(md, space.edge_to_dof, space.ndof, coeffs.k, coeffs.xi, eps=coeffs.eps, mu=coeffs.mu,
-                      sigma=coeffs.sigma)
+    if getattr(space, "order", 1) == 2:
+        from oracle import nedelec2_oracle as O2
+
+        sysm = O2.assemble(space.mesh.vertices, space.mesh.tets, space.tet_dofs, space.ndof, coeffs.k, coeffs.xi,
+                           eps=coeffs.eps, mu=coeffs.mu, sigma=coeffs.sigma)
+    else:
+        sysm = O.assemble(md, space.edge_to_dof, space.ndof, coeffs.k, coeffs.xi, eps=coeffs.eps, mu=coeffs.mu,
+                          sigma=coeffs.sigma)
     t_asm = time.perf_counter() - t0
     A = sysm["A"]
     nsub = len(dec.dofs)

@@ -130,6 +130,22 @@ int mdd_assemble_rhs_gaussian(mdd_space* sp, const double* center, double alpha,
 int mdd_element_matrices(mdd_ctx* ctx, int64_t nt, const double* coords,
                          const double* signs, double* s_el, double* m_el, double* vol);
 
+/* Second-order Nedelec fine space (BASELINE.json config 2; no reference
+ * counterpart: the reference implements Whitney elements only, fem.py:1-7).
+ * 20 hierarchical basis functions per tet, defined with the tet's vertices
+ * sorted by global index: 6 Whitney, 6 edge gradients grad(l_a l_b), 8 face
+ * functions (l_c w_ab, l_a w_bc per face (a<b<c)); tet_dofs (nt,20) gives the
+ * global DoF of each (-1 = eliminated by PEC).  qbary (nq,4) / qweights (nq)
+ * are the load-vector quadrature (weights sum to 1).  mdd_assemble /
+ * mdd_assemble_rhs* accept the returned space (PEC only); for
+ * mdd_assemble_rhs the source values are laid out (nq, nt, 3). */
+int mdd_space2_create(mdd_ctx* ctx, int32_t cells_per_axis, int64_t nv, const double* vertices,
+                      int64_t nt, const int64_t* tets, const int64_t* tet_dofs, int64_t ndof,
+                      int32_t nq, const double* qbary, const double* qweights, mdd_space** out);
+/* 20x20 element matrices of the order-2 basis for tets given by coords (nt,4,3)
+ * (vertex order = basis frame). */
+int mdd_element2_matrices(mdd_ctx* ctx, int64_t nt, const double* coords, double* s_el, double* m_el);
+
 /* ------------------------------------------------------ preconditioner
  * precond.PreconditionerState.__init__ / setup (precond.py:280-323, 380-387)
  * and PreconditionerState.apply (precond.py:347-375).
@@ -151,9 +167,11 @@ typedef struct {
   const int64_t* sub_ptr;   /* nsub+1 offsets into sub_dofs                  */
   const int64_t* sub_dofs;  /* sorted global DOF sets I_l (decomp.py:140-191) */
   const double* sub_pou;    /* aligned weights (decomp.py:194-205) or NULL   */
-  const int32_t* dof_xyz;   /* (ndof,3) edge midpoints in half-cell units    */
+  const int32_t* dof_xyz;   /* (ndof,3) DoF positions in 1/dof_grid cell units */
   /* impras: local matrices assembled on the submesh (precond.py:212-269)    */
-  const mdd_space* space;   /* fine space (for impras local assembly)        */
+  const mdd_space* space;   /* fine lowest-order space (impras local assembly,
+                               coarse Galerkin; for an order-2 fine space its
+                               Whitney companion on the same mesh)            */
   const mdd_coeffs* prec_coeffs;
   const int64_t* sub_tet_ptr; /* nsub+1 offsets into sub_tets (impras)        */
   const int64_t* sub_tets;    /* per-subdomain tet lists (decomp.elements)    */
@@ -166,6 +184,8 @@ typedef struct {
   const int32_t* coarse_dof_xyz; /* (ncs,3) half-cell units of the coarse mesh */
   int64_t nbf_global;         /* global impedance faces (bc=impedance) or 0  */
   const int64_t* bfaces_global;
+  int32_t dof_grid;           /* dof_xyz units per mesh cell: 2 (edge midpoints,
+                                 0 = default) or 6 (order-2 edges and faces)  */
 } mdd_prec_desc;
 
 /* On MDD_ESINGULAR/MDD_ECAP, *failed_ctx is the subdomain id, or -1 for the

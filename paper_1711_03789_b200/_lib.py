@@ -64,6 +64,7 @@ class mdd_prec_desc(C.Structure):
         ("coarse_dof_xyz", C.POINTER(C.c_int32)),
         ("nbf_global", C.c_int64),
         ("bfaces_global", C.POINTER(C.c_int64)),
+        ("dof_grid", C.c_int32),
     ]
 
 
@@ -139,6 +140,11 @@ SIGNATURES = {
     "mdd_assemble_rhs": (C.c_int, [_P, _pz, _pz]),
     "mdd_assemble_rhs_gaussian": (C.c_int, [_P, _pd, C.c_double, C.c_double, _pd, _pz]),
     "mdd_element_matrices": (C.c_int, [_P, _i64, _pd, _pd, _pd, _pd, _pd]),
+    "mdd_space2_create": (
+        C.c_int,
+        [_P, _i32, _i64, _pd, _i64, _pi64, _pi64, _i64, _i32, _pd, _pd, _PP],
+    ),
+    "mdd_element2_matrices": (C.c_int, [_P, _i64, _pd, _pd, _pd]),
     "mdd_prec_create": (C.c_int, [_P, C.POINTER(mdd_prec_desc), _PP, _pi32]),
     "mdd_prec_variant": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _PP]),
     "mdd_prec_destroy": (None, [_P]),

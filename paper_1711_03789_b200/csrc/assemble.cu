@@ -185,9 +185,6 @@ __device__ __forceinline__ double qlam(int q, int i) {
 
 // contrib[(q*nt + t)*6 + e] = (w_e(x_q) . F_q) * s_e * |T|/4   (fem.py:382-389)
 // F from fvals (4,nt,3) or the device Gaussian when fvals == nullptr.
-struct GaussSrc {
-  double cx, cy, cz, alpha, amp, dx, dy, dz;
-};
 __global__ void k_rhs_contrib(int64_t nt, const double* __restrict__ verts,
                               const int32_t* __restrict__ tets, const int8_t* __restrict__ signs,
                               const double2* __restrict__ fvals, GaussSrc gs,
@@ -603,7 +600,13 @@ int mdd_assemble(mdd_space* sp, const mdd_coeffs* co, int impedance, int64_t nbf
                  const int64_t* bfaces, mdd_csr** A, mdd_csr** S, mdd_csr** M, mdd_csr** Dk,
                  mdd_csr** Mb) {
   MDD_API_BEGIN
-  assemble_system(sp, co, impedance, nbf, bfaces, A, S, M, Dk, Mb);
+  if (sp->order == 2) {
+    if (impedance) fail(MDD_EINVAL, "order-2 spaces support the PEC boundary only");
+    if (Mb) *Mb = nullptr;
+    assemble_system2(sp, co, A, S, M, Dk);
+  } else {
+    assemble_system(sp, co, impedance, nbf, bfaces, A, S, M, Dk, Mb);
+  }
   MDD_API_END
 }
 
@@ -612,7 +615,8 @@ int mdd_assemble_rhs(mdd_space* sp, const mdd_complex* fvals, mdd_complex* rhs) 
   mdd_ctx* ctx = sp->ctx;
   CK(cudaSetDevice(ctx->device));
   DevBuf<double2> r(sp->ndof);
-  assemble_rhs_dev(sp, reinterpret_cast<const double2*>(fvals), nullptr, r.p);
+  if (sp->order == 2) assemble_rhs2_dev(sp, reinterpret_cast<const double2*>(fvals), nullptr, r.p);
+  else assemble_rhs_dev(sp, reinterpret_cast<const double2*>(fvals), nullptr, r.p);
   r.download(reinterpret_cast<double2*>(rhs), sp->ndof, ctx->stream);
   CK(cudaStreamSynchronize(ctx->stream));
   MDD_API_END
@@ -625,7 +629,8 @@ int mdd_assemble_rhs_gaussian(mdd_space* sp, const double* center, double alpha,
   CK(cudaSetDevice(ctx->device));
   GaussSrc g{center[0], center[1], center[2], alpha, amp, dir[0], dir[1], dir[2]};
   DevBuf<double2> r(sp->ndof);
-  assemble_rhs_dev(sp, nullptr, &g, r.p);
+  if (sp->order == 2) assemble_rhs2_dev(sp, nullptr, &g, r.p);
+  else assemble_rhs_dev(sp, nullptr, &g, r.p);
   r.download(reinterpret_cast<double2*>(rhs), sp->ndof, ctx->stream);
   CK(cudaStreamSynchronize(ctx->stream));
   MDD_API_END

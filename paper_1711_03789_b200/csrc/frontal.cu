@@ -458,6 +458,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     in.rowptr = mats[i].rowptr.data();
     in.cols = mats[i].cols.data();
     in.xyz = mats[i].xyz.data();
+    in.grid = mats[i].grid;
     nd_analyze(in, leaf, sym[i]);
   });
   mat_n.resize(nmat);

@@ -69,6 +69,7 @@ struct MatrixInput {
   std::vector<int32_t> rowptr, cols;  // local pattern (sorted)
   std::vector<int32_t> src;           // per local entry: index into the value array
   std::vector<int32_t> xyz;           // (n,3)
+  int32_t grid = 2;                   // xyz units per mesh cell
 };
 
 struct FrontPlan {

@@ -170,8 +170,16 @@ struct mdd_space {
   // colour share an edge, so one thread per cell scatters without atomics
   mdd::DevBuf<int32_t> cells_by_color;
   int64_t color_off[9] = {0};
-  // dof -> incident (tet*6 + local edge), ascending tet (rhs gather)
+  // dof -> incident (tet*6 + local edge), ascending tet (rhs gather);
+  // order 2: (tet*20 + local dof)
   mdd::DevBuf<int32_t> inc_ptr, inc;
+  // order-2 spaces (nedelec2.cu): tets hold vertices sorted by global index,
+  // tdofs (nt*20) the global DoF of each local basis function (-1: eliminated),
+  // and the load-vector quadrature (nq barycentric points + weights)
+  int32_t order = 1;
+  mdd::DevBuf<int32_t> tdofs;
+  int32_t nq = 0;
+  mdd::DevBuf<double> qbary, qw;
 };
 
 // NCCL communicator (comm.cu); `comm` is an ncclComm_t (NCCL is dlopen'ed)
@@ -211,6 +219,16 @@ void vec_sub(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int
              cudaStream_t s);
 void vec_add(mdd_ctx* ctx, const double2* a, const double2* b, double2* out, int64_t n,
              cudaStream_t s);
+// assembly shared by the order-1 (assemble.cu) and order-2 (nedelec2.cu) spaces
+struct GaussSrc {
+  double cx, cy, cz, alpha, amp, dx, dy, dz;
+};
+__global__ void k_combine(int64_t nnz, const double* __restrict__ S, const double* __restrict__ M,
+                          double2* __restrict__ A, double* __restrict__ Dk, double k2, double xi,
+                          int write_a);
+void assemble_system2(mdd_space* sp, const mdd_coeffs* co, mdd_csr** A, mdd_csr** S, mdd_csr** M,
+                      mdd_csr** Dk);
+void assemble_rhs2_dev(mdd_space* sp, const double2* fvals_host, const GaussSrc* gsrc, double2* rhs_dev);
 // complex CSR with the given pattern, values zeroed
 mdd_csr* new_csr(mdd_ctx* ctx, std::shared_ptr<mdd_pattern> pat, bool cplx);
 std::shared_ptr<mdd_pattern> make_pattern(int64_t nrow, int64_t ncol,

@@ -45,6 +45,11 @@ struct PrecCore {
   FrontPlan coarse;
   std::unique_ptr<mdd_csr> R0p, R0Tp;  // rows / columns in coarse ND order
   std::unique_ptr<mdd_csr> A0;         // assembled coarse Galerkin matrix (coarse pattern)
+  // non-nested coarse mesh: A0[slot] = sum_t rap_c[t] * A_prec[rap_k[t]], t in [rap_ptr[slot], rap_ptr[slot+1])
+  bool rap = false;
+  DevBuf<int64_t> rap_ptr;
+  DevBuf<int32_t> rap_k;
+  DevBuf<double> rap_c;
   // Galerkin data
   const mdd_space* fine_space = nullptr;
   const mdd_space* coarse_space = nullptr;
@@ -561,6 +566,120 @@ static void impras_local_assemble(PrecCore& c, const mdd_coeffs* co, cudaStream_
   }
 }
 
+// Generic Galerkin product for a coarse mesh that does not nest in the fine
+// one (tet_map == NULL; extension, BASELINE config 2): A0 = R0 A_prec R0^T
+// with R0 given entry by entry (decomp.coarse_restriction_nonnested).  The
+// symbolic phase (host, once) lists for every A0 slot (p,q) its terms
+// R0[p,i] R0[q,j] * A_prec[i,j] as (A entry index, coefficient), in a fixed
+// order; the numeric phase (k_rap, one warp per slot) is a deterministic
+// gather-reduce over the current A_prec values.  This is exact: no element
+// integration, so it holds for any operator on the fine space.
+static void build_rap(PrecCore& c, const mdd_csr& R0, const mdd_pattern& AP, cudaStream_t s) {
+  const mdd_pattern& RP = *R0.pat;
+  const int64_t ncs = RP.nrow, ndof = RP.ncol;
+  std::vector<double> rv(RP.nnz);
+  R0.vals.download(rv.data(), RP.nnz, s);
+  CK(cudaStreamSynchronize(s));
+  // R0^T rows: fine dof -> (coarse row, value), ascending coarse row
+  std::vector<int32_t> tp(ndof + 1, 0), tc(RP.nnz);
+  std::vector<double> tv(RP.nnz);
+  for (int64_t k = 0; k < RP.nnz; ++k) tp[RP.h_cols[k] + 1]++;
+  for (int64_t i = 0; i < ndof; ++i) tp[i + 1] += tp[i];
+  {
+    std::vector<int32_t> fp(tp.begin(), tp.end() - 1);
+    for (int64_t r = 0; r < ncs; ++r)
+      for (int32_t k = RP.h_rowptr[r]; k < RP.h_rowptr[r + 1]; ++k) {
+        const int32_t pos = fp[RP.h_cols[k]]++;
+        tc[pos] = (int32_t)r;
+        tv[pos] = rv[k];
+      }
+  }
+  struct Term {
+    int32_t q, k;
+    double c;
+  };
+  std::vector<std::vector<int32_t>> rq(ncs);
+  std::vector<std::vector<int64_t>> rcnt(ncs);
+  std::vector<std::vector<int32_t>> rk(ncs);
+  std::vector<std::vector<double>> rc(ncs);
+  const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::atomic<int64_t> next{0};
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nth; ++t)
+    th.emplace_back([&] {
+      std::vector<Term> terms;
+      for (int64_t p = next++; p < ncs; p = next++) {
+        terms.clear();
+        for (int32_t e = RP.h_rowptr[p]; e < RP.h_rowptr[p + 1]; ++e) {
+          const int32_t i = RP.h_cols[e];
+          const double rpi = rv[e];
+          for (int32_t kk = AP.h_rowptr[i]; kk < AP.h_rowptr[i + 1]; ++kk) {
+            const int32_t j = AP.h_cols[kk];
+            for (int32_t u = tp[j]; u < tp[j + 1]; ++u) terms.push_back({tc[u], kk, rpi * tv[u]});
+          }
+        }
+        std::stable_sort(terms.begin(), terms.end(), [](const Term& a, const Term& b) { return a.q < b.q; });
+        for (size_t a = 0; a < terms.size(); ++a) {
+          if (a == 0 || terms[a].q != terms[a - 1].q) {
+            rq[p].push_back(terms[a].q);
+            rcnt[p].push_back(0);
+          }
+          rcnt[p].back()++;
+          rk[p].push_back(terms[a].k);
+          rc[p].push_back(terms[a].c);
+        }
+      }
+    });
+  for (auto& x : th) x.join();
+  std::vector<int32_t> rowptr(ncs + 1, 0), cols;
+  std::vector<int64_t> tptr(1, 0);
+  std::vector<int32_t> hk;
+  std::vector<double> hc;
+  for (int64_t p = 0; p < ncs; ++p) {
+    if ((int64_t)rowptr[p] + (int64_t)rq[p].size() > INT32_MAX) fail(MDD_EINVAL, "coarse: nnz > 2^31");
+    rowptr[p + 1] = rowptr[p] + (int32_t)rq[p].size();
+    cols.insert(cols.end(), rq[p].begin(), rq[p].end());
+    for (int64_t n : rcnt[p]) tptr.push_back(tptr.back() + n);
+    hk.insert(hk.end(), rk[p].begin(), rk[p].end());
+    hc.insert(hc.end(), rc[p].begin(), rc[p].end());
+    std::vector<int32_t>().swap(rk[p]);
+    std::vector<double>().swap(rc[p]);
+  }
+  auto pat = make_pattern(ncs, ncs, std::move(rowptr), std::move(cols), s);
+  c.A0.reset(new_csr(c.ctx, pat, true));
+  c.rap_ptr.upload(tptr, s);
+  c.rap_k.upload(hk, s);
+  c.rap_c.upload(hc, s);
+  c.rap = true;
+  CK(cudaStreamSynchronize(s));
+}
+
+__global__ void __launch_bounds__(256) k_rap(int64_t nslot, const int64_t* __restrict__ ptr,
+                                             const int32_t* __restrict__ kidx, const double* __restrict__ coef,
+                                             const double2* __restrict__ A, double2* __restrict__ A0) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nslot) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t t = ptr[w] + lane; t < ptr[w + 1]; t += 32) {
+    const double cf = __ldg(coef + t);
+    const double2 a = __ldg(A + __ldg(kidx + t));
+    acc.x += cf * a.x;
+    acc.y += cf * a.y;
+  }
+  acc = warp_sum2(acc);
+  if (lane == 0) A0[w] = acc;
+}
+
+static void rap_assemble(PrecCore& c, const mdd_csr* A_prec, cudaStream_t s) {
+  const int64_t nslot = c.A0->pat->nnz;
+  if (!nslot) return;
+  k_rap<<<nb(nslot * 32, 256), 256, 0, s>>>(nslot, c.rap_ptr.p, c.rap_k.p, c.rap_c.p,
+                                            reinterpret_cast<const double2*>(A_prec->vals.p),
+                                            reinterpret_cast<double2*>(c.A0->vals.p));
+  CK_LAUNCH(c.ctx);
+}
+
 static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc,
                           int32_t* failed_ctx) {
   PrecCore& c = *P->core;
@@ -577,7 +696,8 @@ static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* 
     c.sub.factor(c.loc_vals.p, s);
   }
   if (c.have_coarse) {
-    galerkin_assemble(c, pc, s);
+    if (c.rap) rap_assemble(c, A_prec, s);
+    else galerkin_assemble(c, pc, s);
     c.coarse.factor(reinterpret_cast<const double2*>(c.A0->vals.p), s);
   }
   CK(cudaEventRecord(e1, s));
@@ -650,6 +770,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
           mi.n = (int32_t)(e - b);
           for (int64_t i = b; i < e; ++i) g2l[d->sub_dofs[i]] = (int32_t)(i - b);
           mi.rowptr.assign(1, 0);
+          mi.grid = d->dof_grid > 0 ? d->dof_grid : 2;
           mi.xyz.resize(3 * (size_t)mi.n);
           for (int64_t i = b; i < e; ++i) {
             const int64_t g = d->sub_dofs[i];
@@ -834,7 +955,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
   }
   // ---- coarse level
   if (d->levels == 2) {
-    if (!d->R0 || !d->coarse_space || !d->tet_map || !d->coarse_dof_xyz)
+    if (!d->R0 || !d->coarse_space || !d->coarse_dof_xyz)
       fail(MDD_EINVAL, "two-level preconditioner needs a coarse link");
     c.have_coarse = true;
     const mdd_space* cs = d->coarse_space;
@@ -847,11 +968,15 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
                          " exceeds cap " + std::to_string(d->lu_cap) +
                          "; raise the cap or shrink the block", -1);
     }
-    c.A0.reset(new_csr(ctx, cs->pat, true));
     std::vector<MatrixInput> cm(1);
     cm[0].n = (int32_t)c.ncs;
-    cm[0].rowptr = cs->pat->h_rowptr;
-    cm[0].cols = cs->pat->h_cols;
+    if (d->tet_map) {  // nested meshes: element-wise Galerkin on the coarse mesh pattern
+      c.A0.reset(new_csr(ctx, cs->pat, true));
+    } else {           // non-nested: generic R0 A_prec R0^T plan (pattern of the product)
+      build_rap(c, *d->R0, AP, s);
+    }
+    cm[0].rowptr = c.A0->pat->h_rowptr;
+    cm[0].cols = c.A0->pat->h_cols;
     cm[0].src.resize(cm[0].cols.size());
     std::iota(cm[0].src.begin(), cm[0].src.end(), 0);
     cm[0].xyz.assign(d->coarse_dof_xyz, d->coarse_dof_xyz + 3 * c.ncs);
@@ -891,6 +1016,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
     c.R0Tp = csr_host(ctx, ndof, c.ncs, std::move(tp), std::move(tc), tv);
     // Galerkin index data: fine tets per coarse tet (ascending)
     const mdd_space* fs = d->space;
+    if (c.rap) goto coarse_done;
     if (!fs) fail(MDD_EINVAL, "two-level preconditioner needs the fine space");
     std::vector<int32_t> tm(fs->nt);
     for (int64_t t = 0; t < fs->nt; ++t) {
@@ -942,6 +1068,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
       c.cface_idx.upload(gidx2, s);
     }
   }
+coarse_done:
   CK(cudaStreamCreateWithFlags(&c.s2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));

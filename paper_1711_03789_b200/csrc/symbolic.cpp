@@ -3,8 +3,9 @@
 // Replaces nothing in the reference directly: the reference factors each
 // subdomain block densely (linalg.DenseLU, linalg.py:73-101, via
 // precond.py:296-313).  The DOFs of an edge space carry integer midpoint
-// coordinates in half-cell units; a grid plane x_axis = c (c even) contains
-// exactly the edges lying in that vertex plane, and because every
+// coordinates in half-cell units (order 2: sixth-cell units for edge
+// midpoints and face centroids, SymIn::grid); a vertex plane x_axis = c (c a
+// multiple of the grid unit) contains exactly the edges (faces) lying in it, and because every
 // tetrahedron lies inside one cell, no matrix entry couples an edge with
 // coordinate < c to one with coordinate > c.  Recursive bisection along the
 // longest axis therefore yields an exact nested-dissection tree whose
@@ -74,9 +75,12 @@ struct Builder {
       for (int32_t v : set) vals.push_back(in.xyz[3 * v + a]);
       std::nth_element(vals.begin(), vals.begin() + vals.size() / 2, vals.end());
       const int32_t med = vals[vals.size() / 2];
+      // vertex planes lie at multiples of the grid unit
+      const int32_t g = in.grid > 0 ? in.grid : 2;
+      const int32_t fl = (med >= 0 ? med / g : -((-med + g - 1) / g)) * g;
       int32_t cands[2];
-      if (med % 2 == 0) { cands[0] = med; cands[1] = med; }
-      else { cands[0] = med - 1; cands[1] = med + 1; }
+      if (fl == med) { cands[0] = med; cands[1] = med; }
+      else { cands[0] = fl; cands[1] = fl + g; }
       int64_t best_imb = INT64_MAX;
       for (int32_t c : cands) {
         if (c <= lo[a] || c >= hi[a]) continue;

@@ -10,7 +10,8 @@ struct SymIn {
   int32_t n = 0;
   const int32_t* rowptr = nullptr;  // local pattern (sorted, structurally symmetric)
   const int32_t* cols = nullptr;
-  const int32_t* xyz = nullptr;     // (n,3) DOF coordinates in half-cell units
+  const int32_t* xyz = nullptr;     // (n,3) DOF coordinates in 1/grid cell units
+  int32_t grid = 2;                 // coordinate units per mesh cell (vertex planes at multiples)
 };
 
 struct SymNode {

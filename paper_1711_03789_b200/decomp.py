@@ -145,6 +145,8 @@ def subdomain_boundary_faces(mesh: Mesh, elems: np.ndarray) -> np.ndarray:
 
 def subdomain_dof_sets(space: EdgeSpace, elements: list) -> list:
     """Unknowns with zero trace on internal boundaries (reference decomp.py:140-176)."""
+    if getattr(space, "order", 1) == 2:
+        return _subdomain_dof_sets2(space, elements)
     mesh = space.mesh
     nv = np.int64(mesh.n_vertices)
     dom_keys = np.sort(_face_keys(mesh.boundary_faces, nv))
@@ -160,6 +162,34 @@ def subdomain_dof_sets(space: EdgeSpace, elements: list) -> list:
             member = member[~np.isin(member, excl)]
         d = space.edge_to_dof[member]
         out.append(np.sort(d[d >= 0]))
+    return out
+
+
+def _subdomain_dof_sets2(space, elements: list) -> list:
+    """Order-2 restatement of the rule above (extension, BASELINE config 2):
+    drop the edge DoFs of edges on internal subdomain-boundary faces and the
+    face DoFs of those faces; keep everything else the subdomain tets touch."""
+    mesh = space.mesh
+    nv = np.int64(mesh.n_vertices)
+    dom_keys = np.sort(_face_keys(mesh.boundary_faces, nv))
+    ekeys = mesh.edges[:, 0].astype(np.int64) * nv + mesh.edges[:, 1]
+    fkeys = _face_keys(space.faces, nv)  # ascending (np.unique order)
+    ned, nfd = space.n_edge_dofs, space.n_face_dofs
+    out = []
+    for elems in elements:
+        bf = subdomain_boundary_faces(mesh, elems)
+        internal = bf[~np.isin(_face_keys(bf, nv), dom_keys)]
+        medges = np.unique(mesh.tet_edges[elems].ravel())
+        mfaces = np.unique(space.tet_faces[elems].ravel())
+        if len(internal):
+            pairs = internal[:, [[0, 1], [0, 2], [1, 2]]].reshape(-1, 2)
+            medges = medges[~np.isin(medges, np.searchsorted(ekeys, pairs[:, 0] * nv + pairs[:, 1]))]
+            mfaces = mfaces[~np.isin(mfaces, np.searchsorted(fkeys, _face_keys(internal, nv)))]
+        ed = space.edge_to_dof[medges]
+        ed = ed[ed >= 0]
+        fd = space.face_to_dof[mfaces]
+        fd = fd[fd >= 0]
+        out.append(np.sort(np.concatenate([ed, ed + ned, fd + 2 * ned, fd + 2 * ned + nfd])))
     return out
 
 
@@ -246,18 +276,106 @@ def coarse_restriction(
     return r0
 
 
+_KUHN_ORDERS = {p: i for i, p in enumerate(__import__("itertools").permutations((0, 1, 2)))}
+
+
+def coarse_restriction_nonnested(fine_space: EdgeSpace, coarse_space: EdgeSpace) -> sp.csr_matrix:
+    """R0 for a coarse Kuhn mesh that does not nest in the fine one (extension:
+    the reference requires nesting, mesh.py:231-242; BASELINE config 2 pairs a
+    fine N=30 with a coarse N=8 mesh; the paper's non-nested setting, §6.2).
+
+    Entry (p, j) is still the line integral of coarse basis p along fine edge j
+    (reference decomp.py:212-297), now over a fine edge that may cross coarse
+    tets.  The edge is split at every coarse cell plane (nc x_a integer) and
+    every Kuhn diagonal plane (nc (x_a - x_b) integer), found exactly in integer
+    lattice arithmetic; on each piece the coarse Whitney function is affine, so
+    the midpoint rule is exact.  Pieces of one edge are summed.  A piece lying
+    on a coarse face may be attributed to either neighbour: the tangential
+    trace along it is continuous.
+    """
+    fine, coarse = fine_space.mesh, coarse_space.mesh
+    nf, nc = fine.cells_per_axis, coarse.cells_per_axis
+    kept = fine_space.kept_edges
+    lat = fine.lattice()
+    L0 = lat[fine.edges[kept, 0]]
+    L1 = lat[fine.edges[kept, 1]]
+    dirs = np.array([[1, 0, 0], [0, 1, 0], [0, 0, 1], [1, -1, 0], [0, 1, -1], [1, 0, -1]], dtype=np.int64)
+    F0 = nc * (L0 @ dirs.T)  # nc * x . dir, in units of 1/nf (exact integers)
+    F1 = nc * (L1 @ dirs.T)
+    lo, hi = np.minimum(F0, F1), np.maximum(F0, F1)
+    kmin = lo // nf + 1  # smallest integer k with k*nf > lo
+    K = int(max(1, ((hi - 1) // nf - kmin + 1).max(initial=0)))
+    ss = [np.zeros((len(kept), 1)), np.ones((len(kept), 1))]
+    for r in range(K):
+        k = (kmin + r) * nf
+        ok = (k > lo) & (k < hi)
+        den = np.where(F1 != F0, F1 - F0, 1)
+        ss.append(np.where(ok, (k - F0) / den, 1.0))
+    s = np.sort(np.concatenate(ss, axis=1), axis=1)  # (ne, npts)
+    sa, sb = s[:, :-1], s[:, 1:]
+    ln = sb - sa
+    e_idx, piece = np.nonzero(ln > 0)
+    mid = 0.5 * (sa[e_idx, piece] + sb[e_idx, piece])
+    x0 = fine.vertices[fine.edges[kept[e_idx], 0]]
+    d = fine.vertices[fine.edges[kept[e_idx], 1]] - x0
+    xm = x0 + mid[:, None] * d
+    u = xm * nc
+    cell = np.clip(np.floor(u).astype(np.int64), 0, nc - 1)
+    loc = u - cell
+    order = np.argsort(-loc, axis=1, kind="stable")
+    perm = np.array([_KUHN_ORDERS[tuple(o)] for o in map(tuple, order)]) if len(order) else np.zeros(0, int)
+    ct = ((cell[:, 0] * nc + cell[:, 1]) * nc + cell[:, 2]) * 6 + perm
+    cc = coarse.tet_coords()
+    binv = np.linalg.inv(np.transpose(cc[:, 1:] - cc[:, :1], (0, 2, 1)))
+    lam = np.einsum("pij,pj->pi", binv[ct], xm - cc[ct, 0])
+    lam = np.concatenate([1.0 - lam.sum(axis=1, keepdims=True), lam], axis=1)
+    g = np.empty((len(ct), 4, 3))
+    g[:, 1:] = binv[ct]
+    g[:, 0] = -binv[ct].sum(axis=1)
+    a, b = LOCAL_EDGES[:, 0], LOCAL_EDGES[:, 1]
+    w = lam[:, a, None] * g[:, b] - lam[:, b, None] * g[:, a]  # (npc, 6, 3)
+    vals = np.einsum("pec,pc->pe", w, d) * ln[e_idx, piece][:, None] * coarse.tet_edge_signs[ct]
+    rows = coarse_space.edge_to_dof[coarse.tet_edges[ct]].ravel()
+    cols = np.repeat(fine_space.edge_to_dof[kept[e_idx]], 6)
+    v = vals.ravel()
+    ok = rows >= 0
+    r0 = sp.csr_matrix((v[ok], (rows[ok], cols[ok])), shape=(coarse_space.ndof, fine_space.ndof))
+    r0.sum_duplicates()
+    r0.eliminate_zeros()
+    r0.sort_indices()
+    return r0
+
+
 def build_decomposition(
-    space: EdgeSpace, p_axis: int, layers: int, coarse_space: EdgeSpace | None = None
+    space: EdgeSpace, p_axis: int, layers: int, coarse_space: EdgeSpace | None = None,
+    allow_nonnested: bool = False,
 ) -> Decomposition:
-    """Box partition + overlap + DOF sets + PoU (+ coarse link) (reference decomp.py:304-332)."""
+    """Box partition + overlap + DOF sets + PoU (+ coarse link) (reference decomp.py:304-332).
+
+    ``allow_nonnested`` (extension): a coarse mesh whose resolution does not
+    divide the fine one gets the split-edge R0 of
+    :func:`coarse_restriction_nonnested` and ``tet_map=None`` (the reference,
+    and the default here, raise ``MeshError`` from the nesting check)."""
     mesh = space.mesh
     elements = extend_overlap(mesh, box_partition(mesh, p_axis), layers)
     dofs = subdomain_dof_sets(space, elements)
     pou = build_pou(dofs, space.ndof)
     coarse = None
-    if coarse_space is not None:
+    if coarse_space is not None and allow_nonnested and mesh.cells_per_axis % coarse_space.mesh.cells_per_axis:
+        p1 = space.lowest_order() if getattr(space, "order", 1) == 2 else space
+        r1 = coarse_restriction_nonnested(p1, coarse_space)
+        r0 = sp.csr_matrix((r1.data, r1.indices, r1.indptr), shape=(coarse_space.ndof, space.ndof))
+        coarse = CoarseLink(space=coarse_space, R0=r0, tet_map=None)
+    elif coarse_space is not None:
         tmap = nesting_map(coarse_space.mesh, mesh)
-        coarse = CoarseLink(space=coarse_space, R0=coarse_restriction(space, coarse_space, tmap), tet_map=tmap)
+        if getattr(space, "order", 1) == 2:
+            # the lowest-order coarse space is nested in the Whitney part of the
+            # order-2 space (first n_edge_dofs unknowns): R0 = [R0_1 | 0]
+            r1 = coarse_restriction(space.lowest_order(), coarse_space, tmap)
+            r0 = sp.csr_matrix((r1.data, r1.indices, r1.indptr), shape=(coarse_space.ndof, space.ndof))
+        else:
+            r0 = coarse_restriction(space, coarse_space, tmap)
+        coarse = CoarseLink(space=coarse_space, R0=r0, tet_map=tmap)
     return Decomposition(
         space=space,
         elements=elements,

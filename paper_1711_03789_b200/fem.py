@@ -25,13 +25,14 @@ import numpy as np
 
 from . import _lib
 from .linalg import DeviceCSR, raise_for
-from .mesh import LOCAL_EDGES, Mesh
+from .mesh import LOCAL_EDGES, LOCAL_FACES, Mesh
 
 __all__ = [
     "Coefficients",
     "EdgeSpace",
     "FemError",
     "GaussianSource",
+    "NedelecSpace2",
     "SystemBundle",
     "assemble",
     "assemble_boundary_mass",
@@ -126,14 +127,211 @@ class DeviceSpace:
             self.handle = None
 
 
-def build_edge_space(mesh: Mesh, bc: str = "pec") -> EdgeSpace:
-    """Reference fem.py:71-80: PEC drops boundary edges, impedance keeps all."""
+def build_edge_space(mesh: Mesh, bc: str = "pec", order: int = 1):
+    """Reference fem.py:71-80: PEC drops boundary edges, impedance keeps all.
+
+    ``order=2`` (extension, BASELINE config 2; the reference has Whitney
+    elements only) returns a :class:`NedelecSpace2`.
+    """
     if bc not in ("pec", "impedance"):
         raise FemError(f"unknown boundary condition {bc!r}")
+    if order == 2:
+        return build_nedelec2_space(mesh, bc)
+    if order != 1:
+        raise FemError(f"order must be 1 or 2, got {order!r}")
     kept = np.flatnonzero(~mesh.boundary_edge_flags) if bc == "pec" else np.arange(mesh.n_edges)
     e2d = np.full(mesh.n_edges, -1, dtype=np.int64)
     e2d[kept] = np.arange(len(kept))
     return EdgeSpace(mesh=mesh, bc_kind=bc, kept_edges=kept, edge_to_dof=e2d)
+
+
+# ------------------------------------------------- second-order space
+def stroud_rule(n: int = 3):
+    """Conical-product (Stroud) rule on the tetrahedron: n^3 points, exact for
+    degree 2n-1.  Returns barycentric points (n^3, 4) and weights summing to 1."""
+    from scipy.special import roots_jacobi
+
+    def gj(alpha):
+        x, w = roots_jacobi(n, alpha, 0.0)  # weight (1-x)^alpha on [-1,1]
+        return (1.0 + x) / 2.0, w / w.sum()
+
+    u, wu = gj(2.0)
+    v, wv = gj(1.0)
+    t, wt = gj(0.0)
+    pts, wts = [], []
+    for i in range(n):
+        for j in range(n):
+            for k in range(n):
+                x = u[i]
+                y = v[j] * (1.0 - u[i])
+                z = t[k] * (1.0 - u[i]) * (1.0 - v[j])
+                pts.append((1.0 - x - y - z, x, y, z))
+                wts.append(wu[i] * wv[j] * wt[k])
+    return np.array(pts), np.array(wts)
+
+
+@dataclass(frozen=True)
+class NedelecSpace2:
+    """Second-order Nedelec (first kind) space: 2 DoFs per edge, 2 per face.
+
+    Extension for BASELINE config 2 (the reference implements Whitney elements
+    only, reference fem.py:1-7).  Hierarchical basis in the frame
+    of each tet's vertices sorted by global index (csrc/nedelec2.cu): Whitney
+    w_ab, edge gradients grad(l_a l_b), face functions l_c w_ab and l_a w_bc.
+    Global numbering: [Whitney DoFs in the lowest-order numbering | edge
+    gradient DoFs | first face DoFs | second face DoFs], so the lowest-order
+    space (and the lowest-order coarse space nested in it) sits on the first
+    ``n_edge_dofs`` unknowns.
+    """
+
+    mesh: Mesh
+    bc_kind: str
+    kept_edges: np.ndarray
+    edge_to_dof: np.ndarray
+    faces: np.ndarray          # (nf, 3) sorted vertex triples
+    tet_faces: np.ndarray      # (nt, 4) face ids in LOCAL_FACES order
+    kept_faces: np.ndarray
+    face_to_dof: np.ndarray    # index among kept faces, -1 if eliminated
+    tet_dofs: np.ndarray       # (nt, 20) sorted-frame local -> global DoF (-1: eliminated)
+    _cache: dict = field(default_factory=dict, compare=False, repr=False)
+
+    order = 2
+
+    @property
+    def n_edge_dofs(self) -> int:
+        return int(len(self.kept_edges))
+
+    @property
+    def n_face_dofs(self) -> int:
+        return int(len(self.kept_faces))
+
+    @property
+    def ndof(self) -> int:
+        return 2 * self.n_edge_dofs + 2 * self.n_face_dofs
+
+    def lowest_order(self) -> EdgeSpace:
+        """The Whitney space on the same mesh and boundary condition."""
+        e = self._cache.get("p1")
+        if e is None:
+            e = EdgeSpace(mesh=self.mesh, bc_kind=self.bc_kind, kept_edges=self.kept_edges,
+                          edge_to_dof=self.edge_to_dof)
+            self._cache["p1"] = e
+        return e
+
+    def dof_coords(self) -> np.ndarray:
+        """(ndof, 3) int32 DoF positions in sixth-cell units (edge midpoints,
+        face centroids): vertex planes sit at multiples of 6 (ND separators)."""
+        c = self._cache.get("xyz6")
+        if c is None:
+            lat = self.mesh.lattice()
+            e = self.mesh.edges[self.kept_edges]
+            ec = 3 * (lat[e[:, 0]] + lat[e[:, 1]])
+            f = self.faces[self.kept_faces]
+            fc = 2 * (lat[f[:, 0]] + lat[f[:, 1]] + lat[f[:, 2]])
+            c = np.ascontiguousarray(np.concatenate([ec, ec, fc, fc]), dtype=np.int32)
+            self._cache["xyz6"] = c
+        return c
+
+    def device(self) -> "DeviceSpace2":
+        d = self._cache.get("dev")
+        if d is None:
+            d = DeviceSpace2(self)
+            self._cache["dev"] = d
+        return d
+
+
+def build_nedelec2_space(mesh: Mesh, bc: str = "pec") -> NedelecSpace2:
+    """Order-2 DoF map: PEC drops the DoFs of boundary edges and boundary faces."""
+    if bc != "pec":
+        raise FemError("order-2 spaces support bc='pec' only")
+    p1 = build_edge_space(mesh, bc)
+    nv = np.int64(mesh.n_vertices)
+    tri = np.sort(mesh.tets[:, LOCAL_FACES], axis=2)  # (nt, 4, 3)
+    fkeys = (tri[..., 0] * nv + tri[..., 1]) * nv + tri[..., 2]
+    ukeys, tet_faces, cnt = np.unique(fkeys.ravel(), return_inverse=True, return_counts=True)
+    tet_faces = tet_faces.reshape(-1, 4).astype(np.int64)
+    faces = np.stack([ukeys // (nv * nv), (ukeys // nv) % nv, ukeys % nv], axis=1)
+    kept_faces = np.flatnonzero(cnt == 2)
+    f2d = np.full(len(faces), -1, dtype=np.int64)
+    f2d[kept_faces] = np.arange(len(kept_faces))
+    # sorted-frame local DoFs (csrc/nedelec2.cu): edges / faces of the sorted tet
+    st = np.sort(mesh.tets, axis=1)
+    ekeys = mesh.edges[:, 0] * nv + mesh.edges[:, 1]  # ascending
+    a, b = LOCAL_EDGES[:, 0], LOCAL_EDGES[:, 1]
+    eid = np.searchsorted(ekeys, st[:, a] * nv + st[:, b])  # (nt, 6)
+    fa, fb, fc = LOCAL_FACES[:, 0], LOCAL_FACES[:, 1], LOCAL_FACES[:, 2]
+    fid = np.searchsorted(ukeys, (st[:, fa] * nv + st[:, fb]) * nv + st[:, fc])  # (nt, 4)
+    ned, nfd = len(p1.kept_edges), len(kept_faces)
+    ed = p1.edge_to_dof[eid]
+    fd = f2d[fid]
+    td = np.empty((mesh.n_tets, 20), dtype=np.int64)
+    td[:, 0:6] = ed
+    td[:, 6:12] = np.where(ed >= 0, ed + ned, -1)
+    td[:, 12:20:2] = np.where(fd >= 0, fd + 2 * ned, -1)
+    td[:, 13:20:2] = np.where(fd >= 0, fd + 2 * ned + nfd, -1)
+    return NedelecSpace2(mesh=mesh, bc_kind=bc, kept_edges=p1.kept_edges, edge_to_dof=p1.edge_to_dof,
+                         faces=faces, tet_faces=tet_faces, kept_faces=kept_faces, face_to_dof=f2d,
+                         tet_dofs=td)
+
+
+_STROUD = None
+
+
+def _rule():
+    global _STROUD
+    if _STROUD is None:
+        _STROUD = stroud_rule(3)
+    return _STROUD
+
+
+class DeviceSpace2:
+    """Owner of the ``mdd_space`` handle of a :class:`NedelecSpace2`."""
+
+    def __init__(self, space: NedelecSpace2):
+        ctx = _lib.get_context()
+        m = space.mesh
+        self.ctx = ctx
+        qb, qw = _rule()
+        self._arrays = [
+            np.ascontiguousarray(m.vertices, dtype=np.float64),
+            np.ascontiguousarray(m.tets, dtype=np.int64),
+            np.ascontiguousarray(space.tet_dofs, dtype=np.int64),
+            np.ascontiguousarray(qb, dtype=np.float64),
+            np.ascontiguousarray(qw, dtype=np.float64),
+        ]
+        v, t, td, qbc, qwc = self._arrays
+        h = C.c_void_p()
+        try:
+            _lib.check(
+                _lib.lib.mdd_space2_create(
+                    ctx.handle, m.cells_per_axis, m.n_vertices, _lib.ptr(v, C.c_double), m.n_tets,
+                    _lib.ptr(t, C.c_int64), _lib.ptr(td, C.c_int64), space.ndof, len(qwc),
+                    _lib.ptr(qbc, C.c_double), _lib.ptr(qwc, C.c_double), C.byref(h),
+                )
+            )
+        except _lib.MddError as e:
+            raise_for(e)
+        self.handle = h
+        self.nt = m.n_tets
+        self.ndof = space.ndof
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _lib.lib.mdd_space_destroy(h)
+            self.handle = None
+
+
+def element2_matrices(coords: np.ndarray):
+    """20x20 order-2 element matrices (device) for tets (nt,4,3) in basis-frame vertex order."""
+    ctx = _lib.get_context()
+    c = np.ascontiguousarray(np.asarray(coords, dtype=np.float64).reshape(-1, 4, 3))
+    nt = c.shape[0]
+    s_el = np.empty((nt, 20, 20))
+    m_el = np.empty((nt, 20, 20))
+    _lib.check(_lib.lib.mdd_element2_matrices(ctx.handle, nt, _lib.ptr(c, C.c_double),
+                                              _lib.ptr(s_el, C.c_double), _lib.ptr(m_el, C.c_double)))
+    return s_el, m_el
 
 
 @dataclass(frozen=True)
@@ -288,6 +486,14 @@ def assemble_rhs(space: EdgeSpace, source) -> np.ndarray:
                     _lib.zptr(rhs),
                 )
             )
+        elif getattr(space, "order", 1) == 2:
+            m = space.mesh
+            coords = m.vertices[np.sort(m.tets, axis=1)]  # basis frame
+            qb, _ = _rule()
+            fv = np.empty((len(qb), m.n_tets, 3), dtype=np.complex128)
+            for q in range(len(qb)):
+                fv[q] = np.asarray(source(np.einsum("i,tic->tc", qb[q], coords)), dtype=complex)
+            _lib.check(_lib.lib.mdd_assemble_rhs(dev.handle, _lib.zptr(fv), _lib.zptr(rhs)))
         else:
             coords = space.mesh.tet_coords()
             fv = np.empty((4, space.mesh.n_tets, 3), dtype=np.complex128)

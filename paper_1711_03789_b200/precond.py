@@ -118,6 +118,8 @@ class PreconditionerState:
         self._prec_coeffs = prec_coeffs
 
         t0 = time.perf_counter()
+        if getattr(space, "order", 1) == 2 and spec.family == "impras":
+            raise ValueError("impras local problems are not available for order-2 spaces")
         if _local_kind(spec) == "pec":
             self.dof_sets = decomp.dofs
             self.pou_weights = decomp.pou
@@ -165,9 +167,20 @@ class PreconditionerState:
         d.sub_ptr = _lib.ptr(sptr, C.c_int64)
         d.sub_dofs = _lib.ptr(sdofs, C.c_int64)
         d.sub_pou = _lib.ptr(pou_flat, C.c_double)
-        xyz = space.dof_half_coords()
+        if getattr(space, "order", 1) == 2:
+            # sixth-cell DoF positions; the Whitney companion space carries the
+            # mesh for the coarse Galerkin product (R0 lives on the Whitney DoFs)
+            xyz = space.dof_coords()
+            d.dof_grid = 6
+            p1dev = space.lowest_order().device()
+            keep.append(p1dev)
+            d.space = p1dev.handle
+        else:
+            xyz = space.dof_half_coords()
+            d.dof_grid = 2
+            d.space = dev.handle
+        keep.append(xyz)
         d.dof_xyz = _lib.ptr(xyz, C.c_int32)
-        d.space = dev.handle
         cc, hold = prec_coeffs.to_c(space.mesh.n_tets)
         keep += [cc, hold]
         d.prec_coeffs = C.pointer(cc)
@@ -186,14 +199,17 @@ class PreconditionerState:
             link = decomp.coarse
             r0 = as_device_csr(link.R0)
             cdev = link.space.device()
-            tmap = np.ascontiguousarray(link.tet_map, dtype=np.int64)
             cxyz = link.space.dof_half_coords()
-            keep += [r0, cdev, tmap, cxyz]
+            keep += [r0, cdev, cxyz]
             self._r0_dev = r0
             self._coarse_dev = cdev
             d.R0 = r0.handle
             d.coarse_space = cdev.handle
-            d.tet_map = _lib.ptr(tmap, C.c_int64)
+            if link.tet_map is not None:  # nested: element-wise Galerkin product
+                tmap = np.ascontiguousarray(link.tet_map, dtype=np.int64)
+                keep.append(tmap)
+                d.tet_map = _lib.ptr(tmap, C.c_int64)
+            # else (non-nested coarse mesh): tet_map stays NULL -> generic R0 A R0^T plan
             d.coarse_dof_xyz = _lib.ptr(cxyz, C.c_int32)
             if space.bc_kind == "impedance":
                 gb = np.ascontiguousarray(space.mesh.boundary_faces, dtype=np.int64)
