@@ -146,6 +146,35 @@ int mdd_space2_create(mdd_ctx* ctx, int32_t cells_per_axis, int64_t nv, const do
  * (vertex order = basis frame). */
 int mdd_element2_matrices(mdd_ctx* ctx, int64_t nt, const double* coords, double* s_el, double* m_el);
 
+/* -------------------------------------------- decomposition (host C++)
+ * Setup-time index work of reference decomp.py / mesh.py (SURVEY.md §8f rank
+ * 1), threaded C++ over the structured Kuhn mesh; no device needed.  Arrays
+ * returned through out-pointers are malloc'ed by the library: release them
+ * with mdd_free.  Index sets are bit-identical to the reference's. */
+void mdd_free(void* p);
+/* decomp.extend_overlap (decomp.py:97-110): nsub tet sets (part_ptr/part_idx)
+ * grown by `layers` rings of vertex-touching tets; outputs ascending. */
+int mdd_extend_overlap(int32_t cells_per_axis, int64_t nv, const int64_t* tets, int32_t nsub,
+                       const int64_t* part_ptr, const int64_t* part_idx, int32_t layers,
+                       int64_t** out_ptr, int64_t** out_idx);
+/* decomp.subdomain_dof_sets (decomp.py:140-176); tet_faces != NULL selects the
+ * order-2 space (face DoFs, numbering [e | e+ned | f+2ned | f+2ned+nfd]). */
+int mdd_subdomain_dofs(int32_t cells_per_axis, int64_t nv, const int64_t* tets, const int64_t* tet_edges,
+                       int64_t ne, const int64_t* edge_to_dof, int64_t ned, const int64_t* tet_faces, int64_t nf,
+                       const int64_t* face_to_dof, int64_t nfd, int32_t nsub, const int64_t* sub_ptr,
+                       const int64_t* sub_tets, int64_t** out_ptr, int64_t** out_dofs);
+/* mesh.nesting_map (mesh.py:231-263): out[nt_fine] = containing coarse tet. */
+int mdd_nesting_map(int32_t nc, const double* cverts, const int64_t* ctets, int32_t nf, const double* fverts,
+                    const int64_t* ftets, double tol, int64_t* out);
+/* decomp.coarse_restriction for nested meshes (decomp.py:212-297): R0 as CSR
+ * (ncs rows over the nkept fine DoFs); *bad_edge = fine edge of a
+ * tangential-trace discontinuity (MDD_EDECOMP). */
+int mdd_coarse_restriction(int64_t nv, const double* fverts, int64_t ntf, const int64_t* ftet_edges,
+                           const int64_t* fedges, int64_t nkept, const int64_t* kept_edges, const double* cverts,
+                           int64_t ntc, const int64_t* ctets, const int64_t* ctet_edges, const int64_t* csigns,
+                           const int64_t* cedge_to_dof, int64_t ncs, const int64_t* tet_map, double continuity_tol,
+                           int64_t** out_rowptr, int64_t** out_cols, double** out_vals, int64_t* bad_edge);
+
 /* ------------------------------------------------------ preconditioner
  * precond.PreconditionerState.__init__ / setup (precond.py:280-323, 380-387)
  * and PreconditionerState.apply (precond.py:347-375).

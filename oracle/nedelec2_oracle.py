@@ -90,10 +90,14 @@ def basis(lam, g):
 def element_matrices(coords, rule=None):
     """S_e, M_e (nt,20,20) for tets (nt,4,3) given in basis-frame vertex order."""
     lam, wq = rule if rule is not None else conical_rule(4)
-    g, vol = gradients(np.asarray(coords, dtype=float))
-    phi, cur = basis(lam, g)
-    M = np.einsum("q,tqkc,tqlc->tkl", wq, phi, phi) * vol[:, None, None]
-    S = np.einsum("q,tqkc,tqlc->tkl", wq, cur, cur) * vol[:, None, None]
+    coords = np.asarray(coords, dtype=float)
+    S = np.empty((len(coords), 20, 20))
+    M = np.empty((len(coords), 20, 20))
+    for a in range(0, len(coords), 2048):  # chunks bound the (nt, Q, 20, 3) temporaries
+        g, vol = gradients(coords[a:a + 2048])
+        phi, cur = basis(lam, g)
+        M[a:a + 2048] = np.einsum("q,tqkc,tqlc->tkl", wq, phi, phi) * vol[:, None, None]
+        S[a:a + 2048] = np.einsum("q,tqkc,tqlc->tkl", wq, cur, cur) * vol[:, None, None]
     return S, M
 
 

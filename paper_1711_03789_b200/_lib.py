@@ -145,6 +145,22 @@ SIGNATURES = {
         [_P, _i32, _i64, _pd, _i64, _pi64, _pi64, _i64, _i32, _pd, _pd, _PP],
     ),
     "mdd_element2_matrices": (C.c_int, [_P, _i64, _pd, _pd, _pd]),
+    "mdd_free": (None, [C.c_void_p]),
+    "mdd_extend_overlap": (
+        C.c_int,
+        [_i32, _i64, _pi64, _i32, _pi64, _pi64, _i32, C.POINTER(_pi64), C.POINTER(_pi64)],
+    ),
+    "mdd_subdomain_dofs": (
+        C.c_int,
+        [_i32, _i64, _pi64, _pi64, _i64, _pi64, _i64, _pi64, _i64, _pi64, _i64, _i32, _pi64, _pi64,
+         C.POINTER(_pi64), C.POINTER(_pi64)],
+    ),
+    "mdd_nesting_map": (C.c_int, [_i32, _pd, _pi64, _i32, _pd, _pi64, C.c_double, _pi64]),
+    "mdd_coarse_restriction": (
+        C.c_int,
+        [_i64, _pd, _i64, _pi64, _pi64, _i64, _pi64, _pd, _i64, _pi64, _pi64, _pi64, _pi64, _i64, _pi64,
+         C.c_double, C.POINTER(_pi64), C.POINTER(_pi64), C.POINTER(_pd), _pi64],
+    ),
     "mdd_prec_create": (C.c_int, [_P, C.POINTER(mdd_prec_desc), _PP, _pi32]),
     "mdd_prec_variant": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _PP]),
     "mdd_prec_destroy": (None, [_P]),
@@ -181,10 +197,20 @@ SIGNATURES = {
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python paper_1711_03789_b200/build.py` "
-            "(the package has no CPU fallback)"
-        )
+        # build the native library in-tree (nvcc); there is no CPU fallback
+        try:
+            import importlib.util
+
+            spec = importlib.util.spec_from_file_location("_mdd_build", os.path.join(os.path.dirname(LIB_PATH),
+                                                                                      "build.py"))
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            mod.build()
+        except Exception as exc:  # noqa: BLE001
+            raise ImportError(
+                f"{LIB_PATH} is missing and could not be built ({exc}): build it with "
+                "`python paper_1711_03789_b200/build.py` (the package has no CPU fallback)"
+            ) from exc
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
@@ -302,3 +328,16 @@ class DeviceBuffer:
 
 def exported_symbols():
     return list(SIGNATURES)
+
+
+def take_ragged(ptr_p, idx_p, n: int) -> list:
+    """Copy a library-allocated ragged array (n+1 offsets + flat int64) into numpy and free it."""
+    import numpy as np
+
+    try:
+        ptr = np.ctypeslib.as_array(ptr_p, shape=(n + 1,)).copy()
+        flat = np.ctypeslib.as_array(idx_p, shape=(max(int(ptr[-1]), 1),))[: int(ptr[-1])].copy()
+    finally:
+        lib.mdd_free(C.cast(ptr_p, C.c_void_p))
+        lib.mdd_free(C.cast(idx_p, C.c_void_p))
+    return [flat[ptr[i]: ptr[i + 1]] for i in range(n)]

@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", f"-I{INCLUDE}"]
 CUFLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["core.cu", "assemble.cu", "nedelec2.cu", "frontal.cu", "solve.cu", "precond.cu", "gmres.cu", "comm.cu", "symbolic.cpp"]
+SOURCES = ["core.cu", "assemble.cu", "nedelec2.cu", "frontal.cu", "solve.cu", "precond.cu", "gmres.cu", "comm.cu", "symbolic.cpp", "decomp.cpp"]
 
 
 def _headers_mtime() -> float:

@@ -6,7 +6,10 @@
 //
 // Algebra (frontal.h): forward  r_U -= F_UP r_P   (leaves -> root)
 //                      backward x_P  = -(F_PP r_P + F_PU x_U)   (root -> leaves)
-// One launch per tree level, one CTA per task.  A task is a row range of one
+// One launch per tree level, one CTA per task; consecutive levels are chained
+// with programmatic dependent launch (the next level's CTAs start their factor
+// TMA copies during this level's tail and wait in griddepcontrol.wait before
+// touching vectors).  A task is a row range of one
 // front block holding ~32 KB of factor data: [F_PP F_PU] rows are contiguous
 // in the row-major front, and F_UP rows are written row-contiguous by the
 // factorisation's F_UP GEMM (frontal.cu), so every task is one contiguous byte range that
@@ -130,6 +133,9 @@ __global__ void __launch_bounds__(256) k_solve_tma(const LvlTask* __restrict__ t
   __shared__ double2 red[8];
   double2* D = reinterpret_cast<double2*>(smraw);
   double2* z = D + dcap;
+  // programmatic dependent launch: let the next level's grid get resident
+  // while this level's last wave runs (its prologue only touches factor data)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t t = first + blockIdx.x;
   const LvlTask tk = tasks[t];
   const int np = tk.np, nrow = tk.nrow, len = tk.len;
@@ -149,6 +155,9 @@ __global__ void __launch_bounds__(256) k_solve_tma(const LvlTask* __restrict__ t
     }
   }
   const int64_t base = tk.base;
+  // everything below reads vectors written by the previous level (or the
+  // kernels before the solve): wait for the prerequisite grid to complete
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (FWD) {
     const int32_t* ga = gabs + tk.aux_off;
     const int m = tk.m;
@@ -242,17 +251,29 @@ void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
   if (nnodes == 0) return;
   const int nl = nlevels;
   static const int pf = (int)env_int("MDD_TSOLVE_PF", kTSolvePrefetch);
+  static const bool pdl = !getenv("MDD_PDL") || atoi(getenv("MDD_PDL")) != 0;  // MDD_PDL=0: plain launches
   const int64_t total = lvl_off[2 * nl];
   for (int k = 0; k < 2 * nl; ++k) {
     const int64_t n = lvl_off[k + 1] - lvl_off[k];
     if (!n) continue;
-    const size_t sm = 16 * (size_t)(lvl_dcap[k] + lvl_zcap[k]);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)n);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 16 * (size_t)(lvl_dcap[k] + lvl_zcap[k]);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     if (k < nl)
-      k_solve_tma<true><<<(unsigned)n, 256, sm, s>>>(ltasks.p, lvl_off[k], total, pf, gmap_abs.p, upd.p, fronts.p,
-                                                     bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]);
+      CK(cudaLaunchKernelEx(&cfg, k_solve_tma<true>, (const LvlTask*)ltasks.p, lvl_off[k], total, pf,
+                            (const int32_t*)gmap_abs.p, (const int32_t*)upd.p, (const double2*)fronts.p,
+                            (const double2*)bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]));
     else
-      k_solve_tma<false><<<(unsigned)n, 256, sm, s>>>(ltasks.p, lvl_off[k], total, pf, gmap_abs.p, upd.p, fronts.p,
-                                                      bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]);
+      CK(cudaLaunchKernelEx(&cfg, k_solve_tma<false>, (const LvlTask*)ltasks.p, lvl_off[k], total, pf,
+                            (const int32_t*)gmap_abs.p, (const int32_t*)upd.p, (const double2*)fronts.p,
+                            (const double2*)bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]));
     CK_LAUNCH(ctx);
   }
 }

@@ -20,11 +20,13 @@ SURVEY.md §8f ranks moving this module off the Python path as the first
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
 import scipy.sparse as sp
 
+from . import _lib
 from .fem import EdgeSpace
 from .linalg import selection_matrix
 from .mesh import LOCAL_EDGES, LOCAL_FACES, Mesh, nesting_map
@@ -96,14 +98,34 @@ def _cell_coords(mesh: Mesh, tets: np.ndarray) -> np.ndarray:
     return np.stack([c // (n * n), (c // n) % n, c % n], axis=1)
 
 
+def _ragged(sets):
+    ptr = np.zeros(len(sets) + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(x) for x in sets])
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int64) for x in sets])
+                                if len(sets) else np.zeros(0, np.int64), dtype=np.int64)
+    return ptr, flat
+
+
 def extend_overlap(mesh: Mesh, partition: list, layers: int) -> list:
     """Grow each set by `layers` rings of vertex-touching tets (reference decomp.py:97-110).
 
-    A tet touching a vertex of a set tet lies in a cell within one cell of
-    it, so each layer is computed on the window of cells around the set.
+    Threaded C++ (csrc/decomp.cpp, ``mdd_extend_overlap``): a tet touching a
+    vertex of a set tet lies in a cell within one cell of it, so each ring is
+    searched in the window of cells around the set.
     """
     if layers < 1:
         raise DecompositionError("layers must be >= 1")
+    ptr, flat = _ragged(partition)
+    tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+    op, oi = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    _lib.check(_lib.lib.mdd_extend_overlap(mesh.cells_per_axis, mesh.n_vertices, _lib.ptr(tets, C.c_int64),
+                                           len(partition), _lib.ptr(ptr, C.c_int64), _lib.ptr(flat, C.c_int64),
+                                           int(layers), C.byref(op), C.byref(oi)))
+    return _lib.take_ragged(op, oi, len(partition))
+
+
+def _extend_overlap_numpy(mesh: Mesh, partition: list, layers: int) -> list:
+    """Vectorised numpy form of :func:`extend_overlap` (kept as a cross-check in tests)."""
     n = mesh.cells_per_axis
     out = []
     for elems in partition:
@@ -144,7 +166,31 @@ def subdomain_boundary_faces(mesh: Mesh, elems: np.ndarray) -> np.ndarray:
 
 
 def subdomain_dof_sets(space: EdgeSpace, elements: list) -> list:
-    """Unknowns with zero trace on internal boundaries (reference decomp.py:140-176)."""
+    """Unknowns with zero trace on internal boundaries (reference decomp.py:140-176).
+
+    Threaded C++ (csrc/decomp.cpp, ``mdd_subdomain_dofs``) for both the
+    Whitney and the order-2 space; the numpy forms below are cross-checks."""
+    mesh = space.mesh
+    o2 = getattr(space, "order", 1) == 2
+    ptr, flat = _ragged(elements)
+    tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+    te = np.ascontiguousarray(mesh.tet_edges, dtype=np.int64)
+    e2d = np.ascontiguousarray(space.edge_to_dof, dtype=np.int64)
+    if o2:
+        tf = np.ascontiguousarray(space.tet_faces, dtype=np.int64)
+        f2d = np.ascontiguousarray(space.face_to_dof, dtype=np.int64)
+        tf_p, f2d_p, nf, nfd = _lib.ptr(tf, C.c_int64), _lib.ptr(f2d, C.c_int64), len(f2d), space.n_face_dofs
+    else:
+        tf_p, f2d_p, nf, nfd = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), 0, 0
+    op, oi = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    _lib.check(_lib.lib.mdd_subdomain_dofs(
+        mesh.cells_per_axis, mesh.n_vertices, _lib.ptr(tets, C.c_int64), _lib.ptr(te, C.c_int64), len(e2d),
+        _lib.ptr(e2d, C.c_int64), int((e2d >= 0).sum()), tf_p, nf, f2d_p, nfd, len(elements),
+        _lib.ptr(ptr, C.c_int64), _lib.ptr(flat, C.c_int64), C.byref(op), C.byref(oi)))
+    return _lib.take_ragged(op, oi, len(elements))
+
+
+def _subdomain_dof_sets_numpy(space: EdgeSpace, elements: list) -> list:
     if getattr(space, "order", 1) == 2:
         return _subdomain_dof_sets2(space, elements)
     mesh = space.mesh
@@ -222,7 +268,47 @@ def coarse_restriction(
     tet_map: np.ndarray | None = None,
     continuity_tol: float = 1e-10,
 ) -> sp.csr_matrix:
-    """R0[p, j] = line integral of coarse basis p along fine edge j (reference decomp.py:212-297)."""
+    """R0[p, j] = line integral of coarse basis p along fine edge j (reference decomp.py:212-297).
+
+    Threaded C++ (csrc/decomp.cpp, ``mdd_coarse_restriction``) with the exact
+    closed form of the line integral; the numpy form below is a cross-check."""
+    fine, coarse = fine_space.mesh, coarse_space.mesh
+    if tet_map is None:
+        tet_map = nesting_map(coarse, fine)
+    arr = lambda a, t=np.int64: np.ascontiguousarray(a, dtype=t)  # noqa: E731
+    fv, fte, fe, kept = arr(fine.vertices, np.float64), arr(fine.tet_edges), arr(fine.edges), arr(fine_space.kept_edges)
+    cv, ctt, cte, cs, ce2d = (arr(coarse.vertices, np.float64), arr(coarse.tets), arr(coarse.tet_edges),
+                              arr(coarse.tet_edge_signs), arr(coarse_space.edge_to_dof))
+    tm = arr(tet_map)
+    rp, cl, vl = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_double)()
+    bad = C.c_int64(-1)
+    I64, F64 = C.c_int64, C.c_double
+    code = _lib.lib.mdd_coarse_restriction(
+        fine.n_vertices, _lib.ptr(fv, F64), fine.n_tets, _lib.ptr(fte, I64), _lib.ptr(fe, I64), len(kept),
+        _lib.ptr(kept, I64), _lib.ptr(cv, F64), coarse.n_tets, _lib.ptr(ctt, I64), _lib.ptr(cte, I64),
+        _lib.ptr(cs, I64), _lib.ptr(ce2d, I64), coarse_space.ndof, _lib.ptr(tm, I64), continuity_tol,
+        C.byref(rp), C.byref(cl), C.byref(vl), C.byref(bad))
+    if code == 7:  # MDD_EDECOMP
+        raise DecompositionError(f"tangential trace discontinuity on fine edge {bad.value}")
+    _lib.check(code)
+    ncs = coarse_space.ndof
+    try:
+        indptr = np.ctypeslib.as_array(rp, shape=(ncs + 1,)).copy()
+        nnz = int(indptr[-1])
+        indices = np.ctypeslib.as_array(cl, shape=(max(nnz, 1),))[:nnz].astype(np.int32)
+        data = np.ctypeslib.as_array(vl, shape=(max(nnz, 1),))[:nnz].copy()
+    finally:
+        for p in (rp, cl, vl):
+            _lib.lib.mdd_free(C.cast(p, C.c_void_p))
+    return sp.csr_matrix((data, indices, indptr.astype(np.int32)), shape=(ncs, fine_space.ndof))
+
+
+def _coarse_restriction_numpy(
+    fine_space: EdgeSpace,
+    coarse_space: EdgeSpace,
+    tet_map: np.ndarray | None = None,
+    continuity_tol: float = 1e-10,
+) -> sp.csr_matrix:
     fine, coarse = fine_space.mesh, coarse_space.mesh
     if tet_map is None:
         tet_map = nesting_map(coarse, fine)

@@ -103,3 +103,26 @@ def test_coarse_equal_fine_is_identity():
     s = fem.build_edge_space(mesh.build_cube_mesh(2), "pec")
     r0 = decomp.coarse_restriction(s, s)
     assert np.abs(r0.toarray() - np.eye(s.ndof)).max() <= 1e-14
+
+
+@pytest.mark.parametrize("n,p,layers,bc,order", [(12, 3, 2, "pec", 1), (8, 2, 1, "impedance", 1), (8, 4, 2, "pec", 2)])
+def test_native_decomposition_matches_numpy(n, p, layers, bc, order):
+    """csrc/decomp.cpp (threaded C++) against the vectorised numpy forms."""
+    m = mesh.build_cube_mesh(n)
+    s = fem.build_edge_space(m, bc, order=order)
+    part = decomp.box_partition(m, p)
+    el = decomp.extend_overlap(m, part, layers)
+    el_np = decomp._extend_overlap_numpy(m, part, layers)
+    assert all(np.array_equal(a, b) for a, b in zip(el, el_np))
+    d = decomp.subdomain_dof_sets(s, el)
+    d_np = decomp._subdomain_dof_sets_numpy(s, el)
+    assert all(np.array_equal(a, b) for a, b in zip(d, d_np))
+    c = fem.build_edge_space(mesh.build_cube_mesh(n // 2), bc)
+    tm = mesh.nesting_map(c.mesh, m)
+    assert np.array_equal(tm, mesh._nesting_map_numpy(c.mesh, m))
+    p1 = s.lowest_order() if order == 2 else s
+    r = decomp.coarse_restriction(p1, c, tm)
+    r_np = decomp._coarse_restriction_numpy(p1, c, tm)
+    # same values to rounding; entries that are zero up to ~1e-17 roundoff may be
+    # stored by one form and exactly zero in the other
+    assert abs(r - r_np).max() <= 1e-15
