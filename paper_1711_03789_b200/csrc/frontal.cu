@@ -132,6 +132,175 @@ __global__ void __launch_bounds__(32 * kInvWarps) k_invert(const NodeDev* __rest
   }
 }
 
+// Whole pivot-block inverse of a small front (np <= 32 levels) in one CTA,
+// the block in shared memory: F_PP <- -F_PP^{-1} by unpivoted in-place
+// Gauss-Jordan.  Per pivot, the pivot row and column are copied to shared
+// memory, one barrier, then every thread updates its elements (dealt
+// round-robin, only the np x np block is touched), one barrier.  It replaces
+// the sweep steps where those are latency-bound; it is issue-bound at ~30
+// instructions per element update, so larger pivot blocks keep the sweeps.
+__global__ void __launch_bounds__(256) k_gj_smem(const NodeDev* __restrict__ nodes, const int32_t* __restrict__ act,
+                                                 double2* __restrict__ fronts, double* __restrict__ pivstat) {
+  extern __shared__ double2 A[];
+  __shared__ double2 colp[96], rowp[96];
+  const int node = act[blockIdx.x];
+  const NodeDev nd = nodes[node];
+  const int np = nd.np, m = nd.m, ne = np * np;
+  double2* F = fronts + nd.front_off;
+  for (int e = threadIdx.x; e < ne; e += 256) A[e] = F[(int64_t)(e / np) * m + e % np];
+  __syncthreads();
+  double pmin = INFINITY, pmax = 0.0;
+  for (int p = 0; p < np; ++p) {
+    const int t = threadIdx.x;
+    if (t < np) colp[t] = A[t * np + p];
+    else if (t < 2 * np) rowp[t - np] = A[p * np + t - np];
+    __syncthreads();
+    const double2 piv = colp[p];
+    const double2 d = cdiv(make_double2(1.0, 0.0), piv);
+    if (t == 0) {
+      const double am = hypot(piv.x, piv.y);
+      pmin = fmin(pmin, isfinite(am) ? am : 0.0);
+      pmax = fmax(pmax, isfinite(am) ? am : INFINITY);
+    }
+    int r = t / np, c = t - r * np;
+    const int dr = 256 / np, dc = 256 - dr * np;  // e += 256 in (r, c)
+    for (int e = t; e < ne; e += 256) {
+      double2 v;
+      if (r == p) v = (c == p) ? d : cmul(rowp[c], d);
+      else if (c == p) v = cneg(cmul(colp[r], d));
+      else v = csub(A[e], cmul(colp[r], cmul(rowp[c], d)));
+      A[e] = v;
+      r += dr;
+      c += dc;
+      if (c >= np) {
+        c -= np;
+        ++r;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < ne; e += 256) F[(int64_t)(e / np) * m + e % np] = cneg(A[e]);
+  if (threadIdx.x == 0) {
+    pivstat[2 * node] = fmin(pivstat[2 * node], pmin);
+    pivstat[2 * node + 1] = fmax(pivstat[2 * node + 1], pmax);
+  }
+}
+
+// Inverse of the 32x32 pivot block of one sweep step, one 256-thread CTA
+// per active node (replaces the one-warp k_invert, kept as MDD_INV_WARP=1:
+// 10 us instead of 59 us
+// per step at the cfg1 root level).  The kb x kb diagonal block at
+// K0 = step*kPB, padded with the identity, is held in registers (thread
+// (ti,tj) of a 16x16 grid owns an NBxNB tile); per pivot the owners of row p
+// and column p publish them to shared memory (double-buffered by parity),
+// one barrier, then every thread applies the rank-1 update to its tile.
+// Output P = inverse (not negated) in pbuf.  (SWEEP = false would invert a
+// whole np <= 16*NB pivot block in place as -F_PP^{-1}.)
+template <int NB, bool SWEEP = false>
+__global__ void __launch_bounds__(256, NB <= 4 ? 2 : 1) k_gj_small(const NodeDev* __restrict__ nodes,
+                                                  const int32_t* __restrict__ act, double2* __restrict__ fronts,
+                                                  double* __restrict__ pivstat, int step = 0,
+                                                  double2* __restrict__ pbuf = nullptr) {
+  constexpr int N = 16 * NB;
+  __shared__ double2 rowb[2][N], colb[2][N];
+  __shared__ double2 pivs[2];
+  const int node = act[blockIdx.x];
+  const NodeDev nd = nodes[node];
+  const int K0 = SWEEP ? step * kPB : 0;
+  const int np = SWEEP ? min(kPB, nd.np - K0) : nd.np, m = nd.m;
+  double2* F = fronts + nd.front_off + (int64_t)K0 * m + K0;
+  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+  const int r0 = NB * ti, c0 = NB * tj;
+  double2 a[NB][NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int r = r0 + i, c = c0 + j;
+      a[i][j] = (r < np && c < np) ? F[(int64_t)r * m + c] : make_double2(r == c ? 1.0 : 0.0, 0.0);
+    }
+  double pmin = INFINITY, pmax = 0.0;
+  for (int p = 0; p < np; ++p) {
+    const int b = p & 1;
+    const int pi = p / NB, pj = p - NB * (p / NB);  // owner tile row/col and offset
+    // owners of column p publish the old column (incl. the pivot)
+    // (compile-time indices only, so the tile stays in registers)
+    if (tj == pi) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj)
+          if (jj == pj) colb[b][r0 + i] = a[i][jj];
+    }
+    if (ti == pi) {
+#pragma unroll
+      for (int ii = 0; ii < NB; ++ii)
+        if (ii == pj) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            rowb[b][c0 + j] = a[ii][j];
+            if (tj == pi && j == pj) {  // the pivot's owner: reciprocal + magnitude
+              const double2 piv = a[ii][j];
+              pivs[b] = cdiv(make_double2(1.0, 0.0), piv);
+              const double am = hypot(piv.x, piv.y);
+              pmin = fmin(pmin, isfinite(am) ? am : 0.0);
+              pmax = fmax(pmax, isfinite(am) ? am : INFINITY);
+            }
+          }
+        }
+    }
+    __syncthreads();
+    const double2 d = pivs[b];
+    double2 cf[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) cf[i] = colb[b][r0 + i];
+    // uniform rank-1 update, then overwrite row p / column p (their owners)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double2 rs = cmul(rowb[b][c0 + j], d);  // scaled pivot row
+#pragma unroll
+      for (int i = 0; i < NB; ++i) a[i][j] = csub(a[i][j], cmul(cf[i], rs));
+      if (ti == pi) {
+#pragma unroll
+        for (int ii = 0; ii < NB; ++ii)
+          if (ii == pj) a[ii][j] = rs;
+      }
+    }
+    if (tj == pi) {
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj)
+        if (jj == pj) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) a[i][jj] = (r0 + i == p) ? d : cneg(cmul(cf[i], d));
+        }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int r = r0 + i, c = c0 + j;
+      if (SWEEP) pbuf[(int64_t)blockIdx.x * kPB * kPB + r * kPB + c] = a[i][j];
+      else if (r < np && c < np) F[(int64_t)r * m + c] = cneg(a[i][j]);
+    }
+  // pivot magnitudes: each diagonal owner saw its own pivots
+  __shared__ double pm[2][16];
+  if (ti == tj) {
+    pm[0][ti] = pmin;
+    pm[1][ti] = pmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mn = pm[0][0], mx = pm[1][0];
+    for (int k = 1; k < 16; ++k) {
+      mn = fmin(mn, pm[0][k]);
+      mx = fmax(mx, pm[1][k]);
+    }
+    pivstat[2 * node] = fmin(pivstat[2 * node], mn);
+    pivstat[2 * node + 1] = fmax(pivstat[2 * node + 1], mx);
+  }
+}
+
 // Row panel F[K][c] <- P F[K][c] (c outside K), F[K][K] <- -P, and the copy
 // W[r][:] = old F[r][K] (r outside K) used by the trailing update.
 __global__ void __launch_bounds__(kPanelCols) k_panel(const int2* __restrict__ tasks,
@@ -616,6 +785,9 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   step_panel_off.assign(1, 0);
   step_tile_off.assign(1, 0);
   lev_copyb_off.assign(1, 0);
+  lev_gjs_off.assign(1, 0);
+  lev_gj_nb.clear();
+  std::vector<int32_t> h_gjs;
   lev_yz_off.assign(1, 0);
   lev_s_off.assign(1, 0);
   int64_t bb_max = 0;
@@ -661,7 +833,15 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     lev_copyb_off.push_back((int64_t)h_copyb.size());
     lev_yz_off.push_back((int64_t)h_yz.size());
     lev_s_off.push_back((int64_t)h_s.size());
-    const int nst = (lnp + kPB - 1) / kPB;
+    // small pivot blocks: one k_gj_smem CTA per node instead of the sweeps
+    // (k_gj_smem is issue-bound at ~30 instructions per element update; it
+    // beats the sweeps for np <= 32 only, measured on the B200)
+    lev_gj_nb.push_back(lnp <= 32 ? lnp : 0);
+    if (getenv("MDD_NO_GJ_SMALL")) lev_gj_nb.back() = 0;
+    for (int32_t g : lev[L])
+      if (lev_gj_nb.back() && h_nodes[g].np > 0) h_gjs.push_back(g);
+    lev_gjs_off.push_back((int64_t)h_gjs.size());
+    const int nst = lev_gj_nb.back() ? 0 : (lnp + kPB - 1) / kPB;
     lev_steps[L] = nst;
     lev_step_base[L] = nsteps_total;
     for (int st = 0; st < nst; ++st) {
@@ -724,6 +904,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   }
   bbuf.alloc(std::max<int64_t>(1, bb_max));
   act_node.upload(h_act, s);
+  gjs_node.upload(h_gjs.empty() ? std::vector<int32_t>{0} : h_gjs, s);
   act_woff.upload(h_woff, s);
   fronts.alloc(front_total + upk_total);
   uvec.alloc(std::max<int64_t>(1, uvec_total));
@@ -738,6 +919,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
     CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
+    CK(cudaFuncSetAttribute(k_gj_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double2) * 96 * 96)));
     CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
     attr_set = true;
@@ -773,6 +955,7 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
   CK_LAUNCH(ctx);
   const size_t upd_smem = sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1));
   const size_t inv_smem = sizeof(double2) * kInvWarps * kPB * (kPB + 1);
+  static const bool inv_warp = getenv("MDD_INV_WARP") != nullptr;  // A/B: the one-warp k_invert
   for (int L = 0; L < nlevels; ++L) {
     const int64_t ni = lev_init_off[L + 1] - lev_init_off[L];
     if (ni) {
@@ -791,14 +974,26 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
       k_copy_b<<<(unsigned)((ncb + 7) / 8), 256, 0, s>>>(copyb_tasks.p + cb0, ncb, nodes.p, fronts.p, bbuf.p);
       CK_LAUNCH(ctx);
     }
+    if (lev_gj_nb[L]) {
+      const int64_t g0 = lev_gjs_off[L], ng = lev_gjs_off[L + 1] - g0;
+      if (ng) {
+        const int n = lev_gj_nb[L];  // max np of the level
+        k_gj_smem<<<(unsigned)ng, 256, sizeof(double2) * n * n, s>>>(nodes.p, gjs_node.p + g0, fronts.p,
+                                                                      pivstat.p);
+        CK_LAUNCH(ctx);
+      }
+    }
     for (int st = 0; st < lev_steps[L]; ++st) {
       const int64_t si = lev_step_base[L] + st;
       const int64_t a0 = step_act_off[si], na = step_act_off[si + 1] - a0;
       const int64_t p0 = step_panel_off[si], npn = step_panel_off[si + 1] - p0;
       const int64_t t0 = step_tile_off[si], ntl = step_tile_off[si + 1] - t0;
       if (!na) continue;
-      k_invert<<<(unsigned)((na + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, inv_smem, s>>>(
-          nodes.p, act_node.p + a0, (int)na, st, fronts.p, pbuf.p, pivstat.p);
+      if (inv_warp)
+        k_invert<<<(unsigned)((na + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, inv_smem, s>>>(
+            nodes.p, act_node.p + a0, (int)na, st, fronts.p, pbuf.p, pivstat.p);
+      else
+        k_gj_small<2, true><<<(unsigned)na, 256, 0, s>>>(nodes.p, act_node.p + a0, fronts.p, pivstat.p, st, pbuf.p);
       CK_LAUNCH(ctx);
       k_panel<<<(unsigned)npn, kPanelCols, 0, s>>>(panel_tasks.p + p0, nodes.p, act_node.p + a0,
                                                    act_woff.p + a0, st, fronts.p, pbuf.p, wbuf.p);

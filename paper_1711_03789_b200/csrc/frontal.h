@@ -95,6 +95,10 @@ struct FrontPlan {
   std::vector<int64_t> step_panel_off;
   std::vector<int64_t> step_tile_off;
   DevBuf<int32_t> act_node;
+  // levels whose pivot blocks all have np <= 96: one k_gj_small CTA per node
+  std::vector<int32_t> lev_gj_nb;        // 0 (sweeps) or the level's max np (<= 96, k_gj_smem)
+  std::vector<int64_t> lev_gjs_off;
+  DevBuf<int32_t> gjs_node;
   DevBuf<int64_t> act_woff;
   DevBuf<int2> panel_tasks;
   DevBuf<int4> tile_tasks;
