@@ -50,7 +50,7 @@ struct ArnoldiArgs {
   double2* w;      // new direction (input: operator output)
   double2* dw;     // D w (weighted) or nullptr
   double2* vin;    // out: copy of V[m] = next operator input
-  double2* partials;  // (2*maxit+1) publications x 2 (dot, drift) x G, NaN-filled per launch
+  double2* partials;  // (2*maxit+1) publications x G slots of `pad` double2 (dot, drift), NaN-filled per launch
   double2* H;      // (maxit+1) x maxit, column j at H + j*(maxit+1)
   double2* cs;
   double2* sn;
@@ -66,6 +66,7 @@ struct ArnoldiArgs {
   cudaGraphConditionalHandle cond;
   int use_cond;
   int64_t wcap;  // STREAM path: w elements of the slice held in shared memory
+  int pad;       // double2 per publication slot (2 or 8)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -100,31 +101,6 @@ __device__ __forceinline__ void block_sum2x2(double2& a, double2& b, double2* sh
   b = sh[65];
 }
 
-// deterministic sums of the G partials of one step (dot and drift)
-__device__ __forceinline__ void reduce_step(const double2* p, int G, double2* sh, double2& dot,
-                                            double2& dr) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
-    for (int k = threadIdx.x; k < G; k += 32) {
-      const double2 u = __ldcg(p + k), v = __ldcg(p + G + k);
-      a.x += u.x;
-      a.y += u.y;
-      b.x += v.x;
-      b.y += v.y;
-    }
-    a = warp_sum2(a);
-    b = warp_sum2(b);
-    if (threadIdx.x == 0) {
-      sh[66] = a;
-      sh[67] = b;
-    }
-  }
-  __syncthreads();
-  dot = sh[66];
-  dr = sh[67];
-}
-
 constexpr int kArnE = 12;  // vector elements per thread kept in registers (register path)
 constexpr int kArnPf = 4;  // REG path: L2 prefetch distance in MGS steps
 
@@ -143,9 +119,15 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 // non-NaN (each half is single-copy atomic).  Reading the value *is* the
 // synchronisation: one round trip, no flags, no fences.  Partial sums of
 // finite vectors are finite; a NaN input traps instead of hanging.
-__device__ __forceinline__ void publish(double2* slot_step, int G, double2 a, double2 b) {
-  __stcg(slot_step + blockIdx.x, a);
-  __stcg(slot_step + G + blockIdx.x, b);
+// Each CTA's (dot, drift) pair is one slot of `pad` double2 (pad = 8: alone
+// on a 128-byte L2 line).  In isolation the flat all-gather runs at 3.3 us per
+// step with 16-byte slots and 1.8 us with one slot per line (hot-line
+// serialisation of the G*G polls, tools/allgather_bench.cu); inside k_arnoldi
+// the padded layout is slower on the REG path and faster on the STREAM path,
+// so the host picks the stride per path (measured on the B200).
+__device__ __forceinline__ void publish(double2* slot_step, int pad, double2 a, double2 b) {
+  __stcg(slot_step + (int64_t)blockIdx.x * pad, a);
+  __stcg(slot_step + (int64_t)blockIdx.x * pad + 1, b);
 }
 
 __device__ __forceinline__ bool bad2(double2 v) { return isnan(v.x) || isnan(v.y); }
@@ -163,18 +145,19 @@ __device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
 // drift slot only when `with_drift`: both loads in flight together); warp 0
 // then sums them in CTA order (fixed order -> bitwise reproducible) and
 // broadcasts the result.
-__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, double2* sh,
+__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int pad, double2* sh,
                                            double2& dot, double2& dr, bool with_drift = true) {
   double2* stage = sh + 68;  // 2*G slots after the block-reduce scratch
   if ((int)threadIdx.x < G) {
     const int k = threadIdx.x;
     long long spins = 0;
-    double2 u = ld_relaxed2(slot_step + k);
-    double2 v = with_drift ? ld_relaxed2(slot_step + G + k) : make_double2(0.0, 0.0);
+    const double2* line = slot_step + (int64_t)k * pad;
+    double2 u = ld_relaxed2(line);
+    double2 v = with_drift ? ld_relaxed2(line + 1) : make_double2(0.0, 0.0);
     while (bad2(u) || bad2(v)) {
       if (++spins > (1ll << 28)) __trap();  // never hang the device
-      if (bad2(u)) u = ld_relaxed2(slot_step + k);
-      if (bad2(v)) v = ld_relaxed2(slot_step + G + k);
+      if (bad2(u)) u = ld_relaxed2(line);
+      if (bad2(v)) v = ld_relaxed2(line + 1);
     }
     stage[k] = u;
     stage[G + k] = v;
@@ -306,7 +289,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   const double2* dvm1 = (weighted ? a.DV : a.V) + (int64_t)(m - 1) * n;
   const int nsteps = 2 * m;
   // slots of publication k (k = s+1 for step s; k = 0 for the initial dot)
-  auto slots = [&](int k) { return a.partials + (int64_t)k * 2 * G; };
+  auto slots = [&](int k) { return a.partials + (int64_t)k * G * a.pad; };
   for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
   // X_t = V_{t mod m} for t < nsteps; X_nsteps = w (the norm)
   auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n; };
@@ -352,7 +335,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
       }
     }
     block_sum_t0(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16);
-    if (threadIdx.x == 0) publish(slots(0), G, acc, dacc);
+    if (threadIdx.x == 0) publish(slots(0), a.pad, acc, dacc);
     if constexpr (REG) {
       const double2* x1 = xvec(1);
 #pragma unroll
@@ -367,7 +350,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     const int j = s % m;
     double2 h, d;
     // the drift slot carries data only in the first pass (s <= m-2)
-    gather_sum(slots(s), G, red, h, d, do_drift && s < m - 1);
+    gather_sum(slots(s), G, a.pad, red, h, d, do_drift && s < m - 1);
     if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));  // drift term of X_s = V_s
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
@@ -437,7 +420,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
       }
     }
     block_sum_t0(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16 * (s & 1));
-    if (threadIdx.x == 0) publish(slots(s + 1), G, acc, dacc);
+    if (threadIdx.x == 0) publish(slots(s + 1), a.pad, acc, dacc);
     if constexpr (REG) {
       if (s + 2 < nsteps) {  // preload X_{s+2} while the other CTAs arrive
         const double2* x2 = xvec(s + 2);
@@ -450,7 +433,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     }
   }
   double2 hn2, dummy;
-  gather_sum(slots(nsteps), G, red, hn2, dummy, false);
+  gather_sum(slots(nsteps), G, a.pad, red, hn2, dummy, false);
   const double hlast = sqrt(fmax(hn2.x, 0.0));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
@@ -1047,7 +1030,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
   if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
-  const size_t part_elems = (size_t)(2 * maxit + 1) * 2 * G;
+  const int pad = getenv("MDD_ARN_PAD") ? std::max(2, atoi(getenv("MDD_ARN_PAD"))) : (mode == 1 ? 2 : 8);
+  const size_t part_elems = (size_t)(2 * maxit + 1) * G * pad;
   DevBuf<double2> partials(part_elems);
   // host-mapped status word, allocated once per context (cudaHostAlloc and
   // cudaFreeHost are slow and cudaFreeHost synchronises the device)
@@ -1078,6 +1062,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.iter = diter.p;
   aa.dstatus = dstat.p;
   aa.wcap = wcap;
+  aa.pad = pad;
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
     // NaN-fill the publication slots (0xFF bytes are a NaN pattern)

@@ -117,8 +117,8 @@ __device__ __forceinline__ void smem_gemv(const double2* __restrict__ D, int R, 
 // level this reaches into the next level's first tasks and also covers the
 // launch gap).  HBM is thus kept busy by prefetches independently of how long
 // each CTA spends in its vector gathers.
-template <bool FWD>
-__global__ void __launch_bounds__(256) k_solve_tma(const LvlTask* __restrict__ tasks, int64_t first,
+template <bool FWD, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_solve_tma(const LvlTask* __restrict__ tasks, int64_t first,
                                                    int64_t total, int pf,
                                                    const int32_t* __restrict__ gabs,
                                                    const int32_t* __restrict__ upd,
@@ -241,8 +241,12 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
   ltasks.upload(ht, ctx->stream);
   static bool attr = false;  // per-function attribute shared by every plan
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_solve_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CK(cudaFuncSetAttribute(k_solve_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CK(cudaFuncSetAttribute(k_solve_tma<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
 }
@@ -252,6 +256,7 @@ void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
   const int nl = nlevels;
   static const int pf = (int)env_int("MDD_TSOLVE_PF", kTSolvePrefetch);
   static const bool pdl = !getenv("MDD_PDL") || atoi(getenv("MDD_PDL")) != 0;  // MDD_PDL=0: plain launches
+  static const int minb = getenv("MDD_SOLVE_MINB") ? atoi(getenv("MDD_SOLVE_MINB")) : 6;  // register cap (40 regs: 6 CTAs/SM; measured best)
   const int64_t total = lvl_off[2 * nl];
   for (int k = 0; k < 2 * nl; ++k) {
     const int64_t n = lvl_off[k + 1] - lvl_off[k];
@@ -266,14 +271,11 @@ void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (k < nl)
-      CK(cudaLaunchKernelEx(&cfg, k_solve_tma<true>, (const LvlTask*)ltasks.p, lvl_off[k], total, pf,
-                            (const int32_t*)gmap_abs.p, (const int32_t*)upd.p, (const double2*)fronts.p,
-                            (const double2*)bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]));
-    else
-      CK(cudaLaunchKernelEx(&cfg, k_solve_tma<false>, (const LvlTask*)ltasks.p, lvl_off[k], total, pf,
-                            (const int32_t*)gmap_abs.p, (const int32_t*)upd.p, (const double2*)fronts.p,
-                            (const double2*)bloc.p, v, gidx, fpst.p, uvec.p, xloc.p, (int)lvl_dcap[k]));
+    auto kfn = k < nl ? (minb == 8 ? k_solve_tma<true, 8> : minb == 6 ? k_solve_tma<true, 6> : k_solve_tma<true, 0>)
+                      : (minb == 8 ? k_solve_tma<false, 8> : minb == 6 ? k_solve_tma<false, 6> : k_solve_tma<false, 0>);
+    CK(cudaLaunchKernelEx(&cfg, kfn, (const LvlTask*)ltasks.p, lvl_off[k], total, pf, (const int32_t*)gmap_abs.p,
+                          (const int32_t*)upd.p, (const double2*)fronts.p, (const double2*)bloc.p, v, gidx, fpst.p,
+                          uvec.p, xloc.p, (int)lvl_dcap[k]));
     CK_LAUNCH(ctx);
   }
 }

@@ -61,6 +61,25 @@ __global__ void __launch_bounds__(256, 1) k_steps(int nsteps, double2* slots, do
       }
       __syncthreads();
       tot = sh[62];
+    } else if (MODE == 3) {
+      // flat all-gather with every slot on its own 128-byte L2 line
+      constexpr int PAD = 8;
+      if (threadIdx.x == 0) __stcg(slots + ((size_t)s * G + blockIdx.x) * PAD, part);
+      double2* st = sh + 64;
+      if ((int)threadIdx.x < G) {
+        double2 u = ld_relaxed2(slots + ((size_t)s * G + threadIdx.x) * PAD);
+        { long long sp = 0; while (bad2(u)) { if (++sp > (1ll << 26)) __trap(); u = ld_relaxed2(slots + ((size_t)s * G + threadIdx.x) * PAD); } }
+        st[threadIdx.x] = u;
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double2 x = make_double2(0, 0);
+        for (int k = threadIdx.x; k < G; k += 32) x.x += st[k].x, x.y += st[k].y;
+        x = wsum(x);
+        if (threadIdx.x == 0) sh[62] = x;
+      }
+      __syncthreads();
+      tot = sh[62];
     } else if (MODE == 1) {
       if (threadIdx.x < 32) {
         unsigned old = 0;
@@ -132,21 +151,22 @@ int main(int argc, char** argv) {
   double2* res;
   unsigned* cnt;
   double* out;
-  cudaMalloc(&slots, sizeof(double2) * (size_t)steps * G);
+  cudaMalloc(&slots, sizeof(double2) * (size_t)steps * G * 8);
   cudaMalloc(&res, sizeof(double2) * steps);
   cudaMalloc(&cnt, sizeof(unsigned) * steps);
   cudaMalloc(&out, sizeof(double) * G);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
     for (int rep = 0; rep < 3; ++rep) {
-      cudaMemset(slots, 0xff, sizeof(double2) * (size_t)steps * G);  // NaN
+      cudaMemset(slots, 0xff, sizeof(double2) * (size_t)steps * G * 8);  // NaN
       cudaMemset(res, 0xff, sizeof(double2) * steps);
       cudaMemset(cnt, 0, sizeof(unsigned) * steps);
       cudaEventRecord(a);
       if (mode == 0) k_steps<0><<<G, 256>>>(steps, slots, res, cnt, out);
       if (mode == 1) k_steps<1><<<G, 256>>>(steps, slots, res, cnt, out);
+      if (mode == 3) k_steps<3><<<G, 256>>>(steps, slots, res, cnt, out);
       if (mode == 2) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(G);
