@@ -67,6 +67,7 @@ struct ArnoldiArgs {
   int use_cond;
   int64_t wcap;  // STREAM path: w elements of the slice held in shared memory
   int pad;       // double2 per publication slot (2 or 8)
+  int wg;        // 1: warp 0 alone polls the slots (gather_sum)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -145,8 +146,54 @@ __device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
 // drift slot only when `with_drift`: both loads in flight together); warp 0
 // then sums them in CTA order (fixed order -> bitwise reproducible) and
 // broadcasts the result.
-__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int pad, double2* sh,
-                                           double2& dot, double2& dr, bool with_drift = true) {
+__device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int pad, bool warp_gather,
+                                           double2* sh, double2& dot, double2& dr, bool with_drift = true) {
+  if (warp_gather) {
+    // warp 0 alone polls: each lane keeps its <= kNPL slots' loads in flight
+    // together and re-polls only the missing ones; it sums in the same order
+    // as the staged variant below (bitwise-identical results), and the CTA
+    // needs one barrier instead of two
+    constexpr int kNPL = (kMaxArnCTAs + 31) / 32;
+    if (threadIdx.x < 32) {
+      double2 u[kNPL], v[kNPL];
+#pragma unroll
+      for (int i = 0; i < kNPL; ++i) {
+        const int k = threadIdx.x + 32 * i;
+        const double2* line = slot_step + (int64_t)k * pad;
+        u[i] = k < G ? ld_relaxed2(line) : make_double2(0.0, 0.0);
+        v[i] = (k < G && with_drift) ? ld_relaxed2(line + 1) : make_double2(0.0, 0.0);
+      }
+      long long spins = 0;
+      for (;;) {
+        bool miss = false;
+#pragma unroll
+        for (int i = 0; i < kNPL; ++i) {
+          const int k = threadIdx.x + 32 * i;
+          const double2* line = slot_step + (int64_t)k * pad;
+          if (bad2(u[i])) { u[i] = ld_relaxed2(line); miss = true; }
+          if (bad2(v[i])) { v[i] = ld_relaxed2(line + 1); miss = true; }
+        }
+        if (!miss) break;
+        if (++spins > (1ll << 28)) __trap();  // never hang the device
+      }
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < kNPL; ++i) {
+        x = cadd(x, u[i]);
+        y = cadd(y, v[i]);
+      }
+      x = warp_sum2(x);
+      y = warp_sum2(y);
+      if (threadIdx.x == 0) {
+        sh[66] = x;
+        sh[67] = y;
+      }
+    }
+    __syncthreads();
+    dot = sh[66];
+    dr = sh[67];
+    return;
+  }
   double2* stage = sh + 68;  // 2*G slots after the block-reduce scratch
   if ((int)threadIdx.x < G) {
     const int k = threadIdx.x;
@@ -350,7 +397,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     const int j = s % m;
     double2 h, d;
     // the drift slot carries data only in the first pass (s <= m-2)
-    gather_sum(slots(s), G, a.pad, red, h, d, do_drift && s < m - 1);
+    gather_sum(slots(s), G, a.pad, a.wg, red, h, d, do_drift && s < m - 1);
     if (do_drift && s < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));  // drift term of X_s = V_s
     if (threadIdx.x == 0) {
       col[j] = cadd(col[j], h);
@@ -433,7 +480,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     }
   }
   double2 hn2, dummy;
-  gather_sum(slots(nsteps), G, a.pad, red, hn2, dummy, false);
+  gather_sum(slots(nsteps), G, a.pad, a.wg, red, hn2, dummy, false);
   const double hlast = sqrt(fmax(hn2.x, 0.0));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
@@ -1063,6 +1110,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.dstatus = dstat.p;
   aa.wcap = wcap;
   aa.pad = pad;
+  // measured per path: warp-0 polling helps the REG path (cfg1 123.9 -> 119.5 ms), hurts STREAM
+  aa.wg = getenv("MDD_ARN_WG") ? atoi(getenv("MDD_ARN_WG")) : (mode == 1 ? 1 : 0);
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
     // NaN-fill the publication slots (0xFF bytes are a NaN pattern)
