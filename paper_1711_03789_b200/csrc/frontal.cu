@@ -569,6 +569,31 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
   }
 }
 
+// Complex-symmetric fronts: F_UP = C A^{-1} = (A^{-1} B)^T = F_PU^T (A^{-1} is
+// symmetric, C = B^T), so the packed F_UP rows of the solve are a transpose
+// of F_PU instead of a second GEMM (8 np^2 nu flops).  One 32x32 tile per CTA
+// through shared memory, coalesced on both sides.
+__global__ void __launch_bounds__(256) k_transpose_up(const int4* __restrict__ tasks,
+                                                      const NodeDev* __restrict__ nodes,
+                                                      double2* __restrict__ fronts) {
+  __shared__ double2 t[32][33];
+  const int4 tk = tasks[blockIdx.x];
+  const NodeDev nd = nodes[tk.x];
+  const int r0 = tk.y, c0 = tk.z, np = nd.np, nu = nd.nu, m = nd.m;
+  const double2* pu = fronts + nd.front_off + np;  // F_PU: np x nu, ld m
+  double2* up = fronts + nd.upk_off;              // packed F_UP: nu x np, ld np
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, r = r0 + tx;  // F_PU[c][r]
+    if (c < np && r < nu) t[k][tx] = pu[(int64_t)c * m + r];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + tx;  // F_UP[r][c] = F_PU[c][r]
+    if (r < nu && c < np) up[(int64_t)r * np + c] = t[tx][k];
+  }
+}
+
 // B_orig rows: front row r (< np), columns np..m -> bbuf (np x nu, row-major)
 __global__ void __launch_bounds__(256) k_copy_b(const int2* __restrict__ tasks, int64_t ntask,
                                                 const NodeDev* __restrict__ nodes,
@@ -774,7 +799,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int2> h_init, h_panel;
   std::vector<int4> h_tile;
   std::vector<int2> h_copyb;
-  std::vector<GemmTask> h_yz, h_s;
+  std::vector<GemmTask> h_yz, h_yzup, h_s;
+  std::vector<int4> h_tr;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
   lev_ent_off.assign(1, 0);
@@ -789,6 +815,8 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   lev_gj_nb.clear();
   std::vector<int32_t> h_gjs;
   lev_yz_off.assign(1, 0);
+  lev_yzup_off.clear();
+  lev_tr_off.assign(1, 0);
   lev_s_off.assign(1, 0);
   int64_t bb_max = 0;
   w_max = 0;
@@ -824,15 +852,22 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
             }
         };
         tiles(h_yz, A, m, nd.bb_off, nu, 1, B, m, np, nu, 0);            // F_PU = -(-A^-1) B_orig
-        tiles(h_yz, C, m, A, m, 0, nd.upk_off, np, nu, np, 0);           // F_UP = -C_orig (-A^-1), packed
+        tiles(h_yzup, C, m, A, m, 0, nd.upk_off, np, nu, np, 0);         // F_UP = -C_orig (-A^-1), packed
         tiles(h_s, C, m, B, m, 0, D, m, nu, nu, 1);                      // F_UU -= C_orig F_PU
+        // symmetric matrices: packed F_UP = F_PU^T, 32x32 transpose tiles
+        for (int r0 = 0; r0 < nu; r0 += 32)
+          for (int c0 = 0; c0 < np; c0 += 32) h_tr.push_back(make_int4(g, r0, c0, 0));
       }
     }
     bb_max = std::max(bb_max, bb);
     lev_init_off.push_back((int64_t)h_init.size());
     lev_copyb_off.push_back((int64_t)h_copyb.size());
+    lev_yzup_off.push_back((int64_t)h_yz.size());
+    h_yz.insert(h_yz.end(), h_yzup.begin(), h_yzup.end());
+    h_yzup.clear();
     lev_yz_off.push_back((int64_t)h_yz.size());
     lev_s_off.push_back((int64_t)h_s.size());
+    lev_tr_off.push_back((int64_t)h_tr.size());
     // small pivot blocks: one k_gj_smem CTA per node instead of the sweeps
     // (k_gj_smem is issue-bound at ~30 instructions per element update; it
     // beats the sweeps for np <= 32 only, measured on the B200)
@@ -895,6 +930,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   panel_tasks.upload(h_panel, s);
   tile_tasks.upload(h_tile, s);
   copyb_tasks.upload(h_copyb, s);
+  tr_tasks.upload(h_tr.empty() ? std::vector<int4>{make_int4(0, 0, 0, 0)} : h_tr, s);
   // one task list: the YZ tiles of every level, then the Schur tiles of every level
   {
     const int64_t nyz = (int64_t)h_yz.size();
@@ -949,7 +985,7 @@ static unsigned gblocks(int64_t n, int bs, int cap) {
 }
 
 
-void FrontPlan::factor(const double2* vals, cudaStream_t s) {
+void FrontPlan::factor(const double2* vals, cudaStream_t s, bool sym) {
   if (nnodes == 0) return;
   k_pivinit<<<gblocks(nnodes, 256, 1024), 256, 0, s>>>(pivstat.p, nnodes);
   CK_LAUNCH(ctx);
@@ -1004,9 +1040,14 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s) {
         CK_LAUNCH(ctx);
       }
     }
-    const int64_t y0 = lev_yz_off[L], ny = lev_yz_off[L + 1] - y0;
-    if (ny) {  // F_PU and F_UP from -A^{-1}
+    const int64_t y0 = lev_yz_off[L], yup = sym ? lev_yzup_off[L] : lev_yz_off[L + 1], ny = yup - y0;
+    if (ny) {  // F_PU (and F_UP unless symmetric) from -A^{-1}
       k_gemm<<<(unsigned)ny, 256, kGemmSmem, s>>>(gemm_tasks.p + y0, fronts.p, bbuf.p);
+      CK_LAUNCH(ctx);
+    }
+    const int64_t r0t = lev_tr_off[L], nt = lev_tr_off[L + 1] - r0t;
+    if (sym && nt) {  // F_UP = F_PU^T into the packed solve layout
+      k_transpose_up<<<(unsigned)nt, dim3(32, 8), 0, s>>>(tr_tasks.p + r0t, nodes.p, fronts.p);
       CK_LAUNCH(ctx);
     }
     const int64_t s0 = lev_s_off[L], nsg = lev_s_off[L + 1] - s0;

@@ -108,6 +108,10 @@ struct FrontPlan {
   DevBuf<GemmTask> gemm_tasks;
   DevBuf<double2> bbuf;
   std::vector<int64_t> lev_copyb_off, lev_yz_off, lev_s_off;
+  // per level: start of the F_UP tiles inside the YZ range; transpose tiles
+  // (symmetric fronts: packed F_UP = F_PU^T, k_transpose_up)
+  std::vector<int64_t> lev_yzup_off, lev_tr_off;
+  DevBuf<int4> tr_tasks;
   DevBuf<int32_t> gmap_abs;            // gather maps as absolute uvec indices (solve)
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
@@ -127,7 +131,8 @@ struct FrontPlan {
   // build from analysed matrices
   void build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf);
   // numeric factorisation from `vals` (complex, indexed by MatrixInput.src)
-  void factor(const double2* vals, cudaStream_t s);
+  // sym: the matrices are complex symmetric (bitwise), F_UP is transposed from F_PU
+  void factor(const double2* vals, cudaStream_t s, bool sym = false);
   // per-matrix pivot ratio check; returns index of the first failing matrix or -1
   int check_pivots(std::string& msg, cudaStream_t s);
   // solve: bloc (ND-ordered local rhs) -> xloc; with v/gidx the local rhs is

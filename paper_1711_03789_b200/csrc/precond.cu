@@ -45,6 +45,10 @@ struct PrecCore {
   FrontPlan coarse;
   std::unique_ptr<mdd_csr> R0p, R0Tp;  // rows / columns in coarse ND order
   std::unique_ptr<mdd_csr> A0;         // assembled coarse Galerkin matrix (coarse pattern)
+  // A_prec entry -> transposed entry (AS/RAS minors), symmetry flag of the last factorisation
+  DevBuf<int32_t> tpos;
+  DevBuf<int> symflag;
+  bool sym = false;
   // non-nested coarse mesh: A0[slot] = sum_t rap_c[t] * A_prec[rap_k[t]], t in [rap_ptr[slot], rap_ptr[slot+1])
   bool rap = false;
   DevBuf<int64_t> rap_ptr;
@@ -680,6 +684,33 @@ static void rap_assemble(PrecCore& c, const mdd_csr* A_prec, cudaStream_t s) {
   CK_LAUNCH(c.ctx);
 }
 
+// bitwise complex symmetry of A_prec (its minors then are too): flag != 0 on
+// any A[i][j] != A[j][i]; tpos maps every entry to its transposed position
+__global__ void k_symcheck(int64_t nnz, const int32_t* __restrict__ tpos, const double2* __restrict__ a,
+                           int* __restrict__ flag) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = tpos[k];
+    if (t < 0) { atomicOr(flag, 1); continue; }
+    const double2 x = a[k], y = a[t];
+    if (__double_as_longlong(x.x) != __double_as_longlong(y.x) ||
+        __double_as_longlong(x.y) != __double_as_longlong(y.y))
+      atomicOr(flag, 1);
+  }
+}
+
+static bool prec_symmetric(PrecCore& c, const mdd_csr* A_prec, cudaStream_t s) {
+  if (c.tpos.n == 0 || getenv("MDD_NO_SYM")) return false;
+  const int64_t nnz = A_prec->pat->nnz;
+  c.symflag.zero(s);
+  k_symcheck<<<nb(std::min<int64_t>(nnz, (int64_t)c.ctx->nsm * 16 * 256), 256), 256, 0, s>>>(
+      nnz, c.tpos.p, reinterpret_cast<const double2*>(A_prec->vals.p), c.symflag.p);
+  CK_LAUNCH(c.ctx);
+  int f = 1;
+  c.symflag.download(&f, 1, s);
+  CK(cudaStreamSynchronize(s));
+  return f == 0;
+}
+
 static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc,
                           int32_t* failed_ctx) {
   PrecCore& c = *P->core;
@@ -690,7 +721,8 @@ static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* 
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
   if (c.local_kind == 0) {
-    c.sub.factor(reinterpret_cast<const double2*>(A_prec->vals.p), s);
+    c.sym = prec_symmetric(c, A_prec, s);
+    c.sub.factor(reinterpret_cast<const double2*>(A_prec->vals.p), s, c.sym);
   } else {
     impras_local_assemble(c, pc, s);
     c.sub.factor(c.loc_vals.p, s);
@@ -757,6 +789,18 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
   // ---- local matrices (patterns + value sources)
   std::vector<MatrixInput> mats(d->nsub);
   if (c.local_kind == 0) {
+    // transposed positions of A_prec's pattern (symmetry check per factorisation)
+    std::vector<int32_t> tp(AP.nnz, -1);
+    for (int64_t i = 0; i < AP.nrow; ++i)
+      for (int32_t k = AP.h_rowptr[i]; k < AP.h_rowptr[i + 1]; ++k) {
+        const int32_t j = AP.h_cols[k];
+        const int32_t* b = AP.h_cols.data() + AP.h_rowptr[j];
+        const int32_t* e = AP.h_cols.data() + AP.h_rowptr[j + 1];
+        const int32_t* it = std::lower_bound(b, e, (int32_t)i);
+        if (it != e && *it == i) tp[k] = (int32_t)(it - AP.h_cols.data());
+      }
+    c.tpos.upload(tp, s);
+    c.symflag.alloc(1);
     // exact minors of A_prec on I_l (precond.py:296-301)
     const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> th;

@@ -186,3 +186,27 @@ def test_larger_cases_vs_oracle(gpu, n, p, layers, nc, leaf):
     rng = np.random.default_rng(n)
     v = rng.standard_normal(s.ndof) + 1j * rng.standard_normal(s.ndof)
     assert rel(st.apply(v), ref.apply(v)) <= 1e-10
+
+
+def test_symmetric_transpose_path_matches_gemm_path(gpu, monkeypatch):
+    """Complex-symmetric A_prec: the packed F_UP of the solve is F_PU^T
+    (k_transpose_up) instead of a second GEMM; MDD_NO_SYM forces the GEMM.
+    Both must agree with each other and with the oracle to rounding."""
+    from paper_1711_03789_b200 import decomp, precond
+
+    prob = _problem(8, 3.0, xi=9.0)
+    d = decomp.build_decomposition(prob.space, 2, 2, coarse_space=_coarse(4))
+    spec = precond.PreconditionerSpec("as", "two", "additive", xi_prec=9.0)
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal(prob.ndof) + 1j * rng.standard_normal(prob.ndof)
+    st_sym = precond.setup(prob, d, spec, lu_cap=None)
+    y_sym = st_sym.apply(v)
+    monkeypatch.setenv("MDD_NO_SYM", "1")
+    st_gemm = precond.setup(prob, d, spec, lu_cap=None)
+    y_gemm = st_gemm.apply(v)
+    assert rel(y_sym, y_gemm) <= 1e-12
+    A = prob.A.to_scipy()
+    R0 = d.coarse.R0
+    ref = O.Schwarz(d.dofs, d.pou, O.minors(A, d.dofs), levels="two", R0=R0, A0=(R0 @ A @ R0.T).tocsc(),
+                    ndof=prob.ndof)
+    assert rel(y_sym, ref.apply(v)) <= 1e-11
