@@ -248,6 +248,9 @@ int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm);
 /* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
  *              levels, sum_local_dofs, coarse_n] */
 int mdd_prec_stats(const mdd_prec* P, double* out8);
+/* 1 if the last factorisation found A_prec bitwise complex symmetric and
+ * formed the packed F_UP blocks as F_PU^T (no second GEMM), else 0 */
+int mdd_prec_symmetric(const mdd_prec* P, int* sym);
 /* refactorise in place (same pattern) from new A_prec values: the numeric part
  * of setup, used by the benchmark's timed step */
 int mdd_prec_refactor(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* prec_coeffs);

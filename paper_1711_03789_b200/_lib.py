@@ -146,6 +146,7 @@ SIGNATURES = {
     ),
     "mdd_element2_matrices": (C.c_int, [_P, _i64, _pd, _pd, _pd]),
     "mdd_free": (None, [C.c_void_p]),
+    "mdd_prec_symmetric": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "mdd_extend_overlap": (
         C.c_int,
         [_i32, _i64, _pi64, _i32, _pi64, _pi64, _i32, C.POINTER(_pi64), C.POINTER(_pi64)],

@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(128) k_assemble_cells(
       const int da = e2d[tet_edges[t * 6 + a]], db = e2d[tet_edges[t * 6 + b]];
       if (da < 0 || db < 0) continue;
       double sv, mv;
-      element_entry(g, sg, a, b, sv, mv);
+      // (a,b) and (b,a) from the same evaluation: the assembled matrices are
+      // bitwise complex symmetric (the factorisation's transpose path relies on it)
+      element_entry(g, sg, min(a, b), max(a, b), sv, mv);
       const int slot = csr_find(rowptr, cols, da, db);
       S[slot] += sv;
       M[slot] += mv;

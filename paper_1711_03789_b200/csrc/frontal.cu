@@ -477,7 +477,8 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
 __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ tasks, double2* __restrict__ fronts,
-                                                 const double2* __restrict__ bbuf) {
+                                                 const double2* __restrict__ bbuf, const int* __restrict__ gate = nullptr) {
+  if (gate && *gate == 0) return;  // F_UP GEMM of a symmetric factorisation: k_transpose_up does it
   extern __shared__ double2 sm[];
   constexpr int LA = kGemmKC + 4, LB = kTile + 2;  // padded leading dimensions
   const GemmTask tk = tasks[blockIdx.x];
@@ -575,7 +576,8 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
 // through shared memory, coalesced on both sides.
 __global__ void __launch_bounds__(256) k_transpose_up(const int4* __restrict__ tasks,
                                                       const NodeDev* __restrict__ nodes,
-                                                      double2* __restrict__ fronts) {
+                                                      double2* __restrict__ fronts, const int* __restrict__ gate) {
+  if (*gate != 0) return;  // not symmetric: the F_UP GEMM ran
   __shared__ double2 t[32][33];
   const int4 tk = tasks[blockIdx.x];
   const NodeDev nd = nodes[tk.x];
@@ -985,7 +987,7 @@ static unsigned gblocks(int64_t n, int bs, int cap) {
 }
 
 
-void FrontPlan::factor(const double2* vals, cudaStream_t s, bool sym) {
+void FrontPlan::factor(const double2* vals, cudaStream_t s, const int* sym_flag) {
   if (nnodes == 0) return;
   k_pivinit<<<gblocks(nnodes, 256, 1024), 256, 0, s>>>(pivstat.p, nnodes);
   CK_LAUNCH(ctx);
@@ -1040,14 +1042,20 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s, bool sym) {
         CK_LAUNCH(ctx);
       }
     }
-    const int64_t y0 = lev_yz_off[L], yup = sym ? lev_yzup_off[L] : lev_yz_off[L + 1], ny = yup - y0;
-    if (ny) {  // F_PU (and F_UP unless symmetric) from -A^{-1}
-      k_gemm<<<(unsigned)ny, 256, kGemmSmem, s>>>(gemm_tasks.p + y0, fronts.p, bbuf.p);
+    // F_PU from -A^{-1}; F_UP by GEMM, or (sym_flag == 0 on the device: the
+    // matrices are bitwise symmetric) as F_PU^T -- decided on the device, no sync
+    const int64_t y0 = lev_yz_off[L], yup = lev_yzup_off[L], y1 = lev_yz_off[L + 1];
+    if (yup > y0) {
+      k_gemm<<<(unsigned)(yup - y0), 256, kGemmSmem, s>>>(gemm_tasks.p + y0, fronts.p, bbuf.p);
+      CK_LAUNCH(ctx);
+    }
+    if (y1 > yup) {
+      k_gemm<<<(unsigned)(y1 - yup), 256, kGemmSmem, s>>>(gemm_tasks.p + yup, fronts.p, bbuf.p, sym_flag);
       CK_LAUNCH(ctx);
     }
     const int64_t r0t = lev_tr_off[L], nt = lev_tr_off[L + 1] - r0t;
-    if (sym && nt) {  // F_UP = F_PU^T into the packed solve layout
-      k_transpose_up<<<(unsigned)nt, dim3(32, 8), 0, s>>>(tr_tasks.p + r0t, nodes.p, fronts.p);
+    if (sym_flag && nt) {
+      k_transpose_up<<<(unsigned)nt, dim3(32, 8), 0, s>>>(tr_tasks.p + r0t, nodes.p, fronts.p, sym_flag);
       CK_LAUNCH(ctx);
     }
     const int64_t s0 = lev_s_off[L], nsg = lev_s_off[L + 1] - s0;

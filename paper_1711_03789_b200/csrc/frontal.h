@@ -131,8 +131,9 @@ struct FrontPlan {
   // build from analysed matrices
   void build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf);
   // numeric factorisation from `vals` (complex, indexed by MatrixInput.src)
-  // sym: the matrices are complex symmetric (bitwise), F_UP is transposed from F_PU
-  void factor(const double2* vals, cudaStream_t s, bool sym = false);
+  // sym_flag (device, may be null): 0 = the matrices are bitwise complex
+  // symmetric, F_UP is transposed from F_PU instead of a second GEMM
+  void factor(const double2* vals, cudaStream_t s, const int* sym_flag = nullptr);
   // per-matrix pivot ratio check; returns index of the first failing matrix or -1
   int check_pivots(std::string& msg, cudaStream_t s);
   // solve: bloc (ND-ordered local rhs) -> xloc; with v/gidx the local rhs is

@@ -48,7 +48,7 @@ struct PrecCore {
   // A_prec entry -> transposed entry (AS/RAS minors), symmetry flag of the last factorisation
   DevBuf<int32_t> tpos;
   DevBuf<int> symflag;
-  bool sym = false;
+  bool sym_checked = false;
   // non-nested coarse mesh: A0[slot] = sum_t rap_c[t] * A_prec[rap_k[t]], t in [rap_ptr[slot], rap_ptr[slot+1])
   bool rap = false;
   DevBuf<int64_t> rap_ptr;
@@ -698,17 +698,16 @@ __global__ void k_symcheck(int64_t nnz, const int32_t* __restrict__ tpos, const 
   }
 }
 
-static bool prec_symmetric(PrecCore& c, const mdd_csr* A_prec, cudaStream_t s) {
-  if (c.tpos.n == 0 || getenv("MDD_NO_SYM")) return false;
+// device-side symmetry flag for the factorisation (no host sync); null when
+// the check does not apply (impras local matrices) or MDD_NO_SYM is set
+static const int* prec_symmetric(PrecCore& c, const mdd_csr* A_prec, cudaStream_t s) {
+  if (c.tpos.n == 0 || getenv("MDD_NO_SYM")) return nullptr;
   const int64_t nnz = A_prec->pat->nnz;
   c.symflag.zero(s);
   k_symcheck<<<nb(std::min<int64_t>(nnz, (int64_t)c.ctx->nsm * 16 * 256), 256), 256, 0, s>>>(
       nnz, c.tpos.p, reinterpret_cast<const double2*>(A_prec->vals.p), c.symflag.p);
   CK_LAUNCH(c.ctx);
-  int f = 1;
-  c.symflag.download(&f, 1, s);
-  CK(cudaStreamSynchronize(s));
-  return f == 0;
+  return c.symflag.p;
 }
 
 static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc,
@@ -721,8 +720,8 @@ static void numeric_setup(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* 
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
   if (c.local_kind == 0) {
-    c.sym = prec_symmetric(c, A_prec, s);
-    c.sub.factor(reinterpret_cast<const double2*>(A_prec->vals.p), s, c.sym);
+    c.sym_checked = prec_symmetric(c, A_prec, s) != nullptr;
+    c.sub.factor(reinterpret_cast<const double2*>(A_prec->vals.p), s, c.sym_checked ? c.symflag.p : nullptr);
   } else {
     impras_local_assemble(c, pc, s);
     c.sub.factor(c.loc_vals.p, s);
@@ -1233,6 +1232,17 @@ int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm) {
 int mdd_prec_stats(const mdd_prec* P, double* out8) {
   MDD_API_BEGIN
   for (int i = 0; i < 8; ++i) out8[i] = P->core->stats[i];
+  MDD_API_END
+}
+
+int mdd_prec_symmetric(const mdd_prec* P, int* sym) {
+  MDD_API_BEGIN
+  int f = 1;
+  if (P->core->sym_checked) {
+    P->core->symflag.download(&f, 1, P->core->ctx->stream);
+    CK(cudaStreamSynchronize(P->core->ctx->stream));
+  }
+  *sym = f == 0 ? 1 : 0;
   MDD_API_END
 }
 

@@ -204,6 +204,16 @@ def test_symmetric_transpose_path_matches_gemm_path(gpu, monkeypatch):
     monkeypatch.setenv("MDD_NO_SYM", "1")
     st_gemm = precond.setup(prob, d, spec, lu_cap=None)
     y_gemm = st_gemm.apply(v)
+    import ctypes
+
+    from paper_1711_03789_b200 import _lib
+
+    flags = []
+    for st in (st_sym, st_gemm):
+        f = ctypes.c_int(-1)
+        _lib.check(_lib.lib.mdd_prec_symmetric(st.handle, ctypes.byref(f)))
+        flags.append(f.value)
+    assert flags == [1, 0]  # the assembled A_prec is bitwise symmetric; MDD_NO_SYM forces the GEMM
     assert rel(y_sym, y_gemm) <= 1e-12
     A = prob.A.to_scipy()
     R0 = d.coarse.R0

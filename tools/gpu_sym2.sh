@@ -1,0 +1,4 @@
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_sym2.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_sym2.log
+timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 > gpurun_out/bench_sym2.json 2> gpurun_out/bench_sym2.err
+MDD_NO_SYM=1 timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 > gpurun_out/bench_nosym2.json 2> /dev/null
