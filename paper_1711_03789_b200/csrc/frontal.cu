@@ -513,6 +513,21 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
 #pragma unroll
     for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
   const int nk = (K + kGemmKC - 1) / kGemmKC;
+  if (tk.mode == 1) {
+    // accumulate mode: pull the output tile's old values toward L2 now, so the
+    // epilogue's read-modify-write does not pay HBM latency after the K loop
+    // (each thread covers its 2x4 blocks' 32-byte row segments)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = r0 + (warp >> 1) * 16 + 8 * i + gid;
+      if (r >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + (warp & 1) * 32 + 8 * j + 2 * tig;
+        if (c < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(Og + (int64_t)r * ldo + c));
+      }
+    }
+  }
   load(0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) {

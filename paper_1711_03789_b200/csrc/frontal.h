@@ -63,6 +63,7 @@ struct LvlTask {
 };
 constexpr int kTSolveTaskElems = 2048;  // factor entries per solve task (32 KB)
 constexpr int kTSolvePrefetch = 500;    // L2 prefetch distance (tasks)
+constexpr int kTSolveMinRows = 1;       // backward tasks: minimum rows per task
 
 struct MatrixInput {
   int32_t n = 0;

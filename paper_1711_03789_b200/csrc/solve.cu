@@ -199,6 +199,9 @@ static int64_t env_int(const char* name, int64_t dflt) {
 
 void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
   const int64_t te = env_int("MDD_TSOLVE_ELEMS", kTSolveTaskElems);
+  // backward tasks gather the node's whole z (m entries) per task: a floor on
+  // the rows per task bounds that overhead for large fronts
+  const int64_t minrows = env_int("MDD_TSOLVE_MINROWS", kTSolveMinRows);
   std::vector<LvlTask> ht;
   lvl_off.assign(1, 0);
   lvl_dcap.clear();
@@ -209,7 +212,8 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
       const NodeDev& nd = h_nodes[g];
       const int len = kind == 0 ? nd.np : nd.m;
       const int nrows = kind == 0 ? nd.nu : nd.np;
-      const int rows = (int)std::max<int64_t>(1, len > 0 ? te / len : te);
+      int rows = (int)std::max<int64_t>(1, len > 0 ? te / len : te);
+      if (kind == 1) rows = (int)std::max<int64_t>(rows, std::min<int64_t>(minrows, (200 * 1024 / 16 - len) / std::max(1, len)));
       int r = 0;
       do {  // a zero-row forward task still assembles fp (fpst) for its node
         const int r1 = std::min(nrows, r + rows);
