@@ -684,6 +684,9 @@ __global__ void __launch_bounds__(256) k_maxpy(int64_t nl, int64_t ldv, const do
 __global__ void k_cgs_tail(ArnoldiArgs a, const double2* h1, const double2* h2, const double2* nrm,
                            const double2* dr, int do_drift, double2* col, double* scal) {
   if (threadIdx.x || blockIdx.x) return;
+  // the host loop runs one iteration ahead of its convergence check: an
+  // iteration enqueued after convergence must leave the converged state alone
+  if (a.dstatus[0]) return;
   const int m = *a.iter + 1;
   for (int j = 0; j < m; ++j) col[j] = cadd(h1[j], h2[j]);
   const double hlast = sqrt(fmax(nrm[0].x, 0.0));
@@ -895,6 +898,18 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   aa.check_drift = cfg->check_drift;
   aa.iter = diter.p;
   aa.dstatus = dstat.p;
+  // convergence is checked one iteration behind (host-mapped status written by
+  // the tail kernel), so the host enqueues iteration it+1 while the device
+  // still runs iteration it instead of idling through every enqueue
+  if (!ctx->mapped_status) CK(cudaHostAlloc(&ctx->mapped_status, sizeof(int) * 4, cudaHostAllocMapped));
+  volatile int* hst = ctx->mapped_status;
+  int* hst_dev = nullptr;
+  CK(cudaHostGetDevicePointer(&hst_dev, (void*)ctx->mapped_status, 0));
+  hst[0] = 0;
+  aa.hstatus = hst_dev;
+  cudaEvent_t itev[2];
+  CK(cudaEventCreateWithFlags(&itev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&itev[1], cudaEventDisableTiming));
   int st[4] = {0, 0, 0, 0};
   for (int it = 1; it <= maxit; ++it) {
     const int m = it - 1;  // newest basis vector
@@ -913,10 +928,16 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     CK_LAUNCH(ctx);
     k_vscale<<<gs_grid(chunk), 256, 0, s>>>(chunk, w.p, scal.p, V.p + (int64_t)(m + 1) * chunk);
     CK_LAUNCH(ctx);
-    dstat.download(st, 4, s);
-    CK(cudaStreamSynchronize(s));
-    if (st[0]) break;
+    CK(cudaEventRecord(itev[it & 1], s));
+    if (it >= 2) {  // iteration it-1 finished: its tail has published the status
+      CK(cudaEventSynchronize(itev[(it - 1) & 1]));
+      if (hst[0]) break;
+    }
   }
+  cudaEventDestroy(itev[0]);
+  cudaEventDestroy(itev[1]);
+  dstat.download(st, 4, s);
+  CK(cudaStreamSynchronize(s));
   const int m = st[2];
   const bool done = st[0] != 0;
   const bool breakdown = done && st[1];
