@@ -235,8 +235,13 @@ static void launch_spmv(mdd_ctx* ctx, const mdd_csr* A, int64_t row0, int64_t nr
     if (cp) k_spmv_u<true, 8, 4><<<grid(8), 256, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
     else k_spmv_u<false, 8, 4><<<grid(8), 256, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
   } else {
-    if (cp) k_spmv_u<true, 4, 4><<<grid(4), 256, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
-    else k_spmv_u<false, 4, 4><<<grid(4), 256, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
+    // 4 lanes x 5 nonzeros: the edge-element rows (7-19 nonzeros) take one
+    // pass; 128-thread blocks (measured on cfg1's A inside GMRES: 8.52 -> 7.82 ms
+    // per 201 calls, 56% -> 61% of HBM; standalone 4.42 -> 4.71 TB/s; swept
+    // 2x8, 8x2, 4x4, 4x5)
+    const unsigned g128 = (unsigned)((nrow * 4 + 127) / 128);
+    if (cp) k_spmv_u<true, 4, 5><<<g128, 128, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
+    else k_spmv_u<false, 4, 5><<<g128, 128, 0, s>>>(nrow, rp, cl, va, x, y, alpha, beta, z);
   }
   CK_LAUNCH(ctx);
 }
