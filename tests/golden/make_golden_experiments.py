@@ -1,0 +1,64 @@
+"""Golden CSV tables for the experiments driver, produced by running the
+REFERENCE's own ``maxwelldd.experiments.run_table`` (experiments.py:391-467).
+
+    python tests/golden/make_golden_experiments.py   # ~1 minute, writes experiments.json
+
+Needs /root/reference (read-only) in this container; the JSON is committed so
+the GPU box can compare the device path's tables against it.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from maxwelldd.experiments import config_from_preset, run_table  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+TINY = {"k_list": "2", "fine_list": "4", "sub_list": "2", "coarse_list": "2", "overlap_layers": "1",
+        "preconditioners": "as2,as1", "times": "false", "seed": "5"}
+
+# name -> (preset, overrides); the shapes follow the reference's own test_experiments.py cases,
+# plus one row per preconditioner family/correction and the table3/table4 settings
+CASES = {
+    "tiny": (None, dict(TINY)),
+    "tiny_seed6": (None, {**TINY, "seed": "6"}),
+    "single_subdomain": (None, {"k_list": "2", "fine_list": "2", "sub_list": "1", "coarse_rule": "none",
+                                "overlap_layers": "1", "preconditioners": "as1", "times": "false"}),
+    "heterogeneous": (None, {"k_list": "2", "fine_list": "4", "sub_list": "2", "coarse_list": "2",
+                             "overlap_layers": "1", "preconditioners": "imphras,impras1",
+                             "heterogeneity": "inclusion", "incl_box": "0,1,0,1,0.25,0.75",
+                             "incl_sigma_over_k": "0.0", "bg_sigma_over_k": "1.0", "xi_prob": "zero",
+                             "xi_prec": "zero", "times": "false"}),
+    "maxit2": (None, {**TINY, "preconditioners": "as1", "gmres_maxit": "2", "xi_prob": "zero",
+                      "xi_prec": "k2"}),
+    "table6_small": ("table6", {"k_list": "3,4", "fine_list": "6,8", "sub_list": "2,2", "coarse_list": "2,2",
+                                "times": "false"}),
+    "table3_small": ("table3", {"k_list": "4", "fine_list": "8", "sub_list": "2", "coarse_list": "2",
+                                "times": "false"}),
+    "table4_small": ("table4", {"k_list": "4", "fine_list": "8", "sub_list": "2", "coarse_list": "2",
+                                "times": "false"}),
+    "impedance_all": (None, {"k_list": "3", "fine_list": "6", "sub_list": "2", "coarse_list": "3",
+                             "overlap_layers": "1",
+                             "preconditioners": "impras1,impras2,imphras,impadef1,as-h,as-adef1",
+                             "times": "false", "seed": "11"}),
+}
+
+
+def main():
+    out = {}
+    for name, (preset, overrides) in CASES.items():
+        cfg = config_from_preset(preset, None, overrides)
+        _, csv_text = run_table(cfg)
+        out[name] = {"preset": preset, "overrides": overrides, "csv": csv_text}
+        print(name, csv_text.count("\n") - 1, "rows")
+    with open(os.path.join(HERE, "experiments.json"), "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
