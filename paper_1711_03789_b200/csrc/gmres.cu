@@ -261,13 +261,41 @@ __device__ __forceinline__ double2 caxmy(double2 w, double2 h, double2 v) {  // 
 
 // Complex Givens update of Hessenberg column m-1 (krylov.py:162-187), residual
 // history clamp and loop status; one thread.  col[0..m] holds the new column.
-__device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool breakdown) {
-  for (int j = 0; j < m - 1; ++j) {
-    const double2 csj = a.cs[j], snj = a.sn[j];
-    const double2 t = cadd(cmul(csj, col[j]), cmul(snj, col[j + 1]));
-    col[j + 1] = cadd(cmul(cneg(cconj(snj)), col[j]), cmul(csj, col[j + 1]));
-    col[j] = t;
+// The rotations are a dependent chain; their operands (cs, sn and the
+// untouched col[j+1]) are loaded kTailBlk at a time into registers ahead of
+// the chain, because col may alias the global arrays as far as the compiler
+// knows and a load per step would otherwise wait out a full memory latency
+// (m x ~0.5 us at m = 200).  Same operations in the same order as the
+// straight loop: bitwise identical.
+constexpr int kTailBlk = 16;
+__device__ __forceinline__ void tail_rotate(const double2* cs, const double2* snv, double2* col, int m) {
+  double2 cur = col[0];
+  for (int j0 = 0; j0 < m - 1; j0 += kTailBlk) {
+    const int nb = min(kTailBlk, m - 1 - j0);
+    double2 c[kTailBlk], sn[kTailBlk], nx[kTailBlk];
+#pragma unroll
+    for (int q = 0; q < kTailBlk; ++q) {
+      if (q < nb) {
+        c[q] = cs[j0 + q];
+        sn[q] = snv[j0 + q];
+        nx[q] = col[j0 + q + 1];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kTailBlk; ++q) {
+      if (q < nb) {
+        const double2 t = cadd(cmul(c[q], cur), cmul(sn[q], nx[q]));
+        cur = cadd(cmul(cneg(cconj(sn[q])), cur), cmul(c[q], nx[q]));
+        col[j0 + q] = t;
+      }
+    }
   }
+  if (m >= 2) col[m - 1] = cur;
+}
+
+// New rotation m-1, rhs g, history clamp and loop status, after the stored
+// rotations were applied to col; returns the final H(m-1, m-1).
+__device__ double2 tail_finish(const ArnoldiArgs& a, const double2* col, int m, bool breakdown) {
   const double am1 = hypot(col[m - 1].x, col[m - 1].y);
   const double am = hypot(col[m].x, col[m].y);
   const double denom = hypot(am1, am);
@@ -284,10 +312,7 @@ __device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool bre
   }
   a.cs[m - 1] = csm;
   a.sn[m - 1] = snm;
-  double2* Hc = a.H + (int64_t)(m - 1) * (a.maxit + 1);
-  for (int j = 0; j <= m; ++j) Hc[j] = col[j];
-  Hc[m - 1] = cadd(cmul(csm, col[m - 1]), cmul(snm, col[m]));
-  Hc[m] = make_double2(0.0, 0.0);
+  const double2 hmm = cadd(cmul(csm, col[m - 1]), cmul(snm, col[m]));
   const double2 gm1 = a.g[m - 1];
   a.g[m] = cmul(cneg(cconj(snm)), gm1);
   a.g[m - 1] = cmul(csm, gm1);
@@ -306,6 +331,23 @@ __device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool bre
     __threadfence_system();
   }
   if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
+  return hmm;
+}
+
+__device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool breakdown) {
+  tail_rotate(a.cs, a.sn, col, m);
+  double2* Hc = a.H + (int64_t)(m - 1) * (a.maxit + 1);
+  for (int j0 = 0; j0 <= m; j0 += kTailBlk) {
+    double2 t[kTailBlk];
+#pragma unroll
+    for (int q = 0; q < kTailBlk; ++q)
+      if (j0 + q <= m) t[q] = col[j0 + q];
+#pragma unroll
+    for (int q = 0; q < kTailBlk; ++q)
+      if (j0 + q <= m) Hc[j0 + q] = t[q];
+  }
+  Hc[m - 1] = tail_finish(a, col, m, breakdown);
+  Hc[m] = make_double2(0.0, 0.0);
 }
 
 // MODE 1 (REG): unweighted, every CTA slice fits in registers (slice <=
@@ -678,30 +720,195 @@ __global__ void __launch_bounds__(256) k_maxpy(int64_t nl, int64_t ldv, const do
   }
 }
 
+// Row-tiled CGS2 passes: three sweeps over the basis per iteration instead of
+// four.  A CTA stages a tile of kCgsRows rows of all nv basis vectors (and of
+// w) in shared memory with cp.async, two tiles in flight, so each basis
+// element is read from HBM once per pass:
+//   kProj    : partial h_j = conj(V_j) . w      (+ drift conj(V_j) . V_{nv-1}, j < nd)
+//   kSubProj : w -= V h;  partial h_j = conj(V_j) . w   (the update and the
+//              reorthogonalisation dots share one read of the tile)
+//   kSubNorm : w -= V h;  partial |w|^2
+// Partials land in partial[k*G + cta] (k-major, CTA order) for k_colsum; the
+// per-row and per-CTA summation orders are fixed, so reruns are bitwise
+// identical.  Rows of the tail tile beyond nl are zero-filled.
+constexpr int kCgsThreads = 256;
+constexpr int kCgsMaxNv = 2 * kCgsThreads;  // dots: thread t owns basis vectors t and t + 256
+enum CgsMode { kProj = 0, kSubProj = 1, kSubNorm = 2 };
+
+// tile of R rows: nv vectors at a padded pitch of R+1 double2 (conflict-free column reads) + w
+__host__ __device__ constexpr size_t cgs_tile_elems(int nv, int R) { return (size_t)nv * (R + 1) + R; }
+static size_t cgs_smem_bytes(int nv, int R, int ns) {
+  return sizeof(double2) * (ns * cgs_tile_elems(nv, R) + (size_t)kCgsThreads + 64);
+}
+
+__device__ __forceinline__ uint32_t smem_u32_g(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32_g(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+template <int MODE, int R>
+__global__ void __launch_bounds__(kCgsThreads) k_cgs_tile(int64_t nl, int64_t ldv, const double2* __restrict__ V,
+                                                          int nv, const double2* __restrict__ h,
+                                                          double2* __restrict__ w, int nd,
+                                                          double2* __restrict__ partial, int ns) {
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x, G = gridDim.x;
+  const size_t TE = cgs_tile_elems(nv, R);
+  constexpr int kCgsRows = R, kCgsPitch = R + 1;
+  double2* red = sm + ns * TE;  // [kCgsThreads/kCgsRows][kCgsRows]
+  const int64_t ntiles = (nl + kCgsRows - 1) / kCgsRows;
+  auto issue = [&](int64_t tile, int buf) {
+    double2* Vs = sm + buf * TE;
+    double2* ws = Vs + (size_t)nv * kCgsPitch;
+    const int64_t row0 = tile * kCgsRows;
+    const int total = nv * kCgsRows;
+    for (int e = tid; e < total; e += kCgsThreads) {
+      const int j = e / kCgsRows, r = e % kCgsRows;
+      const int64_t i = row0 + r;
+      const bool ok = i < nl;
+      cp_async16(Vs + j * kCgsPitch + r, V + (int64_t)j * ldv + (ok ? i : 0), ok);
+    }
+    if (tid < kCgsRows) {
+      const int64_t i = row0 + tid;
+      cp_async16(ws + tid, w + (i < nl ? i : 0), i < nl);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, dacc0 = acc0, dacc1 = acc0, nacc = acc0;
+  const int r = tid % kCgsRows, grp = tid / kCgsRows;
+  constexpr int NG = kCgsThreads / kCgsRows;
+  // ns-stage ring (ns = 2 or 3): one commit group per tile slot, empty past the end
+  int64_t tile = blockIdx.x;
+  for (int q = 0; q < ns - 1; ++q) {
+    if (tile + (int64_t)q * G < ntiles) issue(tile + (int64_t)q * G, q);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int it = 0; tile < ntiles; ++it, tile += G) {
+    const int buf = it % ns;
+    const int64_t tn = tile + (int64_t)(ns - 1) * G;
+    if (tn < ntiles) issue(tn, (it + ns - 1) % ns);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    if (ns == 3) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    double2* Vs = sm + buf * TE;
+    double2* ws = Vs + (size_t)nv * kCgsPitch;
+    if (MODE != kProj) {
+      // w_r -= sum_j h_j V_j[r]: NG groups of kCgsRows threads, combined in group order
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = grp; j < nv; j += NG) s = cfma(__ldg(h + j), Vs[j * kCgsPitch + r], s);
+      red[grp * kCgsRows + r] = s;
+      __syncthreads();
+      if (tid < kCgsRows) {
+        double2 t = red[tid];
+#pragma unroll
+        for (int g = 1; g < NG; ++g) t = cadd(t, red[g * kCgsRows + tid]);
+        const double2 wn = csub(ws[tid], t);
+        ws[tid] = wn;
+        const int64_t i = tile * kCgsRows + tid;
+        if (i < nl) w[i] = wn;
+        if (MODE == kSubNorm) nacc.x += wn.x * wn.x + wn.y * wn.y;
+      }
+      __syncthreads();
+    }
+    if (MODE != kSubNorm) {
+      // h_j partials over the tile's rows in row order; thread t owns j = t, t + 256
+      for (int q = 0; q < 2; ++q) {
+        const int j = tid + q * kCgsThreads;
+        if (j >= nv) break;
+        const double2* vj = Vs + j * kCgsPitch;
+        double2 a = q ? acc1 : acc0;
+#pragma unroll
+        for (int rr = 0; rr < kCgsRows; ++rr) a = cdotc_acc(a, vj[rr], ws[rr]);
+        if (q) acc1 = a; else acc0 = a;
+        if (MODE == kProj && j < nd) {
+          const double2* vm = Vs + (nv - 1) * kCgsPitch;
+          double2 d = q ? dacc1 : dacc0;
+#pragma unroll
+          for (int rr = 0; rr < kCgsRows; ++rr) d = cdotc_acc(d, vj[rr], vm[rr]);
+          if (q) dacc1 = d; else dacc0 = d;
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's issue
+  }
+  if constexpr (MODE == kSubNorm) {
+    const double2 t = block_sum2(nacc, red);
+    if (tid == 0) partial[blockIdx.x] = t;
+  } else {
+    for (int q = 0; q < 2; ++q) {
+      const int j = tid + q * kCgsThreads;
+      if (j < nv) partial[(int64_t)j * G + blockIdx.x] = q ? acc1 : acc0;
+      if (MODE == kProj && j < nd) partial[(int64_t)(nv + j) * G + blockIdx.x] = q ? dacc1 : dacc0;
+    }
+  }
+}
+
 // Column m-1 of H from the two projections and the norm, drift of V_{m-1},
-// breakdown test, Givens update (arnoldi_tail).  One thread.  scal[0] = hlast,
-// scal[1] = 1 on breakdown (k_vscale then leaves V_m alone).
-__global__ void k_cgs_tail(ArnoldiArgs a, const double2* h1, const double2* h2, const double2* nrm,
-                           const double2* dr, int do_drift, double2* col, double* scal) {
-  if (threadIdx.x || blockIdx.x) return;
+// breakdown test, Givens update.  scal[0] = hlast, scal[1] = 1 on breakdown
+// (k_vscale then leaves V_m alone).
+constexpr int kTailThreads = 256;
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    r = warp_max(r);
+    if (threadIdx.x == 0) sh[32] = r;
+  }
+  __syncthreads();
+  return sh[32];
+}
+// One CTA of kTailThreads: the column sums and maxima in parallel; col, cs
+// and sn staged in shared memory (cap = entries that fit, else global), so
+// thread 0 runs the Givens chain off shared memory; H column copied by all.
+__global__ void __launch_bounds__(kTailThreads) k_cgs_tail(ArnoldiArgs a, const double2* h1, const double2* h2,
+                                                           const double2* nrm, const double2* dr, int do_drift,
+                                                           double2* colg, double* scal, int cap) {
+  extern __shared__ double2 tsm[];
+  __shared__ double shm[40];
+  __shared__ double2 hmm_s;
+  if (blockIdx.x) return;
   // the host loop runs one iteration ahead of its convergence check: an
   // iteration enqueued after convergence must leave the converged state alone
   if (a.dstatus[0]) return;
   const int m = *a.iter + 1;
-  for (int j = 0; j < m; ++j) col[j] = cadd(h1[j], h2[j]);
+  const bool staged = m + 1 <= cap;
+  double2* col = staged ? tsm : colg;
+  double2* css = staged ? tsm + cap : a.cs;
+  double2* sns = staged ? tsm + 2 * cap : a.sn;
   const double hlast = sqrt(fmax(nrm[0].x, 0.0));
-  col[m] = make_double2(hlast, 0.0);
-  double cmax = 0.0;
-  for (int j = 0; j <= m; ++j) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
-  const bool breakdown = hlast <= 1e-13 * cmax;
-  if (do_drift && m >= 2) {
-    double dmax = 0.0;
-    for (int j = 0; j < m - 1; ++j) dmax = fmax(dmax, hypot(dr[j].x, dr[j].y));
-    a.drift[m - 1] = dmax;
+  double cm = 0.0, dm = 0.0;
+  for (int j = threadIdx.x; j <= m; j += blockDim.x) {
+    const double2 c = j < m ? cadd(h1[j], h2[j]) : make_double2(hlast, 0.0);
+    col[j] = c;
+    if (staged && j < m - 1) {
+      css[j] = a.cs[j];
+      sns[j] = a.sn[j];
+    }
+    cm = fmax(cm, hypot(c.x, c.y));
+    if (do_drift && j < m - 1) dm = fmax(dm, hypot(dr[j].x, dr[j].y));
   }
-  scal[0] = hlast;
-  scal[1] = breakdown ? 1.0 : 0.0;
-  arnoldi_tail(a, col, m, breakdown);
+  const double cmax = block_max(cm, shm);
+  const double dmax = block_max(dm, shm);
+  __syncthreads();  // col, cs, sn visible to thread 0
+  const bool breakdown = hlast <= 1e-13 * cmax;
+  if (threadIdx.x == 0) {
+    if (do_drift && m >= 2) a.drift[m - 1] = dmax;
+    scal[0] = hlast;
+    scal[1] = breakdown ? 1.0 : 0.0;
+    tail_rotate(css, sns, col, m);
+    hmm_s = tail_finish(a, col, m, breakdown);
+  }
+  __syncthreads();
+  double2* Hc = a.H + (int64_t)(m - 1) * (a.maxit + 1);
+  for (int j = threadIdx.x; j <= m; j += blockDim.x)
+    Hc[j] = j == m ? make_double2(0.0, 0.0) : j == m - 1 ? hmm_s : col[j];
 }
 
 __global__ void k_vscale(int64_t nl, const double2* __restrict__ w, const double* __restrict__ scal,
@@ -777,7 +984,27 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   DevBuf<double2> V((size_t)(maxit + 1) * chunk), w(chunk), t(chunk), full((size_t)N * chunk), z(n), bfull,
       x0full, u(chunk);
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2 * ctx->nsm, (nl + 511) / 512));
-  DevBuf<double2> partial((size_t)(2 * maxit + 2) * G), hb(2 * maxit + 2), h2(maxit + 1), nrm(1),
+  // row-tiled passes (k_cgs_tile): 3 sweeps over the basis per iteration; MDD_CGS_FUSED=0 keeps
+  // the 4-sweep k_mdot/k_maxpy sequence
+  const bool fused_env = !getenv("MDD_CGS_FUSED") || atoi(getenv("MDD_CGS_FUSED")) != 0;
+  constexpr size_t kCgsSmemMax = 227 * 1024;
+  // 16-row tiles (256 B per basis vector per tile); MDD_CGS_ROWS=8 halves the tile (measured slower:
+  // cfg1 411 vs 393 ms/step)
+  // two tiles in flight (2 CTAs per SM at cfg1's basis sizes); MDD_CGS_STAGES=3 triples the ring
+  // where it fits (measured slower: 1 CTA per SM, cfg1 414 vs 397 ms/step)
+  static const int cgs_stages = getenv("MDD_CGS_STAGES") ? atoi(getenv("MDD_CGS_STAGES")) : 2;
+  static const int cgs_rows = getenv("MDD_CGS_ROWS") && atoi(getenv("MDD_CGS_ROWS")) == 8 ? 8 : 16;
+  const int64_t ntiles = (nl + cgs_rows - 1) / cgs_rows;
+  const int Gt_max = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->nsm * 8, ntiles));
+  if (fused_env) {
+    CK(cudaFuncSetAttribute(k_cgs_tile<kProj, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs_tile<kSubProj, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs_tile<kSubNorm, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs_tile<kProj, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs_tile<kSubProj, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+    CK(cudaFuncSetAttribute(k_cgs_tile<kSubNorm, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCgsSmemMax));
+  }
+  DevBuf<double2> partial((size_t)(2 * maxit + 2) * std::max(G, Gt_max)), hb(2 * maxit + 2), h2(maxit + 1), nrm(1),
       col(maxit + 2);
   DevBuf<double2> H((size_t)(maxit + 1) * maxit), cs(maxit), sn(maxit), g(maxit + 1), y(maxit);
   DevBuf<double> hist(maxit + 1), dbeta(1), ddrift(maxit + 1), scal(2);
@@ -917,6 +1144,31 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     comm_allgather_z(dist ? comm : nullptr, vm, full.p, chunk, s);
     op(full.p, w.p);
     const int nd = (cfg->check_drift && m >= 1) ? m : 0;
+    const int nv = m + 1;
+    if (fused_env && nv <= kCgsMaxNv && cgs_smem_bytes(nv, cgs_rows, 2) <= kCgsSmemMax) {
+      const int ns = cgs_stages >= 3 && cgs_smem_bytes(nv, cgs_rows, 3) <= kCgsSmemMax ? 3 : 2;
+      const size_t sm = cgs_smem_bytes(nv, cgs_rows, ns);
+      const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (sm + 1024))));
+      const int Gt = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->nsm * per_sm, ntiles));
+      auto colsum = [&](int nk, double2* out) {
+        k_colsum<<<(unsigned)((nk + 7) / 8), 256, 0, s>>>(partial.p, Gt, nk, out);
+        CK_LAUNCH(ctx);
+        allreduce(out, nk);
+      };
+      auto pass = [&](auto kern, const double2* hh, int ndd) {
+        kern<<<Gt, kCgsThreads, sm, s>>>(nl, chunk, V.p, nv, hh, w.p, ndd, partial.p, ns);
+        CK_LAUNCH(ctx);
+      };
+      if (cgs_rows == 16) pass(k_cgs_tile<kProj, 16>, nullptr, nd);
+      else pass(k_cgs_tile<kProj, 8>, nullptr, nd);
+      colsum(nv + nd, hb.p);  // pass 1 (+ drift of V_m)
+      if (cgs_rows == 16) pass(k_cgs_tile<kSubProj, 16>, hb.p, 0);
+      else pass(k_cgs_tile<kSubProj, 8>, hb.p, 0);
+      colsum(nv, h2.p);  // pass 2 projections, after the pass-1 update
+      if (cgs_rows == 16) pass(k_cgs_tile<kSubNorm, 16>, h2.p, 0);
+      else pass(k_cgs_tile<kSubNorm, 8>, h2.p, 0);
+      colsum(1, nrm.p);
+    } else {
     dots(V.p, m + 1, w.p, vm, nd, hb.p);  // pass 1 (+ drift of V_m)
     k_maxpy<<<gs_grid(chunk), 256, sizeof(double2) * (m + 1), s>>>(nl, chunk, V.p, m + 1, hb.p, w.p);
     CK_LAUNCH(ctx);
@@ -924,7 +1176,10 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     k_maxpy<<<gs_grid(chunk), 256, sizeof(double2) * (m + 1), s>>>(nl, chunk, V.p, m + 1, h2.p, w.p);
     CK_LAUNCH(ctx);
     dots(w.p, 1, w.p, nullptr, 0, nrm.p);
-    k_cgs_tail<<<1, 32, 0, s>>>(aa, hb.p, h2.p, nrm.p, hb.p + m + 1, nd > 0 ? 1 : 0, col.p, scal.p);
+    }
+    const int tcap = (it + 1) * 3 * (int)sizeof(double2) <= 48 * 1024 ? it + 1 : 0;
+    k_cgs_tail<<<1, kTailThreads, sizeof(double2) * 3 * tcap, s>>>(aa, hb.p, h2.p, nrm.p, hb.p + m + 1,
+                                                                  nd > 0 ? 1 : 0, col.p, scal.p, tcap);
     CK_LAUNCH(ctx);
     k_vscale<<<gs_grid(chunk), 256, 0, s>>>(chunk, w.p, scal.p, V.p + (int64_t)(m + 1) * chunk);
     CK_LAUNCH(ctx);

@@ -1,0 +1,9 @@
+timeout 900 python -m pytest tests/test_gpu_gmres.py tests/test_gpu_distributed.py -x -q > gpurun_out/c3_pytest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/c3_pytest.log
+for R in 8 16; do
+MDD_CGS_ROWS=$R timeout 600 python bench.py --no-cpu --steps 3 --warmup 3 --ortho cgs2 > gpurun_out/c3_bench_cgs_r$R.json 2> gpurun_out/c3_bench_cgs_r$R.err
+done
+MDD_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:"k_cgs|k_colsum|k_vscale|k_mdot|k_maxpy" --launch-skip 1400 -c 24 --csv --log-file gpurun_out/c3_launches.csv \
+  python bench.py --no-cpu --steps 1 --warmup 0 --ortho cgs2 > gpurun_out/c3_ncu.log 2>&1
+python tools/ncu_table.py gpurun_out/c3_launches.csv > gpurun_out/c3_launches_table.txt
