@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -74,8 +75,8 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
 }
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s) {
   if (!c || !c->comm) {
-    if (send != recv)
-      CK(cudaMemcpyAsync(recv, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
+    double2* dst = recv + (c && c->emulated ? (int64_t)c->rank * per_rank : 0);
+    if (send != dst) CK(cudaMemcpyAsync(dst, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
     return;
   }
   nccl_check(nccl().allGather(send, recv, (size_t)(2 * per_rank), ncclFloat64, static_cast<ncclComm_t>(c->comm), s),
@@ -101,11 +102,14 @@ int mdd_comm_create(mdd_ctx* ctx, int nranks, int rank, const char* id128, mdd_c
   CK(cudaSetDevice(ctx->device));
   // id128 == NULL: a single-rank communicator without NCCL (all collectives
   // are identities); with an id, NCCL is initialised even for one rank
-  if (nranks > 1 && !id128) fail(MDD_EINVAL, "comm: a unique id is required for more than one rank");
+  const char* emu = getenv("MDD_COMM_EMULATE");
+  const bool emulate = nranks > 1 && !id128 && emu && atoi(emu) != 0;
+  if (nranks > 1 && !id128 && !emulate) fail(MDD_EINVAL, "comm: a unique id is required for more than one rank");
   std::unique_ptr<mdd_comm> c(new mdd_comm());
   c->ctx = ctx;
   c->nranks = nranks;
   c->rank = rank;
+  c->emulated = emulate;
   if (id128) {
     ncclUniqueId id;
     memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);

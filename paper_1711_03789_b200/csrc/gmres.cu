@@ -323,12 +323,10 @@ __device__ double2 tail_finish(const ArnoldiArgs& a, const double2* col, int m, 
   a.dstatus[0] = done;
   a.dstatus[1] = breakdown ? 1 : 0;
   a.dstatus[2] = m;
-  if (a.hstatus) {
+  if (a.hstatus) {  // host-mapped; every host reader first synchronises with this kernel (no fences)
     a.hstatus[1] = breakdown ? 1 : 0;
     a.hstatus[2] = m;
-    __threadfence_system();
     a.hstatus[0] = done;
-    __threadfence_system();
   }
   if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
   return hmm;
@@ -1016,6 +1014,7 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   diter.zero(s);
   dstat.zero(s);
   V.zero(s);  // padding rows of the last block stay zero
+  full.zero(s);
   {
     std::vector<double> nanv(maxit + 1, NAN);
     ddrift.upload(nanv, s);

@@ -187,6 +187,11 @@ struct mdd_comm {
   mdd_ctx* ctx = nullptr;
   void* comm = nullptr;
   int nranks = 1, rank = 0;
+  // MDD_COMM_EMULATE=1 and no unique id: rank `rank` of `nranks` runs alone on
+  // this GPU with every collective replaced by its local part (allreduce: none;
+  // allgather: own block only).  Per-rank TIMING of the sharded path with one
+  // GPU; the numbers it computes are not the solve's (tools/rank_emulation.py).
+  bool emulated = false;
 };
 
 namespace mdd {
@@ -195,7 +200,7 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s);
 // recv[r*per_rank ...] = send of rank r (stream-ordered); one rank: copy
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s);
 // true when collectives go through NCCL (any rank count)
-inline bool comm_active(const mdd_comm* c) { return c && c->comm; }
+inline bool comm_active(const mdd_comm* c) { return c && (c->comm || c->emulated); }
 
 // element geometry + 6x6 stiffness / mass (fem.py:154-195); shared by the
 // global assembly, the impras local assembly and the coarse Galerkin kernel

@@ -80,10 +80,28 @@ class Communicator:
     ``force_nccl`` initialises NCCL even for a single rank (used by the tests
     to exercise the allreduce path on one GPU)."""
 
-    def __init__(self, ctx=None, group=None, force_nccl: bool = False):
+    def __init__(self, ctx=None, group=None, force_nccl: bool = False, emulate=None):
         import torch.distributed as dist
 
         self.ctx = ctx or _lib.get_context()
+        if emulate is not None:
+            # (rank, nranks) run alone on this GPU, collectives reduced to their local part:
+            # per-rank timing only (libmdd MDD_COMM_EMULATE, tools/rank_emulation.py)
+            import os
+
+            self.rank, self.nranks = int(emulate[0]), int(emulate[1])
+            h = C.c_void_p()
+            old = os.environ.get("MDD_COMM_EMULATE")
+            os.environ["MDD_COMM_EMULATE"] = "1"
+            try:
+                _lib.check(_lib.lib.mdd_comm_create(self.ctx.handle, self.nranks, self.rank, None, C.byref(h)))
+            finally:
+                if old is None:
+                    del os.environ["MDD_COMM_EMULATE"]
+                else:
+                    os.environ["MDD_COMM_EMULATE"] = old
+            self.handle = h
+            return
         if dist.is_available() and dist.is_initialized():
             self.rank = dist.get_rank(group)
             self.nranks = dist.get_world_size(group)
