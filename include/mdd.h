@@ -244,6 +244,15 @@ int mdd_comm_create(mdd_ctx* ctx, int nranks, int rank, const char* id128, mdd_c
 void mdd_comm_destroy(mdd_comm* c);
 int mdd_comm_info(const mdd_comm* c, int* nranks, int* rank);
 int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm);
+/* Loopback group (test infrastructure for the multi-rank path on ONE GPU;
+ * no reference counterpart): nranks (<= 8) host threads, each with its own
+ * context on the same device, join one group; every collective synchronises
+ * the caller's stream, meets the other ranks at a host barrier and moves the
+ * data with device copies (allreduce: each rank sums all ranks' buffers in
+ * rank order).  Kernels never wait on other ranks, only host threads do. */
+int mdd_comm_loopback_group(int nranks, void** group_out);
+void mdd_comm_loopback_group_free(void* group);
+int mdd_comm_create_loopback(mdd_ctx* ctx, void* group, int rank, mdd_comm** out);
 
 /* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
  *              levels, sum_local_dofs, coarse_n] */

@@ -171,6 +171,9 @@ SIGNATURES = {
     "mdd_prec_apply_bench": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
     "mdd_comm_unique_id": (C.c_int, [C.c_char_p]),
     "mdd_comm_create": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p, _PP]),
+    "mdd_comm_loopback_group": (C.c_int, [C.c_int, _PP]),
+    "mdd_comm_loopback_group_free": (None, [_P]),
+    "mdd_comm_create_loopback": (C.c_int, [_P, _P, C.c_int, _PP]),
     "mdd_comm_destroy": (None, [_P]),
     "mdd_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "mdd_prec_set_comm": (C.c_int, [_P, _P]),
@@ -293,8 +296,32 @@ def device_count() -> int:
     return n.value
 
 
+_thread_ctx = threading.local()
+
+
+class use_context:
+    """``with use_context(ctx):`` — calls made by this thread use ``ctx``
+    instead of the process-wide default (one context per thread, e.g. the
+    loopback ranks of tests/test_gpu_distributed.py)."""
+
+    def __init__(self, ctx: "Context"):
+        self.ctx = ctx
+
+    def __enter__(self):
+        self.prev = getattr(_thread_ctx, "ctx", None)
+        _thread_ctx.ctx = self.ctx
+        return self.ctx
+
+    def __exit__(self, *exc):
+        _thread_ctx.ctx = self.prev
+
+
 def get_context() -> Context:
-    """Process-wide default context on ``LOCAL_RANK`` (or device 0)."""
+    """The calling thread's context (:class:`use_context`), else the
+    process-wide default context on ``LOCAL_RANK`` (or device 0)."""
+    local = getattr(_thread_ctx, "ctx", None)
+    if local is not None:
+        return local
     global _ctx
     with _ctx_lock:
         if _ctx is None:

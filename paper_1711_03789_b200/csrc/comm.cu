@@ -12,11 +12,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "mdd_internal.h"
+#include "mdd_kernels.cuh"
 
 namespace mdd {
 
@@ -67,13 +70,92 @@ void nccl_check(ncclResult_t r, const char* what) {
 }  // namespace mdd
 
 namespace mdd {
+namespace {
+// Loopback group: host barrier + device copies between the ranks' buffers.
+constexpr int kLoopMax = 8;
+struct LoopGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  const double2* bufs[kLoopMax] = {};
+  int64_t count[kLoopMax] = {};  // per-rank element count of the current collective
+  int kind[kLoopMax] = {};       // 1 allreduce, 2 allgather: every rank must be in the same collective
+};
+void loop_check(LoopGroup* g, int rank) {
+  for (int k = 0; k < g->n; ++k)
+    if (g->kind[k] != g->kind[rank] || g->count[k] != g->count[rank] || !g->bufs[k])
+      fail(MDD_ENCCL, "loopback group: ranks " + std::to_string(rank) + " and " + std::to_string(k) +
+                          " are in different collectives (kind " + std::to_string(g->kind[rank]) + "/" +
+                          std::to_string(g->kind[k]) + ", count " + std::to_string(g->count[rank]) + "/" +
+                          std::to_string(g->count[k]) + ")");
+}
+void loop_barrier(LoopGroup* g) {
+  std::unique_lock<std::mutex> l(g->mu);
+  const uint64_t my = g->gen;
+  if (++g->arrived == g->n) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+  } else if (!g->cv.wait_for(l, std::chrono::seconds(300), [&] { return g->gen != my; })) {
+    fail(MDD_ENCCL, "loopback group: a rank did not reach the collective within 300 s");
+  }
+}
+struct RankPtrs {
+  const double2* p[kLoopMax];
+};
+__global__ void k_sum_ranks(RankPtrs r, int nr, int64_t n, double2* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = r.p[0][i];
+    for (int k = 1; k < nr; ++k) a = cadd(a, r.p[k][i]);
+    out[i] = a;
+  }
+}
+void loop_allreduce(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
+  auto* g = static_cast<LoopGroup*>(c->loop);
+  CK(cudaStreamSynchronize(s));
+  g->bufs[c->rank] = buf;
+  g->count[c->rank] = n;
+  g->kind[c->rank] = 1;
+  loop_barrier(g);  // every rank's partial is final
+  loop_check(g, c->rank);
+  DevBuf<double2> tmp(n);
+  RankPtrs rp{};
+  for (int k = 0; k < g->n; ++k) rp.p[k] = g->bufs[k];
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096));
+  k_sum_ranks<<<grid, 256, 0, s>>>(rp, g->n, n, tmp.p);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  loop_barrier(g);  // nobody reads the partials any more
+  CK(cudaMemcpyAsync(buf, tmp.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+void loop_allgather(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s) {
+  auto* g = static_cast<LoopGroup*>(c->loop);
+  CK(cudaStreamSynchronize(s));
+  g->bufs[c->rank] = send;
+  g->count[c->rank] = per_rank;
+  g->kind[c->rank] = 2;
+  loop_barrier(g);
+  loop_check(g, c->rank);
+  for (int k = 0; k < g->n; ++k)
+    CK(cudaMemcpyAsync(recv + (int64_t)k * per_rank, g->bufs[k], sizeof(double2) * per_rank,
+                       cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  loop_barrier(g);  // the send buffers may change again
+}
+}  // namespace
+
 void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
+  if (c && c->loop) return loop_allreduce(c, buf, n, s);
   if (!c || !c->comm) return;
   nccl_check(nccl().allReduce(buf, buf, (size_t)(2 * n), ncclFloat64, ncclSum,
                               static_cast<ncclComm_t>(c->comm), s),
              "ncclAllReduce");
 }
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s) {
+  if (c && c->loop) return loop_allgather(c, send, recv, per_rank, s);
   if (!c || !c->comm) {
     double2* dst = recv + (c && c->emulated ? (int64_t)c->rank * per_rank : 0);
     if (send != dst) CK(cudaMemcpyAsync(dst, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
@@ -125,6 +207,31 @@ void mdd_comm_destroy(mdd_comm* c) {
   if (!c) return;
   if (c->comm) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
   delete c;
+}
+
+int mdd_comm_loopback_group(int nranks, void** group_out) {
+  MDD_API_BEGIN
+  if (nranks < 1 || nranks > kLoopMax) fail(MDD_EINVAL, "loopback group: 1..8 ranks");
+  auto* g = new LoopGroup();
+  g->n = nranks;
+  *group_out = g;
+  MDD_API_END
+}
+
+void mdd_comm_loopback_group_free(void* group) { delete static_cast<LoopGroup*>(group); }
+
+int mdd_comm_create_loopback(mdd_ctx* ctx, void* group, int rank, mdd_comm** out) {
+  MDD_API_BEGIN
+  auto* g = static_cast<LoopGroup*>(group);
+  if (!g || rank < 0 || rank >= g->n) fail(MDD_EINVAL, "loopback comm: bad group or rank");
+  CK(cudaSetDevice(ctx->device));
+  std::unique_ptr<mdd_comm> c(new mdd_comm());
+  c->ctx = ctx;
+  c->nranks = g->n;
+  c->rank = rank;
+  c->loop = g;
+  *out = c.release();
+  MDD_API_END
 }
 
 int mdd_comm_info(const mdd_comm* c, int* nranks, int* rank) {

@@ -323,10 +323,13 @@ __device__ double2 tail_finish(const ArnoldiArgs& a, const double2* col, int m, 
   a.dstatus[0] = done;
   a.dstatus[1] = breakdown ? 1 : 0;
   a.dstatus[2] = m;
-  if (a.hstatus) {  // host-mapped; every host reader first synchronises with this kernel (no fences)
+  if (a.hstatus) {
+    // host-mapped; [0] = the iteration that finished the solve (0 while running), one
+    // 4-byte store, so a host loop that reads it while a later iteration runs still
+    // sees a consistent value (gmres_cgs breaks on iterations it knows are complete)
     a.hstatus[1] = breakdown ? 1 : 0;
     a.hstatus[2] = m;
-    a.hstatus[0] = done;
+    a.hstatus[0] = done ? m : 0;
   }
   if (a.use_cond) cudaGraphSetConditional(a.cond, (done || m >= a.maxit) ? 0u : 1u);
   return hmm;
@@ -1185,7 +1188,11 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     CK(cudaEventRecord(itev[it & 1], s));
     if (it >= 2) {  // iteration it-1 finished: its tail has published the status
       CK(cudaEventSynchronize(itev[(it - 1) & 1]));
-      if (hst[0]) break;
+      // break only on a solve finished by iteration it-1 (complete on every rank): the
+      // status word may already show iteration it, which one rank can observe and
+      // another not yet, and every rank must leave the loop after the same collectives
+      const int fin = hst[0];
+      if (fin != 0 && fin <= it - 1) break;
     }
   }
   cudaEventDestroy(itev[0]);

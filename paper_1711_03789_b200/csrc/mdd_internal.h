@@ -192,6 +192,7 @@ struct mdd_comm {
   // allgather: own block only).  Per-rank TIMING of the sharded path with one
   // GPU; the numbers it computes are not the solve's (tools/rank_emulation.py).
   bool emulated = false;
+  void* loop = nullptr;  // LoopGroup (mdd_comm_create_loopback)
 };
 
 namespace mdd {
@@ -200,7 +201,7 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s);
 // recv[r*per_rank ...] = send of rank r (stream-ordered); one rank: copy
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s);
 // true when collectives go through NCCL (any rank count)
-inline bool comm_active(const mdd_comm* c) { return c && (c->comm || c->emulated); }
+inline bool comm_active(const mdd_comm* c) { return c && (c->comm || c->emulated || c->loop); }
 
 // element geometry + 6x6 stiffness / mass (fem.py:154-195); shared by the
 // global assembly, the impras local assembly and the coarse Galerkin kernel

@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["Communicator", "Shard", "shard_bounds", "make_shard", "setup_sharded", "row_block"]
+__all__ = ["Communicator", "LoopbackGroup", "Shard", "shard_bounds", "make_shard", "setup_sharded", "row_block"]
 
 
 def shard_bounds(costs, nranks: int) -> np.ndarray:
@@ -80,10 +80,18 @@ class Communicator:
     ``force_nccl`` initialises NCCL even for a single rank (used by the tests
     to exercise the allreduce path on one GPU)."""
 
-    def __init__(self, ctx=None, group=None, force_nccl: bool = False, emulate=None):
+    def __init__(self, ctx=None, group=None, force_nccl: bool = False, emulate=None, loopback=None):
         import torch.distributed as dist
 
         self.ctx = ctx or _lib.get_context()
+        if loopback is not None:
+            # (LoopbackGroup, rank): ranks are host threads sharing one GPU (tests)
+            grp, rank = loopback
+            self.rank, self.nranks, self._group = int(rank), grp.nranks, grp
+            h = C.c_void_p()
+            _lib.check(_lib.lib.mdd_comm_create_loopback(self.ctx.handle, grp.handle, self.rank, C.byref(h)))
+            self.handle = h
+            return
         if emulate is not None:
             # (rank, nranks) run alone on this GPU, collectives reduced to their local part:
             # per-rank timing only (libmdd MDD_COMM_EMULATE, tools/rank_emulation.py)
@@ -118,6 +126,27 @@ class Communicator:
         h = getattr(self, "handle", None)
         if h:
             _lib.lib.mdd_comm_destroy(h)
+            self.handle = None
+
+
+class LoopbackGroup:
+    """Ranks as host threads on ONE GPU (test infrastructure, libmdd
+    ``mdd_comm_loopback_group``): each thread uses its own context
+    (``_lib.use_context``) and ``Communicator(loopback=(group, rank))``;
+    collectives meet at a host barrier and move data with device copies, so
+    the multi-rank code path (row blocks, allgather layout, partial-sum
+    allreduce) runs for real without several GPUs."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        _lib.check(_lib.lib.mdd_comm_loopback_group(int(nranks), C.byref(h)))
+        self.handle = h
+        self.nranks = int(nranks)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _lib.lib.mdd_comm_loopback_group_free(h)
             self.handle = None
 
 

@@ -15,14 +15,18 @@ from conftest import rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def case():
+def _case_objects():
     from paper_1711_03789_b200 import decomp, fem, mesh
 
     s = fem.build_edge_space(mesh.build_cube_mesh(8), "pec")
     prob = fem.assemble(s, fem.Coefficients(k=4.0, xi=4.0), source=fem.gaussian_source)
     d = decomp.build_decomposition(s, 2, 2, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(4), "pec"))
     return prob, d
+
+
+@pytest.fixture(scope="module")
+def case():
+    return _case_objects()
 
 
 @pytest.mark.parametrize("fam", ["as", "ras", "impras"])
@@ -84,3 +88,62 @@ def test_one_rank_nccl_sharded_cgs2(gpu, case, fam, cor):
     rm = gmres(prob.A, prob.rhs, precond=ref, config=KrylovConfig(tol=1e-8, maxit=80))
     assert abs(rm.iterations - r1.iterations) <= 1
     assert rel(r1.x, rm.x) <= 1e-8
+
+
+@pytest.mark.parametrize("nranks,ortho,fam,cor", [
+    (2, "cgs2", "as", "additive"),
+    (3, "cgs2", "ras", "hybrid"),   # uneven row blocks and shards
+    (2, "mgs", "impras", "adef1"),  # replicated Krylov vectors, sharded preconditioner
+    (8, "cgs2", "as", "additive"),  # one subdomain per rank, as cfg0 on 8 GPUs
+])
+def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
+    """The multi-rank path for real on one GPU: each rank is a host thread with
+    its own context and a loopback communicator (collectives = host barrier +
+    device copies; no kernel waits on another rank).  Sharded applies sum to
+    the unsharded one; every rank returns the same solution, and it matches
+    the one-GPU solve to the north_star tolerances."""
+    import threading
+
+    from paper_1711_03789_b200 import KrylovConfig, _lib, gmres, precond
+    from paper_1711_03789_b200.distributed import Communicator, LoopbackGroup, setup_sharded
+
+    prob, d = case
+    spec = precond.PreconditionerSpec(fam, "two", cor, xi_prec=4.0)
+    ref = precond.setup(prob, d, spec)
+    cfg = KrylovConfig(tol=1e-8, maxit=80, orthogonalization=ortho)
+    want = gmres(prob.A, prob.rhs, precond=ref, config=cfg)
+    v = np.random.default_rng(7).standard_normal(prob.space.ndof) * (1 - 1j)
+    want_apply = ref.apply(v)
+    _lib.get_context().synchronize()
+
+    group = LoopbackGroup(nranks)
+    out, errors = [None] * nranks, []
+
+    def rank_main(r):
+        try:
+            with _lib.use_context(_lib.Context(0)) as ctx:
+                # device objects (spaces, matrices, factors) of this rank live on its own context
+                pr, dr = _case_objects()
+                st = setup_sharded(pr, dr, spec, comm=Communicator(ctx, loopback=(group, r)))
+                applied = st.apply(v)
+                rep = gmres(pr.A, pr.rhs, precond=st, config=cfg)
+                ctx.synchronize()
+                out[r] = (len(st.shard.subdomains), applied, rep)
+        except Exception as exc:  # surfaced below
+            errors.append((r, exc))
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=900)
+    assert not errors, errors
+    assert sum(o[0] for o in out) == d.n_subdomains
+    first = out[0][2]
+    for _, applied, rep in out:
+        assert rel(applied, want_apply) < 1e-13
+        assert rep.iterations == first.iterations and np.array_equal(rep.x, first.x)
+        assert np.array_equal(rep.residual_history, first.residual_history)
+    assert first.converged == want.converged
+    assert abs(first.iterations - want.iterations) <= 1
+    assert rel(first.x, want.x) <= 1e-8
