@@ -48,3 +48,34 @@ def test_library_is_sm100a():
 
     data = open(_lib.LIB_PATH, "rb").read()
     assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_loopback_group_host_side():
+    """The loopback group (multi-rank test harness) is host-only: it can be made
+    and freed without a GPU, and rejects sizes outside 1..8."""
+    from paper_1711_03789_b200 import _lib
+    from paper_1711_03789_b200.distributed import LoopbackGroup
+
+    g = LoopbackGroup(3)
+    assert g.nranks == 3 and g.handle
+    del g
+    h = ctypes.c_void_p()
+    with pytest.raises(_lib.MddError, match="1..8 ranks"):
+        _lib.check(_lib.lib.mdd_comm_loopback_group(9, ctypes.byref(h)))
+
+
+def test_thread_local_context_override():
+    """``use_context`` routes one thread's calls to its own context and restores
+    the previous one on exit (no device needed for the bookkeeping)."""
+    import threading
+
+    from paper_1711_03789_b200 import _lib
+
+    sentinel, seen = object(), {}
+    with _lib.use_context(sentinel):
+        assert _lib.get_context() is sentinel
+        t = threading.Thread(target=lambda: seen.setdefault("other", getattr(_lib._thread_ctx, "ctx", None)))
+        t.start()
+        t.join()
+    assert seen["other"] is None  # other threads keep the process default
+    assert getattr(_lib._thread_ctx, "ctx", None) is None
