@@ -1,7 +1,8 @@
 """Golden CSV tables for the experiments driver, produced by running the
 REFERENCE's own ``maxwelldd.experiments.run_table`` (experiments.py:391-467).
 
-    python tests/golden/make_golden_experiments.py   # ~1 minute, writes experiments.json
+    python tests/golden/make_golden_experiments.py             # ~1 minute, writes experiments.json
+    python tests/golden/make_golden_experiments.py --presets   # full presets -> tables/<preset>.csv
 
 Needs /root/reference (read-only) in this container; the JSON is committed so
 the GPU box can compare the device path's tables against it.
@@ -49,7 +50,24 @@ CASES = {
 }
 
 
+# full paper-table presets (reference experiments.py:184-219), times off; minutes of CPU each
+PRESET_TABLES = ("table1", "table2", "table3", "table4", "table6")
+
+
+def presets(names):
+    """tests/golden/tables/<preset>.csv from the reference's own run_table."""
+    os.makedirs(os.path.join(HERE, "tables"), exist_ok=True)
+    for name in names:
+        _, csv_text = run_table(config_from_preset(name, None, {"times": "false"}))
+        with open(os.path.join(HERE, "tables", f"{name}.csv"), "w", encoding="utf-8", newline="\n") as fh:
+            fh.write(csv_text)
+        print(name, csv_text.count("\n") - 1, "rows")
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--presets":
+        presets(sys.argv[2:] or PRESET_TABLES)
+        return
     out = {}
     for name, (preset, overrides) in CASES.items():
         cfg = config_from_preset(preset, None, overrides)

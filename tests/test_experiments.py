@@ -207,3 +207,19 @@ def test_cli_run(tmp_path, capsys):
     assert text.startswith(CSV_HEADER) and ",as1," in text and ",as2," not in text
     _assert_tables_match(text, "\n".join(_golden()["tiny"]["csv"].split("\n")[i] for i in (0, 2)))
     assert "iters=" in capsys.readouterr().out
+
+
+def _preset_tables():
+    d = os.path.join(GOLDEN, "tables")
+    return sorted(f[:-4] for f in os.listdir(d) if f.endswith(".csv")) if os.path.isdir(d) else []
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset", _preset_tables())
+def test_paper_preset_matches_reference(preset):
+    """A whole paper-table preset (reference experiments.py:184-219) through the
+    device path against the reference's own run_table output."""
+    with open(os.path.join(GOLDEN, "tables", f"{preset}.csv"), encoding="utf-8") as fh:
+        ref = fh.read()
+    _, ours = run_table(config_from_preset(preset, None, {"times": "false"}))
+    _assert_tables_match(ours, ref)
