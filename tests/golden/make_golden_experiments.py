@@ -2,7 +2,7 @@
 REFERENCE's own ``maxwelldd.experiments.run_table`` (experiments.py:391-467).
 
     python tests/golden/make_golden_experiments.py             # ~1 minute, writes experiments.json
-    python tests/golden/make_golden_experiments.py --presets   # full presets -> tables/<preset>.csv
+    python tests/golden/make_golden_experiments.py --presets   # whole presets -> experiments_presets.json (~5 min)
 
 Needs /root/reference (read-only) in this container; the JSON is committed so
 the GPU box can compare the device path's tables against it.
@@ -50,18 +50,22 @@ CASES = {
 }
 
 
-# full paper-table presets (reference experiments.py:184-219), times off; minutes of CPU each
+# the paper-table presets (reference experiments.py:184-219), whole wavenumber lists,
+# times off; a few minutes of CPU in total (run one process at a time: concurrent
+# runs oversubscribe the BLAS threads and crawl)
 PRESET_TABLES = ("table1", "table2", "table3", "table4", "table6")
 
 
 def presets(names):
-    """tests/golden/tables/<preset>.csv from the reference's own run_table."""
-    os.makedirs(os.path.join(HERE, "tables"), exist_ok=True)
+    """tests/golden/experiments_presets.json from the reference's own run_table."""
+    out = {}
     for name in names:
-        _, csv_text = run_table(config_from_preset(name, None, {"times": "false"}))
-        with open(os.path.join(HERE, "tables", f"{name}.csv"), "w", encoding="utf-8", newline="\n") as fh:
-            fh.write(csv_text)
-        print(name, csv_text.count("\n") - 1, "rows")
+        overrides = {"times": "false"}
+        _, csv_text = run_table(config_from_preset(name, None, overrides))
+        out[name] = {"preset": name, "overrides": overrides, "csv": csv_text}
+        print(name, csv_text.count("\n") - 1, "rows", flush=True)
+    with open(os.path.join(HERE, "experiments_presets.json"), "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
 
 
 def main():
