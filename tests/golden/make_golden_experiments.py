@@ -47,6 +47,18 @@ CASES = {
                              "overlap_layers": "1",
                              "preconditioners": "impras1,impras2,imphras,impadef1,as-h,as-adef1",
                              "times": "false", "seed": "11"}),
+    # global impedance boundary (bc = impedance keeps every edge), left-preconditioned weighted
+    # GMRES, the alpha/gpw geometry rules, and the hybrid correction built on A_prec
+    "impedance_bc": (None, {"bc": "impedance", "k_list": "3,4", "fine_list": "6,8", "sub_list": "2,2",
+                            "coarse_list": "3,2", "overlap_layers": "1",
+                            "preconditioners": "as2,ras1,impras2,imphras,hras", "times": "false"}),
+    "weighted_left": ("table4", {"k_list": "3,4", "gmres_side": "left", "times": "false"}),
+    "alpha_rules": (None, {"k_list": "3,5", "fine_rule": "gpw", "fine_g": "12", "sub_rule": "alpha",
+                           "sub_c": "0.5", "coarse_rule": "gpw", "coarse_g": "4",
+                           "preconditioners": "as2,adef1,as-h", "times": "false", "initial_guess": "zero"}),
+    "hybrid_prec_matrix": (None, {"k_list": "4", "fine_list": "8", "sub_list": "2", "coarse_list": "2",
+                                  "hybrid_matrix": "prec", "xi_prob": "k", "xi_prec": "k2",
+                                  "preconditioners": "hras,imphras,as-h", "times": "false"}),
 }
 
 
