@@ -181,9 +181,11 @@ __global__ void __launch_bounds__(256) k_spmv_u(int64_t nrow, const int32_t* __r
     for (int u = 0; u < U; ++u) c[u] = (j0 + u * TPR < e) ? __ldcs(cols + j0 + u * TPR) : -1;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      // predicated on the index, not on the loaded column, so the value loads
+      // issue together with the column loads (only the x gathers wait for them)
       const int j = j0 + u * TPR;
-      if (CPLX) a[u] = c[u] >= 0 ? __ldcs(reinterpret_cast<const double2*>(vals) + j) : make_double2(0.0, 0.0);
-      else a[u] = make_double2(c[u] >= 0 ? __ldcs(vals + j) : 0.0, 0.0);
+      if (CPLX) a[u] = j < e ? __ldcs(reinterpret_cast<const double2*>(vals) + j) : make_double2(0.0, 0.0);
+      else a[u] = make_double2(j < e ? __ldcs(vals + j) : 0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? __ldg(x + c[u]) : make_double2(0.0, 0.0);
