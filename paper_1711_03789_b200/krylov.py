@@ -131,7 +131,9 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, ou
 
     ``rhs`` may also be a device-resident :class:`_lib.DeviceBuffer` (then
     ``out`` must be one too and ``report.x`` is ``out``): the benchmark's
-    HBM-resident path, with no host<->device copies of the vectors.
+    HBM-resident path, with no host<->device copies of the vectors.  With a
+    host ``rhs``, ``out`` may be a caller-owned complex128 array (e.g. pinned
+    memory) that receives the solution (then ``report.x`` is ``out``).
     """
     cfg = config if config is not None else KrylovConfig()
     dio = isinstance(rhs, _lib.DeviceBuffer)
@@ -197,7 +199,15 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, ou
     c.keep_basis = 1 if cfg.keep_basis else 0
     c.device_io = 1 if dio else 0
     c.ortho = 1 if cfg.orthogonalization == "cgs2" else 0
-    x = out if dio else np.empty(n, dtype=np.complex128)
+    if dio:
+        x = out
+    elif isinstance(out, np.ndarray):
+        # caller-owned host solution buffer (e.g. pinned memory for the end-to-end timing)
+        if out.shape != (n,) or out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise ValueError("host `out` must be a contiguous complex128 array of the rhs length")
+        x = out
+    else:
+        x = np.empty(n, dtype=np.complex128)
     hist = np.empty(cfg.maxit + 1, dtype=np.float64)
     drift = np.full(cfg.maxit + 1, np.nan)
     basis = np.empty((cfg.maxit + 1, n), dtype=np.complex128) if cfg.keep_basis else None
