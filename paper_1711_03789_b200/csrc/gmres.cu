@@ -528,8 +528,16 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
   __syncthreads();
+  // max |col_j| (breakdown test): strided over the CTA, then warp and CTA max
+  // (exact, order-free; every CTA needs it to decide whether to write V_m)
+  __shared__ double cmax_w[kArnThreads / 32];
   double cmax = 0.0;
-  for (int j = 0; j <= m; ++j) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  for (int j = threadIdx.x; j <= m; j += blockDim.x) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  cmax = warp_max(cmax);
+  if ((threadIdx.x & 31) == 0) cmax_w[threadIdx.x >> 5] = cmax;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kArnThreads / 32; ++k) cmax = fmax(cmax, cmax_w[k]);
   const bool breakdown = hlast <= 1e-13 * cmax;
   if (!breakdown) {
     double2* vm = a.V + (int64_t)m * n;
