@@ -68,6 +68,7 @@ struct ArnoldiArgs {
   int64_t wcap;  // STREAM path: w elements of the slice held in shared memory
   int pad;       // double2 per publication slot (2 or 8)
   int wg;        // 1: warp 0 alone polls the slots (gather_sum)
+  int pf;        // REG path: L2 prefetch distance in MGS steps (kArnPf; MDD_ARN_PF)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   }
   if constexpr (REG) {
     if (threadIdx.x == 0)
-      for (int t = 2; t < kArnPf && t < nsteps; ++t) prefetch_l2(xvec(t) + lo, len * 16);
+      for (int t = 2; t < a.pf && t < nsteps; ++t) prefetch_l2(xvec(t) + lo, len * 16);
 #pragma unroll
     for (int k = 0; k < kArnE; ++k) {
       const int64_t i = lo + threadIdx.x + (int64_t)k * kArnThreads;
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
       if (!REG && s + 2 < nsteps) prefetch_l2(xvec(s + 2) + lo, len * 16);
       // REG: the register preload of X_{s+2} happens after this step's publish;
       // an L2 bulk prefetch kArnPf steps ahead makes that preload an L2 hit
-      if (REG && s + kArnPf < nsteps) prefetch_l2(xvec(s + kArnPf) + lo, len * 16);
+      if (REG && s + a.pf < nsteps) prefetch_l2(xvec(s + a.pf) + lo, len * 16);
     }
     const bool last = (s + 1 == nsteps);
     const bool drift_next = do_drift && s + 1 < m - 1;
@@ -1409,6 +1410,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.pad = pad;
   // measured per path: warp-0 polling helps the REG path (cfg1 123.9 -> 119.5 ms), hurts STREAM
   aa.wg = getenv("MDD_ARN_WG") ? atoi(getenv("MDD_ARN_WG")) : (mode == 1 ? 1 : 0);
+  aa.pf = getenv("MDD_ARN_PF") ? std::max(2, atoi(getenv("MDD_ARN_PF"))) : kArnPf;
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
     // NaN-fill the publication slots (0xFF bytes are a NaN pattern)
