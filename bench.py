@@ -338,6 +338,7 @@ def run_mine(args, rank, world):
     # memory, so the per-step H2D / D2H copies are DMA transfers
     import torch
 
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))  # pin through this rank's GPU context
     rhs_pin = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
     rhs_pin[:] = rhs
     x_pin = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
