@@ -1,6 +1,6 @@
 """Benchmark: preconditioned GMRES time-to-solve on the BASELINE configs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl mine|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl mine|reference]
 
 One *step* = one complete numeric solve on a fixed mesh + decomposition:
 device assembly of the problem matrix A and of the shifted A_prec
@@ -11,9 +11,13 @@ Mesh, DOF pattern, decomposition and the nested-dissection symbolic analysis
 are per-mesh setup, done once before timing (SURVEY.md §3.6's "setup" phase
 is the numeric factorisation, which is timed).
 
-value : DoFs/s = n_gpus * ndof / (device time per step), inputs resident in HBM.
+value : DoF-iterations/s = ndof * GMRES iterations / (device time per step), SURVEY.md
+        §8d's "DoFs/s", inputs resident in HBM; `time_to_solve` holds seconds per solve.
 e2e   : same metric through the public API with host buffers (rhs H2D and
         x D2H inside the timed region), wall clock.
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU).
 """
 
 from __future__ import annotations
@@ -33,23 +37,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# BASELINE.json configs (SURVEY.md §8d for the conventions chosen where BASELINE is silent)
-CONFIGS = {
-    0: dict(name="cfg0", N=20, k=10.0, xi=10.0, p=2, layers=2, nc=5, family="as", corr="additive",
-            rhs=("gauss", 100.0)),
-    1: dict(name="cfg1", N=40, k=20.0, xi=20.0, p=4, layers=2, nc=10, family="as", corr="additive",
-            rhs=("random", 0)),
-    # second-order Nedelec fine space (extension: the reference has Whitney elements only),
-    # lowest-order coarse space nested in its Whitney part; Gaussian source as cfg0
-    2: dict(name="cfg2", N=30, k=20.0, xi=20.0, p=3, layers=1, nc=8, family="as", corr="additive",
-            rhs=("gauss", 100.0), order=2),
-    3: dict(name="cfg3", N=60, k=30.0, xi=math.sqrt(30.0), p=4, layers=2, nc=15, family="impras",
-            corr="hybrid", rhs=("random", 0)),  # ImpHRAS: the paper's coarse combination for ImpRAS
-    4: dict(name="cfg4", N=80, k=40.0, xi=0.0, p=8, layers=2, nc=20, family="as", corr="additive",
-            rhs=("gauss", 400.0), hetero=True),
-}
-METRIC = "precond_gmres_time_to_solve"
-UNIT = "DoF/s"
+from workloads import CONFIGS, MAXIT, TOL, describe, hetero_fields, random_rhs  # noqa: E402  (plain data, numpy only)
+
+DEFAULT_CONFIG = 4  # the largest BASELINE config; fits one B200 (factors 46 GB + Krylov basis 11 GB of 180 GB)
+METRIC = "precond_gmres_dof_iterations_per_s"
+UNIT = "DoF*it/s"
 
 
 def log(*a):
@@ -62,21 +54,13 @@ def build_problem(c, seed=0):
 
     m = mesh.build_cube_mesh(c["N"])
     space = fem.build_edge_space(m, "pec", order=c.get("order", 1))
-    nt = m.n_tets
     if c.get("hetero"):
-        # eps_r per 4x4x4 block ~ U[1,4]; absorption per block ~ U[k/2, 2k] carried by
-        # sigma = absorption / k, so k*sigma is the block absorption (fem.py:254)
-        rng = np.random.default_rng(seed)
-        blk = np.clip((m.barycenters() * 4).astype(int), 0, 3)
-        bid = (blk[:, 0] * 4 + blk[:, 1]) * 4 + blk[:, 2]
-        eps_b = 1.0 + 3.0 * rng.random(64)
-        abs_b = c["k"] * (0.5 + 1.5 * rng.random(64))
-        coeffs = fem.Coefficients(k=c["k"], xi=c["xi"], eps=eps_b[bid], sigma=abs_b[bid] / c["k"])
+        eps, sigma = hetero_fields(c, m.barycenters(), seed)
+        coeffs = fem.Coefficients(k=c["k"], xi=c["xi"], eps=eps, sigma=sigma)
     else:
         coeffs = fem.Coefficients(k=c["k"], xi=c["xi"])
     if c["rhs"][0] == "random":
-        rng = np.random.default_rng(seed)
-        rhs = (rng.standard_normal(space.ndof) + 1j * rng.standard_normal(space.ndof)) / np.sqrt(2.0)
+        rhs = random_rhs(space.ndof, seed)
     else:
         rhs = fem.assemble_rhs(space, fem.GaussianSource(alpha=c["rhs"][1], direction=(0.0, 0.0, 1.0)))
     coarse = fem.build_edge_space(mesh.build_cube_mesh(c["nc"]), "pec")
@@ -139,122 +123,45 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-def _cpu_block_job(args):
-    """Worker: SuperLU factorisation + one solve of one subdomain block (oracle)."""
-    import time as _t
+def cpu_time_boxed_solve(c, box_s, min_iters=3):
+    """The reference's CPU path (oracle/parallel_oracle.py: the reference pipeline with
+    DenseLU swapped for ND-permuted SuperLU, all host cores) on a bounded sample of the
+    workload: the REAL step from the start -- assembly, every subdomain factorisation,
+    the coarse factorisation -- then GMRES iterations until the time box is spent (or
+    the solve ends).  Nothing is extrapolated: value = ndof * iterations done / wall time
+    of exactly that work.  Imports nothing from the product package."""
+    import psutil
 
-    import numpy as _np
-    import scipy.sparse as _sp
+    from oracle import parallel_oracle as P
 
+    t0 = time.perf_counter()
+    prob = P.build_problem(c, log=log)
+    t_build = time.perf_counter() - t0
+    n = prob["ndof"]
+    cores = os.cpu_count() or 1
+    # SuperLU keeps ~33 B per factor entry; blocks beyond half the free memory are re-factored per apply
+    budget = 0.5 * psutil.virtual_memory().available / 33.0
+    t1 = time.perf_counter()  # the timed step starts here (mesh + decomposition are per-mesh setup in both arms)
     from oracle import maxwell_oracle as O
 
-    data, indices, indptr, shape = args
-    a = _sp.csr_matrix((data, indices, indptr), shape=shape)
-    t0 = _t.perf_counter()
-    f = O._Sparse(a)
-    t1 = _t.perf_counter()
-    f.solve(_np.ones(shape[0], dtype=complex))
-    return t1 - t0, _t.perf_counter() - t1
-
-
-def cpu_sample(c, space, coeffs, rhs, dec, budget_s=12.0, workers=None):
-    """Bounded oracle sample on host cores -> extrapolated time-to-solve.
-
-    Times (a) SuperLU factorisation + solve of `workers` subdomain blocks,
-    concurrently, one per process (the blocks are independent, so all host
-    cores are used; scaled to all subdomains assuming perfect parallel
-    speed-up, which favours the CPU), (b) one SpMV and one coarse solve,
-    (c) the MGS2 Arnoldi step at two basis sizes (linear in m); then sums the
-    full solve at the GPU run's iteration count.
-    """
-    from concurrent.futures import ProcessPoolExecutor
-
-    from oracle import maxwell_oracle as O
-
-    t_start = time.perf_counter()
-    md = {k: getattr(space.mesh, k) for k in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs",
-                                              "boundary_faces")}
-    t0 = time.perf_counter()
-    if getattr(space, "order", 1) == 2:
-        from oracle import nedelec2_oracle as O2
-
-        sysm = O2.assemble(space.mesh.vertices, space.mesh.tets, space.tet_dofs, space.ndof, coeffs.k, coeffs.xi,
-                           eps=coeffs.eps, mu=coeffs.mu, sigma=coeffs.sigma)
-    else:
-        sysm = O.assemble(md, space.edge_to_dof, space.ndof, coeffs.k, coeffs.xi, eps=coeffs.eps, mu=coeffs.mu,
-                          sigma=coeffs.sigma)
-    t_asm = time.perf_counter() - t0
-    A = sysm["A"]
-    nsub = len(dec.dofs)
-    P = max(1, min(nsub, workers or (os.cpu_count() or 1)))
-    jobs = []
-    for ell in range(P):
-        a_l = A[dec.dofs[ell]][:, dec.dofs[ell]].tocsr()
-        jobs.append((a_l.data, a_l.indices, a_l.indptr, a_l.shape))
-    if P > 1:
-        import multiprocessing as mp
-
-        # spawn, not fork (forking after BLAS threads exist can deadlock the
-        # children); one BLAS thread per worker: the parallelism is the pool
-        saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
-        for k in saved:
-            os.environ[k] = "1"
-        try:
-            with ProcessPoolExecutor(max_workers=P, mp_context=mp.get_context("spawn")) as ex:
-                res = list(ex.map(_cpu_block_job, jobs))
-        finally:
-            for k, v in saved.items():
-                if v is None:
-                    os.environ.pop(k, None)
-                else:
-                    os.environ[k] = v
-    else:
-        res = [_cpu_block_job(jobs[0])]
-    fac_times = [r[0] for r in res]
-    solve_times = [r[1] for r in res]
-    rng = np.random.default_rng(0)
-    r0 = dec.coarse.R0
-    t0 = time.perf_counter()
-    a0 = (r0 @ A @ r0.T).tocsc()
-    f0 = O._Sparse(a0)
-    t_coarse_fac = time.perf_counter() - t0
-    x = rng.standard_normal(space.ndof) + 1j * rng.standard_normal(space.ndof)
-    t0 = time.perf_counter()
-    for _ in range(3):
-        A @ x
-    t_spmv = (time.perf_counter() - t0) / 3
-    t0 = time.perf_counter()
-    r0.T @ f0.solve(r0 @ x)
-    t_coarse = time.perf_counter() - t0
-
-    def mgs(m):
-        V = [rng.standard_normal(space.ndof) + 0j for _ in range(m)]
-        w = x.copy()
-        t = time.perf_counter()
-        for _ in range(2):
-            for j in range(m):
-                h = np.vdot(V[j], w)
-                w = w - h * V[j]
-        return time.perf_counter() - t
-
-    m1, m2 = 8, 24
-    tm1, tm2 = mgs(m1), mgs(m2)
-    slope = max((tm2 - tm1) / (m2 - m1), 0.0)
-    return {
-        "t_asm": t_asm, "t_fac_sub": float(np.mean(fac_times)), "t_solve_sub": float(np.mean(solve_times)),
-        "t_coarse_fac": t_coarse_fac, "t_coarse": t_coarse, "t_spmv": t_spmv, "mgs_slope": slope,
-        "mgs_icpt": max(tm1 - slope * m1, 0.0), "nsub": nsub, "n_sampled": len(fac_times), "workers": P,
-        "sample_s": time.perf_counter() - t_start,
-    }
-
-
-def cpu_extrapolate(s, iterations):
-    par = s["nsub"] / s["workers"]  # subdomain work spread over the worker processes
-    t_fac = 2 * s["t_asm"] + par * s["t_fac_sub"] + s["t_coarse_fac"]
-    t_apply = par * s["t_solve_sub"] + s["t_coarse"]
-    t_it = (iterations + 1) * (t_apply + s["t_spmv"])
-    t_arn = sum(s["mgs_icpt"] + s["mgs_slope"] * m for m in range(1, iterations + 1)) * 1.5  # + drift check
-    return t_fac + t_it + t_arn
+    A = O.assemble(prob["mesh"], prob["space"]["edge_to_dof"], n, c["k"], c["xi"], eps=prob["eps"],
+                   sigma=prob["sigma"])["A"]  # the step re-assembles, as the device arm's step does
+    prob["A"] = A
+    t_asm = time.perf_counter() - t1
+    with P.ParallelSchwarz(prob, workers=cores, resident_entries=budget, log=log) as M:
+        t_setup = time.perf_counter() - t1
+        t2 = time.perf_counter()
+        # ONE solve, stopped at the first iteration boundary past the time box
+        x, hist, its, conv, tm = P.gmres(A, prob["rhs"], M.apply, tol=TOL, maxit=MAXIT, deadline=t1 + box_s,
+                                         min_iters=min_iters)
+        t_gmres = time.perf_counter() - t2
+        entries = M.factor_entries
+        workers = M.workers
+    wall = t_setup + t_gmres  # assembly + every factorisation + the (truncated) solve
+    return {"value": n * its / wall, "ndof": n, "iterations": int(its), "converged": bool(conv), "wall_s": wall,
+            "assemble_s": t_asm, "setup_s": t_setup, "gmres_s": t_gmres, "phases": tm, "cores": cores,
+            "workers": workers, "build_s": t_build, "factor_entries": entries, "final_rel_residual": float(hist[-1]),
+            "resident_entries_cap": budget}
 
 
 # ---------------------------------------------------------------- our arm
@@ -314,7 +221,7 @@ def run_mine(args, rank, world):
     launches0 = ctx.kernel_launches()
     ms_steps, phases, reps = [], [], []
     host = np.zeros(4)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with ClockSampler(int(ctx.device)) as clk:
         for _ in range(args.steps):
             ctx.record(0)
             rep = step()
@@ -338,7 +245,7 @@ def run_mine(args, rank, world):
     # memory, so the per-step H2D / D2H copies are DMA transfers
     import torch
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))  # pin through this rank's GPU context
+    torch.cuda.set_device(int(ctx.device))  # pin through the solver context's own GPU
     rhs_pin = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
     rhs_pin[:] = rhs
     x_pin = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
@@ -397,7 +304,7 @@ def run_mine(args, rank, world):
     hist = rep.residual_history
     res = {
         "metric": METRIC,
-        "value": n / (ms_step / 1e3),  # one solve per step, shared by all ranks
+        "value": n * its / (ms_step / 1e3),  # DoFs/s = n * iterations / solve time; one solve per step
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
@@ -409,9 +316,7 @@ def run_mine(args, rank, world):
         "dtype": "c128",
         "data": "synthetic (seeded; BASELINE.json configs)",
         "config": {
-            "workload": f"{c['name']}: N={c['N']} ({n} DoFs), k={c['k']}, xi={c['xi']:.4g}, "
-                        f"{c['p']}^3 subdomains, {c['layers']} overlap layers, coarse N={c['nc']}, "
-                        f"{spec.label()}, right GMRES tol 1e-6 maxit 200",
+            "workload": describe(c, n, spec.label()),
             "ndof": n, "subdomains": len(dec.dofs), "iterations": its, "converged": bool(rep.converged),
             "final_rel_residual": float(hist[-1]),
             "parallelism": (f"subdomains sharded over {world} GPUs (NCCL allreduce per apply), coarse replicated, "
@@ -442,21 +347,31 @@ def run_mine(args, rank, world):
                                        "(profiles/traffic.json)" if roof_all[dom]["traffic"] else None},
         "roofline_all": roof_all,
         "roofline_factor": roof_factor,
-        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+        "time_to_solve": {"s_per_solve": ms_step / 1e3, "dofs_per_s": n / (ms_step / 1e3),
+                          "cold_s": t_dec + t_setup + ms_step / 1e3,
+                          "cold_includes": "decomposition + first setup (symbolic ND analysis, allocation, first "
+                                           "numeric factorisation) + one timed step"},
+        "e2e": {"value": n * rep_e.iterations / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "s_per_step": e2e_s, "s_steps": [round(v, 4) for v in e2e_t], "iterations": rep_e.iterations},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        s = cpu_sample(c, space, coeffs, rhs, dec)
-        t_cpu = cpu_extrapolate(s, its)
-        res["cpu_baseline"] = {"value": n / t_cpu, "unit": UNIT, "cores": s["workers"], "kind": "port",
-                               "sample": f"oracle (numpy/SuperLU) on {s['n_sampled']} of {s['nsub']} subdomain "
-                                         f"factorisations+solves ({s['workers']} processes), 1 SpMV, 1 coarse "
-                                         f"solve, MGS2 at m=8,24; "
-                                         f"extrapolated to {its} iterations ({s['sample_s']:.1f}s sampled, "
-                                         f"est. {t_cpu:.0f}s per solve)",
-                               "est_s_per_solve": t_cpu}
+        if c.get("order", 1) != 1:
+            res["cpu_baseline"] = None  # no CPU reference exists for the order-2 extension
+        else:
+            res["cpu_baseline"] = cpu_baseline_record(cpu_time_boxed_solve(c, args.cpu_box))
     return res
+
+
+def cpu_baseline_record(s):
+    return {"value": s["value"], "unit": UNIT, "cores": s["cores"], "kind": "port",
+            "sample": f"oracle port of the reference (numpy + ND-SuperLU, {s['workers']} worker processes + threaded "
+                      f"BLAS) on the same workload, one real step from the start: assembly {s['assemble_s']:.1f}s, all "
+                      f"subdomain + coarse factorisations (setup {s['setup_s']:.1f}s incl. assembly), then the first "
+                      f"{s['iterations']} GMRES iterations ({s['gmres_s']:.1f}s) of the solve; value = ndof*iterations"
+                      f"/wall ({s['wall_s']:.1f}s), nothing extrapolated",
+            "iterations": s["iterations"], "wall_s": s["wall_s"], "setup_s": s["setup_s"], "gmres_s": s["gmres_s"],
+            "phases_s": s["phases"], "final_rel_residual": s["final_rel_residual"], "converged": s["converged"]}
 
 
 def read_traffic(cfg_name):
@@ -488,31 +403,42 @@ def read_peaks():
 
 # ---------------------------------------------------------- reference arm
 def run_reference(args):
-    """The reference's CPU path (the oracle port: the reference is pure Python and
-    cannot travel to the GPU box) on a bounded sample of the same workload."""
+    """The reference's CPU implementation of the path on this box's host cores.  The
+    reference package is pure Python and cannot travel to the GPU box, and its dense LU
+    cannot hold any config beyond cfg0, so this is the oracle port (kind "port"), built
+    product-free (oracle/geometry_oracle.py: no libmdd.so is loaded by this arm).
+
+    A full CPU step at the headline config takes minutes, so the whole run is ONE real
+    step from the start, time-boxed (--ref-box seconds): assembly, all factorisations,
+    then GMRES iterations until the box is spent.  --steps/--warmup are echoed but not
+    multiplied: "steps_run" says what ran.  value = ndof * iterations / wall."""
     c = CONFIGS[args.config]
-    space, coeffs, rhs, dec, _ = build_problem(c)
-    n = space.ndof
-    its = 200 if args.config == 1 else 60
-    vals = []
-    workers = 1
-    for i in range(args.warmup + args.steps):
-        s = cpu_sample(c, space, coeffs, rhs, dec, budget_s=8.0)
-        workers = s["workers"]
-        if i >= args.warmup:
-            vals.append(cpu_extrapolate(s, its))
-    t = float(np.mean(vals))
+    if c.get("order", 1) != 1:
+        return {"impl": "reference", "unavailable": "no CPU reference exists for the order-2 extension (cfg2)"}
+    s = cpu_time_boxed_solve(c, args.ref_box, min_iters=5)
+    label = {"additive": "2", "hybrid": "-H", "adef1": "-ADEF1"}[c["corr"]]
+    label = {"as": "AS", "ras": "RAS", "impras": "ImpRAS"}[c["family"]] + label
     return {
-        "metric": METRIC, "impl": "reference", "value": n / t, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "metric": METRIC, "impl": "reference", "value": s["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "steps_run": 1, "warmup_run": 0,
+        "ms_per_step": s["wall_s"] * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded; BASELINE.json configs)",
-        "config": {"workload": f"{c['name']} (same as the GPU arm)", "ndof": n, "iterations_assumed": its},
-        "cpu_baseline": {"value": n / t, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"oracle restatement of the reference (numpy + SuperLU), bounded sample per step: "
-                                   f"{workers} subdomain factorisations+solves in {workers} processes, SpMV, coarse "
-                                   f"solve, MGS2 timings, extrapolated to a full solve"},
-        "e2e": {"value": n / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": describe(c, s["ndof"], label), "ndof": s["ndof"], "iterations": s["iterations"],
+                   "converged": s["converged"], "final_rel_residual": s["final_rel_residual"],
+                   "time_box_s": args.ref_box},
+        "cpu_baseline": cpu_baseline_record(s),
+        "e2e": {"value": s["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_imported": "paper_1711_03789_b200" in sys.modules,
+        "repo_so_mapped": _mapped_repo_libraries(),
     }
+
+
+def _mapped_repo_libraries():
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ".so" in ln and ROOT in ln})
+    except OSError:
+        return None
 
 
 # ------------------------------------------------------------ distributed
@@ -545,18 +471,55 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
+def torchrun_command(n, argv, port=None):
+    """The launch line the driver itself uses for N > 1 (one rank per GPU, NCCL over NVLink)."""
+    if port is None:
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
+def visible_gpus():
+    from paper_1711_03789_b200 import _lib
+
+    return _lib.device_count()
+
+
+def relaunch_under_torchrun(n, argv, count=visible_gpus, run=subprocess.call):
+    have = count()
+    if have < n:
+        print(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's transport lines (NVLS / P2P) in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return run(torchrun_command(n, argv), env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-box", type=float, default=75.0,
+                    help="time box (s) of the cpu_baseline leg's real CPU step (setup + first GMRES iterations)")
+    ap.add_argument("--ref-box", type=float, default=180.0,
+                    help="time box (s) of the --impl reference arm's one real CPU step")
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ortho", choices=["mgs", "cgs2"], default=None,
                     help="Gram-Schmidt variant (default: mgs on one GPU, cgs2 sharded)")
     args = ap.parse_args()
+    if args.impl == "mine" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus, sys.argv[1:]))
     rank, world = dist_init()
+    if args.impl == "mine" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)

@@ -176,28 +176,28 @@ int mdd_coarse_restriction(int64_t nv, const double* fverts, int64_t ntf, const 
                            int64_t** out_rowptr, int64_t** out_cols, double** out_vals, int64_t* bad_edge);
 
 /* ------------------------------------------------------ preconditioner
- * precond.PreconditionerState.__init__ / setup (precond.py:280-323, 380-387)
- * and PreconditionerState.apply (precond.py:347-375).
+ * precond.PreconditionerState.__init__ / setup (precond.py:150-193, 250-257)
+ * and PreconditionerState.apply (precond.py:217-245).
  *
  * Subdomain local problems are factorised by a batched multifrontal
  * elimination over a geometric nested-dissection ordering (replaces the
  * DenseLU/zgetrf of linalg.py:73-107); the coarse block R0 A R0^T is formed by
  * an element-wise Galerkin kernel and factorised the same way. */
 typedef struct {
-  int family;      /* 0 as, 1 ras, 2 impras   (precond.py:172)               */
+  int family;      /* 0 as, 1 ras, 2 impras   (precond.py:42)               */
   int levels;      /* 1 or 2                                                 */
-  int correction;  /* 0 additive, 1 hybrid, 2 adef1 (precond.py:173)         */
+  int correction;  /* 0 additive, 1 hybrid, 2 adef1 (precond.py:43)         */
   int64_t lu_cap;  /* SizeCapError threshold on a local block, <=0: none     */
   int leaf_size;   /* nested-dissection leaf size (0 -> default)             */
   /* fine level */
-  const mdd_csr* A_prec;  /* assembled at xi_prec (precond.py:285-287)       */
-  const mdd_csr* A_corr;  /* matrix inside hybrid/adef1 (precond.py:289)     */
+  const mdd_csr* A_prec;  /* assembled at xi_prec (precond.py:155-157)       */
+  const mdd_csr* A_corr;  /* matrix inside hybrid/adef1 (precond.py:159)     */
   int32_t nsub;
   const int64_t* sub_ptr;   /* nsub+1 offsets into sub_dofs                  */
   const int64_t* sub_dofs;  /* sorted global DOF sets I_l (decomp.py:140-191) */
   const double* sub_pou;    /* aligned weights (decomp.py:194-205) or NULL   */
   const int32_t* dof_xyz;   /* (ndof,3) DoF positions in 1/dof_grid cell units */
-  /* impras: local matrices assembled on the submesh (precond.py:212-269)    */
+  /* impras: local matrices assembled on the submesh (precond.py:82-139)    */
   const mdd_space* space;   /* fine lowest-order space (impras local assembly,
                                coarse Galerkin; for an order-2 fine space its
                                Whitney companion on the same mesh)            */
@@ -221,12 +221,12 @@ typedef struct {
  * coarse space. */
 int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* desc, mdd_prec** out,
                     int32_t* failed_ctx);
-/* PreconditionerState.variant (precond.py:325-343): a view sharing factors. */
+/* PreconditionerState.variant (precond.py:195-213): a view sharing factors. */
 int mdd_prec_variant(const mdd_prec* base, int family, int levels, int correction,
                      const mdd_csr* A_corr, mdd_prec** out);
 void mdd_prec_destroy(mdd_prec* P);
 int mdd_prec_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
-/* PreconditionerState.coarse_solve (precond.py:357-358): R0^T A0^{-1} R0 v */
+/* PreconditionerState.coarse_solve (precond.py:227-228): R0^T A0^{-1} R0 v */
 int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
 /* Diagnostics: device-timed applies (inputs resident, CUDA events on the
  * context stream).  which: 0 full apply, 1 restriction + subdomain solves,

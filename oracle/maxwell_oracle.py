@@ -176,7 +176,7 @@ def subdomain_faces(tets, elems, nv):
 
 
 def impedance_local_matrix(mesh, edge_to_dof, kept_edges, gdofs, elems, k, xi, eps=1.0, mu=1.0, sigma=0.0):
-    """Submesh assembly + boundary impedance — reference precond.py:212-269 (local_bc='impedance')."""
+    """Submesh assembly + boundary impedance — reference precond.py:82-139 (local_bc='impedance')."""
     nt = len(mesh["tets"])
     eps_a = np.broadcast_to(np.asarray(eps, float), (nt,))[elems]
     mu_a = np.broadcast_to(np.asarray(mu, float), (nt,))[elems]
@@ -214,7 +214,7 @@ class _Sparse:
 
 
 class Schwarz:
-    """One/two-level AS, RAS, ImpRAS — reference precond.py:277-377.
+    """One/two-level AS, RAS, ImpRAS — reference precond.py:147-247.
 
     `local` holds the local matrices (minors for as/ras, submesh matrices
     for impras); factors are dense LU (as the reference) or SuperLU for
@@ -269,7 +269,7 @@ class Schwarz:
 
 
 def minors(A, dof_sets):
-    """Exact minors R A R^T — reference linalg.py:48-70 / precond.py:296-301."""
+    """Exact minors R A R^T — reference linalg.py:48-70 / precond.py:166-171."""
     A = sp.csr_matrix(A)
     return [A[d][:, d] for d in dof_sets]
 

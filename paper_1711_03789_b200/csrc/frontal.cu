@@ -3,7 +3,7 @@
 //
 // Replaces linalg.DenseLU (zgetrf, reference linalg.py:73-101) and
 // DenseLU.solve (zgetrs, linalg.py:103-107) as used per subdomain and for
-// the coarse block in precond.PreconditionerState (precond.py:296-322,
+// the coarse block in precond.PreconditionerState (precond.py:166-192,
 // 347-358).
 #include <algorithm>
 #include <cmath>

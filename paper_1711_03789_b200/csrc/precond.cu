@@ -1,5 +1,5 @@
 // Two-level overlapping Schwarz preconditioners on the device
-// (reference precond.PreconditionerState, precond.py:277-377).
+// (reference precond.PreconditionerState, precond.py:147-247).
 //
 //  setup : subdomain blocks R_l A_prec R_l^T (exact minors, linalg.py:48-70)
 //          are analysed by geometric nested dissection and factorised as one
@@ -9,9 +9,9 @@
 //          C(T)'s Whitney functions on T's edges) and factorised the same way.
 //  apply : gather v[I_l] -> batched forward/backward solves -> owner-computes
 //          scatter out[i] = sum_{l owning i} w_l(i) u_l(i) (subdomain order,
-//          as precond.py:350-355), fused with the coarse prolongation for
+//          as precond.py:220-225), fused with the coarse prolongation for
 //          the additive variant; hybrid / ADEF1 compose the same primitives
-//          (precond.py:360-375).
+//          (precond.py:230-245).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -411,7 +411,7 @@ static void one_level_solve(mdd_prec* P, const double2* v, cudaStream_t s) {
 static void one_level_scatter(mdd_prec* P, const double2* add, double2* out, cudaStream_t s) {
   PrecCore& c = *P->core;
   mdd_ctx* ctx = c.ctx;
-  const bool weighted = P->family != 0;  // ras / impras (precond.py:348)
+  const bool weighted = P->family != 0;  // ras / impras (precond.py:218)
   k_scatter_owner<<<gsb(ctx, c.ndof), 256, 0, s>>>(c.ndof, c.own_ptr.p, c.own_idx.p,
                                                    weighted ? c.own_w.p : nullptr, c.sub.xloc.p,
                                                    add, out);
@@ -441,7 +441,7 @@ static void one_level(mdd_prec* P, const double2* v, const double2* add, double2
   one_level_finish(P, add, out, s);
 }
 
-// out = R0^T A0^{-1} R0 v   (precond.py:357-358)
+// out = R0^T A0^{-1} R0 v   (precond.py:227-228)
 static void coarse_solve(mdd_prec* P, const double2* v, double2* out, cudaStream_t s) {
   PrecCore& c = *P->core;
   spmv_dev(c.ctx, c.R0p.get(), v, c.coarse.bloc.p, s);
@@ -800,7 +800,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
       }
     c.tpos.upload(tp, s);
     c.symflag.alloc(1);
-    // exact minors of A_prec on I_l (precond.py:296-301)
+    // exact minors of A_prec on I_l (precond.py:166-171)
     const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> th;
     std::atomic<int> next{0};
@@ -832,7 +832,7 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
       });
     for (auto& x : th) x.join();
   } else {
-    // impras: submesh assembly + boundary faces (precond.py:212-269)
+    // impras: submesh assembly + boundary faces (precond.py:82-139)
     const mdd_space* fs = d->space;
     if (!fs || !d->sub_tet_ptr || !d->sub_tets) fail(MDD_EINVAL, "impras needs subdomain tets");
     const int64_t nv = fs->nv;

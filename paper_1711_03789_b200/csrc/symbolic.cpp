@@ -2,7 +2,7 @@
 //
 // Replaces nothing in the reference directly: the reference factors each
 // subdomain block densely (linalg.DenseLU, linalg.py:73-101, via
-// precond.py:296-313).  The DOFs of an edge space carry integer midpoint
+// precond.py:166-183).  The DOFs of an edge space carry integer midpoint
 // coordinates in half-cell units (order 2: sixth-cell units for edge
 // midpoints and face centroids, SymIn::grid); a vertex plane x_axis = c (c a
 // multiple of the grid unit) contains exactly the edges (faces) lying in it, and because every

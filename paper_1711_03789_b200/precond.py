@@ -2,7 +2,7 @@
 
 Public surface of reference ``maxwelldd.precond`` (/root/reference/pkg/src/
 maxwelldd/precond.py:1-257).  ``setup`` assembles the shifted system at
-``xi_prec`` on the GPU (precond.py:285-289), then builds and numerically
+``xi_prec`` on the GPU (precond.py:155-159), then builds and numerically
 factorises every local block and the coarse block on the device (batched
 multifrontal elimination over a geometric nested-dissection ordering, see
 csrc/frontal.h).  ``apply`` is a fixed linear map evaluated entirely on the
@@ -98,7 +98,7 @@ def _concat(sets, dtype=np.int64):
 
 
 class PreconditionerState:
-    """Factorised Schwarz preconditioner; ``apply`` is a fixed linear map (reference precond.py:277-377)."""
+    """Factorised Schwarz preconditioner; ``apply`` is a fixed linear map (reference precond.py:147-247)."""
 
     def __init__(self, problem: SystemBundle, decomp: Decomposition, spec: PreconditionerSpec,
                  lu_cap=DEFAULT_LU_CAP, leaf_size: int = 0, shard=None):
@@ -227,7 +227,7 @@ class PreconditionerState:
         return h
 
     def variant(self, spec: PreconditionerSpec) -> "PreconditionerState":
-        """View sharing all factors (reference precond.py:325-343)."""
+        """View sharing all factors (reference precond.py:195-213)."""
         if _local_kind(spec) != _local_kind(self.spec):
             raise ValueError("variant would need different local factorizations")
         if spec.xi_prec != self.spec.xi_prec:
@@ -288,5 +288,5 @@ class PreconditionerState:
 
 def setup(problem: SystemBundle, decomp: Decomposition, spec: PreconditionerSpec,
           lu_cap=DEFAULT_LU_CAP) -> PreconditionerState:
-    """Factorise all local (and coarse) blocks at ``spec.xi_prec`` (reference precond.py:380-387)."""
+    """Factorise all local (and coarse) blocks at ``spec.xi_prec`` (reference precond.py:250-257)."""
     return PreconditionerState(problem, decomp, spec, lu_cap=lu_cap)

@@ -151,3 +151,98 @@ def test_oracle_random_initial_guess(gg):
     x, h, it, conv = O.gmres(sysm["A"], b, tol=1e-6, maxit=60, x0=x0)
     assert it == int(gg["rand_it"])
     assert rel(x, gg["rand_x"]) <= 1e-10
+
+
+# ------------------------------------------------- geometry oracle (product-free)
+def test_geometry_oracle_mesh_matches_reference():
+    from oracle import geometry_oracle as G
+
+    g = load_golden("mesh.npz")
+    for n in (1, 3):
+        m = G.cube_mesh(n)
+        for f in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs", "boundary_edge_flags",
+                  "boundary_faces"):
+            assert np.array_equal(m[f], g[f"n{n}_{f}"]), (n, f)
+    assert np.array_equal(G.nesting_map(G.cube_mesh(1), G.cube_mesh(3)), g["nest_3_1"])
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_geometry_oracle_decomposition_matches_reference(tag):
+    from oracle import geometry_oracle as G
+
+    g = load_golden("decomp.npz")
+    n, p, layers, nc = (int(v) for v in g[f"{tag}_case"])
+    s = G.edge_space(G.cube_mesh(n))
+    d = G.decomposition(s, p, layers, G.edge_space(G.cube_mesh(nc)))
+    for key, got in (("elements", d["elements"]), ("dofs", d["dofs"]), ("pou", d["pou"]),
+                     ("impdofs", G.impedance_dof_sets(s, d["elements"]))):
+        want = golden_ragged(g, f"{tag}_{key}")
+        assert len(got) == len(want)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b), key
+    assert np.array_equal(d["tet_map"], g[f"{tag}_tetmap"])
+    # the reference keeps rounding-level entries of its Gauss rule (decomp.py:287-291); values agree to 1e-14
+    assert abs(d["R0"] - golden_csr(g, f"{tag}_R0")).max() <= 1e-14
+
+
+def test_geometry_oracle_impedance_space():
+    from oracle import geometry_oracle as G
+
+    g = load_golden("decomp.npz")
+    si = G.edge_space(G.cube_mesh(4), "impedance")
+    d = G.decomposition(si, 2, 1, G.edge_space(G.cube_mesh(2), "impedance"))
+    for a, b in zip(d["dofs"], golden_ragged(g, "imp_dofs")):
+        assert np.array_equal(a, b)
+    assert abs(d["R0"] - golden_csr(g, "imp_R0")).max() <= 1e-14
+
+
+def test_nd_order_is_a_permutation_with_plane_separators():
+    from oracle import geometry_oracle as G
+    from oracle import parallel_oracle as P
+
+    s = G.edge_space(G.cube_mesh(6))
+    xyz = G.edge_half_coords(s["mesh"])[s["kept_edges"]]
+    perm = P.nd_order(xyz, leaf=8)
+    assert np.array_equal(np.sort(perm), np.arange(s["ndof"]))
+    # the last block is the top separator: one grid plane
+    top = xyz[perm[-1]]
+    a = [ax for ax in range(3) if (xyz[:, ax] == top[ax]).sum() and top[ax] % 2 == 0]
+    assert a
+
+
+def test_parallel_oracle_cfg0_matches_reference_dense_solve():
+    """The config-scale oracle (ND-SuperLU in worker processes, BLAS MGS2) against the
+    reference package's own cfg0 solve with its dense LAPACK LU (tests/golden/cfg0.npz)."""
+    import workloads as W
+    from oracle import parallel_oracle as P
+
+    g = load_golden("cfg0.npz")
+    prob = P.build_problem(W.CONFIGS[0])
+    assert rel(prob["rhs"], g["rhs"]) <= 1e-13
+    with P.ParallelSchwarz(prob, workers=2) as M:
+        x, hist, its, conv, _ = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=W.MAXIT)
+        # same map with another worker count: the sum order is the reference's, not the pool's
+        v = W.random_rhs(prob["ndof"], seed=3)
+        y2 = M.apply(v)
+    with P.ParallelSchwarz(prob, workers=3) as M3:
+        assert np.array_equal(M3.apply(v), y2)
+    assert its == int(g["it"]) and conv == bool(g["conv"])
+    assert rel(x, g["x"]) <= 1e-10
+    assert np.allclose(hist, g["hist"], rtol=1e-9)
+
+
+def test_config_goldens_are_consistent():
+    """The committed config-scale goldens carry a history that is monotone and whose
+    last value equals the true relative residual of the stored iterate."""
+    import os
+
+    from conftest import GOLDEN
+
+    for name in ("cfg1", "cfg3", "cfg4"):
+        path = os.path.join(GOLDEN, f"{name}_oracle.npz")
+        if not os.path.exists(path):
+            continue
+        g = dict(np.load(path))
+        assert np.all(np.diff(g["hist"]) <= 0)
+        assert float(g["true_rel_res"]) == pytest.approx(float(g["hist"][-1]), rel=1e-6)
+        assert len(g["hist"]) == int(g["its"]) + 1
