@@ -192,7 +192,8 @@ def run_mine(args, rank, world):
     # sharded Krylov vectors (three small allreduces per iteration instead of
     # one per MGS step), validated against MGS2 in tests/test_gpu_gmres.py
     ortho = args.ortho or ("cgs2" if world > 1 else "mgs")
-    kcfg = krylov.KrylovConfig(tol=1e-6, maxit=200, side="right", initial_guess="zero", orthogonalization=ortho)
+    kcfg = krylov.KrylovConfig(tol=TOL, maxit=MAXIT, side="right", initial_guess="zero", orthogonalization=ortho,
+                               check_orthogonality=not args.no_drift)
     rhs_dev = _lib.DeviceBuffer(ctx, 16 * n)
     rhs_dev.upload(rhs)
     x_dev = _lib.DeviceBuffer(ctx, 16 * n)
@@ -512,6 +513,8 @@ def main():
                     help="time box (s) of the --impl reference arm's one real CPU step")
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-drift", action="store_true",
+                    help="experiment: skip the reference's orthogonality-drift check (krylov.py:152-160)")
     ap.add_argument("--ortho", choices=["mgs", "cgs2"], default=None,
                     help="Gram-Schmidt variant (default: mgs on one GPU, cgs2 sharded)")
     args = ap.parse_args()

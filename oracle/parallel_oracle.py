@@ -34,6 +34,7 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 from scipy.linalg import blas as _blas
+from threadpoolctl import threadpool_limits
 
 from . import geometry_oracle as G
 from . import maxwell_oracle as O
@@ -125,6 +126,7 @@ def _load_dir(d):
 
 
 def _worker_main(conn, tmpdir, subs, meta, shm_names):
+    threadpool_limits(limits=1)  # one BLAS thread per worker whatever the inherited environment says
     arr = _load_dir(tmpdir)
     n, total = meta["ndof"], meta["total"]
     A = sp.csr_matrix((arr["A_data"], arr["A_indices"], arr["A_indptr"]), shape=(n, n))
@@ -256,16 +258,22 @@ class ParallelSchwarz:
                     os.environ[k] = val
         t0 = time.perf_counter()
         res = self._round(("factor",))
+        t_sub = time.perf_counter() - t0
         self.factor_entries = sum(r[2] for r in res)
         self.coarse = None
         if self.R0 is not None:
             a0 = (self.R0 @ self.A @ self.R0.T).tocsr()  # triple_product(R0, A_prec), precond.py:189-192
             cs = prob["coarse_space"]
-            self.coarse = NDLU(a0, G.edge_half_coords(cs["mesh"])[cs["kept_edges"]])
+            # SuperLU calls BLAS on small supernodes: one thread (a threaded BLAS only adds sync cost there)
+            with threadpool_limits(limits=1):
+                self.coarse = NDLU(a0, G.edge_half_coords(cs["mesh"])[cs["kept_edges"]])
             self.factor_entries += self.coarse.entries
         self.setup_time_s = time.perf_counter() - t0
+        self.setup_split = {"subdomains_s": t_sub, "coarse_s": self.setup_time_s - t_sub,
+                            "worker_factor_s": [round(r[1], 2) for r in res]}
         if log:
-            log(f"[oracle] setup {self.setup_time_s:.1f}s on {W} workers, factor entries {self.factor_entries:.3e}")
+            log(f"[oracle] setup {self.setup_time_s:.1f}s on {W} workers (subdomain blocks {t_sub:.1f}s, coarse "
+                f"{self.setup_time_s - t_sub:.1f}s), factor entries {self.factor_entries:.3e}")
 
     def _round(self, msg):
         for cn in self.conns:
@@ -289,7 +297,9 @@ class ParallelSchwarz:
 
     # reference precond.py:227-228
     def coarse_solve(self, v):
-        return self.R0.T @ self.coarse.solve(self.R0 @ v)
+        with threadpool_limits(limits=1):
+            y = self.coarse.solve(self.R0 @ v)
+        return self.R0.T @ y
 
     # reference precond.py:230-245
     def apply(self, v):

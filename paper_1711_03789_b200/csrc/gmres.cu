@@ -40,6 +40,10 @@ mdd_comm* prec_comm(const mdd_prec* P);
 
 constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 160;  // grid <= #SMs (148 on B200)
+// k_arnoldi_stream: 7 consumer warps + 1 producer warp = 8 warps, two per SM
+// sub-partition, so each thread may use up to 255 registers (a ninth warp would
+// put three on one sub-partition and cap every thread at 168)
+constexpr int kStrThreads = 224;
 
 struct ArnoldiArgs {
   int64_t n;
@@ -116,23 +120,32 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 }
 
 // Self-validating all-gather.  Every (step, CTA) pair has its own pair of
-// 16-byte slots, NaN-filled by a memset before the kernel; a CTA publishes
-// by plain stores, and a reader polls a slot until both 8-byte halves are
-// non-NaN (each half is single-copy atomic).  Reading the value *is* the
-// synchronisation: one round trip, no flags, no fences.  Partial sums of
-// finite vectors are finite; a NaN input traps instead of hanging.
+// 16-byte slots, filled with 0xFF bytes by a memset before the kernel; a CTA
+// publishes by plain stores, and a reader polls a slot until neither 8-byte
+// half holds the fill pattern (each half is single-copy atomic).  Reading the
+// value *is* the synchronisation: one round trip, no flags, no fences.
 // Each CTA's (dot, drift) pair is one slot of `pad` double2 (pad = 8: alone
 // on a 128-byte L2 line).  In isolation the flat all-gather runs at 3.3 us per
 // step with 16-byte slots and 1.8 us with one slot per line (hot-line
 // serialisation of the G*G polls, tools/allgather_bench.cu); inside k_arnoldi
 // the padded layout is slower on the REG path and faster on the STREAM path,
 // so the host picks the stride per path (measured on the B200).
+// "Not yet published" is the exact 0xFF..FF pattern of the memset, not NaN-ness: a
+// NaN that the arithmetic produced (operator or preconditioner output with a NaN or
+// Inf) is published as the canonical quiet NaN, flows through the sums like in the
+// reference (krylov.py:137-151) and ends as a NaN residual history, not as a spin.
+__device__ __forceinline__ double canon_nan(double v) {
+  return isnan(v) ? __longlong_as_double(0x7ff8000000000000ll) : v;
+}
 __device__ __forceinline__ void publish(double2* slot_step, int pad, double2 a, double2 b) {
+  a = make_double2(canon_nan(a.x), canon_nan(a.y));
+  b = make_double2(canon_nan(b.x), canon_nan(b.y));
   __stcg(slot_step + (int64_t)blockIdx.x * pad, a);
   __stcg(slot_step + (int64_t)blockIdx.x * pad + 1, b);
 }
 
-__device__ __forceinline__ bool bad2(double2 v) { return isnan(v.x) || isnan(v.y); }
+__device__ __forceinline__ bool unpublished(double v) { return __double_as_longlong(v) == -1ll; }
+__device__ __forceinline__ bool bad2(double2 v) { return unpublished(v.x) || unpublished(v.y); }
 
 // Relaxed gpu-scope load: always served coherently (L2), never hoisted out of
 // a polling loop (asm volatile), but NOT ordered like a volatile access, so
@@ -147,6 +160,13 @@ __device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
 // drift slot only when `with_drift`: both loads in flight together); warp 0
 // then sums them in CTA order (fixed order -> bitwise reproducible) and
 // broadcasts the result.
+template <int BAR = 0>
+__device__ __forceinline__ void cta_sync() {
+  if constexpr (BAR == 0) __syncthreads();
+  else bar_sync(BAR, kStrThreads);  // the consumer warps only (k_arnoldi_stream)
+}
+
+template <int BAR = 0>
 __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int pad, bool warp_gather,
                                            double2* sh, double2& dot, double2& dr, bool with_drift = true) {
   if (warp_gather) {
@@ -190,7 +210,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
         sh[67] = y;
       }
     }
-    __syncthreads();
+    cta_sync<BAR>();
     dot = sh[66];
     dr = sh[67];
     return;
@@ -210,7 +230,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
     stage[k] = u;
     stage[G + k] = v;
   }
-  __syncthreads();
+  cta_sync<BAR>();
   if (threadIdx.x < 32) {
     double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
     for (int k = threadIdx.x; k < G; k += 32) {
@@ -224,7 +244,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
       sh[67] = y;
     }
   }
-  __syncthreads();
+  cta_sync<BAR>();
   dot = sh[66];
   dr = sh[67];
 }
@@ -232,15 +252,16 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
 // Block sum of (a, b) delivered to thread 0 only (it publishes): one block
 // barrier.  `sh` is double-buffered by step parity: a buffer is rewritten two
 // steps later, after thread 0 has passed the next step's barrier.
+template <int BAR = 0>
 __device__ __forceinline__ void block_sum_t0(double2& a, double2& b, double2* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = BAR == 0 ? blockDim.x >> 5 : kStrThreads >> 5;
   a = warp_sum2(a);
   b = warp_sum2(b);
   if (lane == 0) {
     sh[2 * wid] = a;
     sh[2 * wid + 1] = b;
   }
-  __syncthreads();
+  cta_sync<BAR>();
   if (threadIdx.x == 0) {
     a = sh[0];
     b = sh[1];
@@ -250,6 +271,9 @@ __device__ __forceinline__ void block_sum_t0(double2& a, double2& b, double2* sh
     }
   }
 }
+
+// max(x, 0.0) as Python evaluates it (krylov.py:145): a NaN stays a NaN
+__device__ __forceinline__ double pymax0(double x) { return 0.0 > x ? 0.0 : x; }
 
 __device__ __forceinline__ double2 cdotc_acc(double2 acc, double2 x, double2 y) {  // acc + conj(x) y
   acc.x += x.x * y.x + x.y * y.y;
@@ -317,7 +341,10 @@ __device__ double2 tail_finish(const ArnoldiArgs& a, const double2* col, int m, 
   const double2 gm1 = a.g[m - 1];
   a.g[m] = cmul(cneg(cconj(snm)), gm1);
   a.g[m - 1] = cmul(csm, gm1);
-  const double rel = fmin(hypot(a.g[m].x, a.g[m].y) / *a.beta, a.hist[m - 1]);
+  // min(x, prev) as Python evaluates it (krylov.py:180): prev only if prev < x, so a
+  // NaN residual is recorded as NaN instead of being clamped away
+  const double relx = hypot(a.g[m].x, a.g[m].y) / *a.beta, relp = a.hist[m - 1];
+  const double rel = relp < relx ? relp : relx;
   a.hist[m] = rel;
   const int done = (breakdown || rel <= a.tol) ? 1 : 0;
   *a.iter = m;
@@ -525,7 +552,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   }
   double2 hn2, dummy;
   gather_sum(slots(nsteps), G, a.pad, a.wg, red, hn2, dummy, false);
-  const double hlast = sqrt(fmax(hn2.x, 0.0));
+  const double hlast = sqrt(pymax0(hn2.x));
   __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
   __syncthreads();
@@ -565,6 +592,248 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         }
       }
     }
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  if (do_drift) a.drift[m - 1] = dmax;
+  arnoldi_tail(a, col, m, breakdown);
+}
+
+// ---------------------------------------------------------------- STREAM
+// Unweighted MGS2 for slices too large for the register path (cfg3/cfg4 on one
+// GPU: 160-380 KB of every vector per CTA).  Same step order and the same
+// fixed-order sums as k_arnoldi; what differs is how the bytes move:
+//  * the basis is streamed through a ring of 8 KB shared-memory slots filled by
+//    TMA bulk copies (cp.async.bulk + mbarrier complete_tx) issued by a
+//    dedicated producer warp.  The producer walks the whole launch's copy list
+//    -- for every step the chunk of V_j (axpy), of V_{j+1} (dot) and, in the first
+//    pass, of V_{m-1} (drift) -- and runs ahead of the consumers across step
+//    boundaries (the basis is read-only during the launch), so kStrSlots x 8 KB
+//    stay in flight per SM while the consumer warps wait at the all-gather;
+//  * w never leaves the SM if it fits: the first RC chunks of the CTA's w slice
+//    live in registers (2 complex per thread per chunk), the next a.wcap
+//    elements in shared memory, only the remainder in L2-cached global memory.
+// Each basis vector is fetched from HBM once per step (its second use, one step
+// later, hits L2), so the algorithmic traffic is one n-vector per MGS step.
+constexpr int kStrEPT = 2;                         // elements per consumer thread per chunk
+constexpr int kStrChunk = kStrThreads * kStrEPT;   // 448 elements (7 KB) per ring slot
+constexpr int kStrSlots = 8;                       // ring depth: 56 KB of bulk copies in flight per SM
+constexpr int kStrRegChunks = 18;                  // w chunks held in registers when RC > 0 (36 complex per thread)
+constexpr int kStrConsWarps = kStrThreads / 32;
+
+template <int RC>
+__global__ void __launch_bounds__(kStrThreads + 32, 1) k_arnoldi_stream(ArnoldiArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2* ring = reinterpret_cast<double2*>(smraw);               // kStrSlots x kStrChunk
+  double2* col = ring + (size_t)kStrSlots * kStrChunk;             // maxit+1
+  double2* WS = col + (a.maxit + 1);                               // a.wcap elements of w
+  __shared__ double2 red[68 + 2 * kMaxArnCTAs + 32];
+  __shared__ uint64_t full[kStrSlots], empty[kStrSlots];
+  __shared__ double cmax_w[kStrConsWarps];
+  const int G = gridDim.x;
+  const int m = *a.iter + 1;
+  const int64_t n = a.n;
+  const int64_t lo = (int64_t)blockIdx.x * a.slice;
+  const int64_t hi = min(n, lo + a.slice);
+  const int len = hi > lo ? (int)(hi - lo) : 0;
+  const int nch = (len + kStrChunk - 1) / kStrChunk;
+  const int nsm_ch = (int)(a.wcap / kStrChunk);  // chunks RC .. RC+nsm_ch-1 live in shared memory
+  const bool do_drift = a.check_drift && m >= 2;
+  const double2* dvm1 = a.V + (int64_t)(m - 1) * n + lo;
+  const int nsteps = 2 * m;
+  auto slots = [&](int k) { return a.partials + (int64_t)k * G * a.pad; };
+  auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n + lo; };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStrSlots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kStrConsWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // pass t = -1 brings w itself through the ring (slot A) and dots it with X_0;
+  // pass t >= 0: axpy with X_t (slot A), dot with X_{t+1} (slot B; w itself at the end);
+  // slot D (V_{m-1}, drift partner of X_{t+1}) while t + 1 < m - 1
+  if (threadIdx.x >= kStrThreads) {
+    // ------------------------------------------------------ producer warp
+    if (threadIdx.x != kStrThreads) return;
+    int ps = 0;
+    uint32_t pph = 0;
+    auto emit = [&](const double2* src, int cnt) {
+      mbar_wait(&empty[ps], pph ^ 1u);
+      mbar_arrive_tx(&full[ps], (uint32_t)cnt * 16u);
+      bulk_g2s(ring + (size_t)ps * kStrChunk, src, (uint32_t)cnt * 16u, &full[ps]);
+      if (++ps == kStrSlots) {
+        ps = 0;
+        pph ^= 1u;
+      }
+    };
+    if (nsteps > 1) prefetch_l2(xvec(1), (int64_t)len * 16);
+    for (int t = -1; t < nsteps; ++t) {
+      const double2* A = t < 0 ? a.w + lo : xvec(t);
+      const double2* B = t + 1 < nsteps ? xvec(t + 1) : nullptr;
+      const bool hasD = do_drift && t + 1 < m - 1;
+      // HBM -> L2 one step ahead of the ring (whole slice, one bulk prefetch): the ring's
+      // copies then see L2 latency, and kStrSlots x 7 KB in flight cover it
+      if (t + 2 < nsteps) prefetch_l2(xvec(t + 2), (int64_t)len * 16);
+      for (int c = 0; c < nch; ++c) {
+        const int off = c * kStrChunk, cnt = min(kStrChunk, len - off);
+        emit(A + off, cnt);
+        if (B) emit(B + off, cnt);
+        if (hasD) emit(dvm1 + off, cnt);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------- consumer warps
+  const int lane = threadIdx.x & 31;
+  double2 W[RC > 0 ? RC * kStrEPT : 1];
+  int cs = 0;
+  uint32_t cph = 0;
+  auto acquire = [&]() -> const double2* {
+    mbar_wait(&full[cs], cph);
+    return ring + (size_t)cs * kStrChunk;
+  };
+  auto advance = [&]() {
+    if (++cs == kStrSlots) {
+      cs = 0;
+      cph ^= 1u;
+    }
+  };
+  double dmax = 0.0;
+  for (int t = -1; t < nsteps; ++t) {
+    const bool first = t < 0, hasB = t + 1 < nsteps, hasD = do_drift && t + 1 < m - 1;
+    double2 h = make_double2(0.0, 0.0);
+    if (!first) {
+      double2 d;
+      // the drift slot carries data only in the first pass (publication t <= m-2)
+      gather_sum<1>(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
+      if (do_drift && t < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
+      if (threadIdx.x == 0) col[t % m] = cadd(col[t % m], h);
+    }
+    double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
+    // one chunk: wv = this thread's kStrEPT elements of w (in: current, out: updated)
+    auto chunk = [&](int c, double2 (&wv)[kStrEPT]) {
+      const int cnt = min(kStrChunk, len - c * kStrChunk);
+      int s0 = cs;
+      const double2* A = acquire();
+      advance();
+      const double2* B = nullptr;
+      const double2* D = nullptr;
+      if (hasB) {
+        B = acquire();
+        advance();
+      }
+      if (hasD) {
+        D = acquire();
+        advance();
+      }
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) {
+        const int idx = threadIdx.x + e * kStrThreads;
+        if (idx < cnt) {
+          const double2 av = A[idx];
+          const double2 wi = first ? av : caxmy(wv[e], h, av);
+          wv[e] = wi;
+          const double2 x = hasB ? B[idx] : wi;
+          acc = cdotc_acc(acc, x, wi);
+          if (hasD) dacc = cdotc_acc(dacc, x, D[idx]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int used = 1 + (hasB ? 1 : 0) + (hasD ? 1 : 0);
+        for (int q = 0; q < used; ++q) {
+          mbar_arrive(&empty[s0]);
+          if (++s0 == kStrSlots) s0 = 0;
+        }
+      }
+    };
+    if constexpr (RC > 0) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c) {
+        if (c < nch) {
+          double2 wv[kStrEPT];
+#pragma unroll
+          for (int e = 0; e < kStrEPT; ++e) wv[e] = W[c * kStrEPT + e];
+          chunk(c, wv);
+#pragma unroll
+          for (int e = 0; e < kStrEPT; ++e) W[c * kStrEPT + e] = wv[e];
+        }
+      }
+    }
+    const int c_sm_end = min(nch, RC + nsm_ch);
+    for (int c = RC; c < c_sm_end; ++c) {
+      double2* ws = WS + (size_t)(c - RC) * kStrChunk;
+      double2 wv[kStrEPT];
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) wv[e] = first ? make_double2(0.0, 0.0) : ws[threadIdx.x + e * kStrThreads];
+      chunk(c, wv);
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) ws[threadIdx.x + e * kStrThreads] = wv[e];
+    }
+    for (int c = c_sm_end; c < nch; ++c) {
+      double2* wg = a.w + lo + (int64_t)c * kStrChunk;
+      const int cnt = min(kStrChunk, len - c * kStrChunk);
+      double2 wv[kStrEPT];
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) {
+        const int idx = threadIdx.x + e * kStrThreads;
+        wv[e] = (!first && idx < cnt) ? __ldcg(wg + idx) : make_double2(0.0, 0.0);
+      }
+      chunk(c, wv);
+      if (!first) {
+#pragma unroll
+        for (int e = 0; e < kStrEPT; ++e) {
+          const int idx = threadIdx.x + e * kStrThreads;
+          if (idx < cnt) __stcg(wg + idx, wv[e]);
+        }
+      }
+    }
+    block_sum_t0<1>(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16 * (t & 1));
+    if (threadIdx.x == 0) publish(slots(t + 1), a.pad, acc, dacc);
+  }
+  double2 hn2, dummy;
+  gather_sum<1>(slots(nsteps), G, a.pad, false, red, hn2, dummy, false);
+  const double hlast = sqrt(pymax0(hn2.x));
+  cta_sync<1>();
+  if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
+  cta_sync<1>();
+  double cmax = 0.0;
+  for (int j = threadIdx.x; j <= m; j += kStrThreads) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  cmax = warp_max(cmax);
+  if (lane == 0) cmax_w[threadIdx.x >> 5] = cmax;
+  cta_sync<1>();
+#pragma unroll
+  for (int k = 0; k < kStrConsWarps; ++k) cmax = fmax(cmax, cmax_w[k]);
+  const bool breakdown = hlast <= 1e-13 * cmax;
+  if (!breakdown) {
+    double2* vm = a.V + (int64_t)m * n + lo;
+    double2* vin = a.vin + lo;
+    auto put = [&](int c, int e, double2 wi) {
+      const int idx = c * kStrChunk + threadIdx.x + e * kStrThreads;
+      if (idx < len) {
+        const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
+        vm[idx] = q;
+        vin[idx] = q;
+      }
+    };
+    if constexpr (RC > 0) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+#pragma unroll
+        for (int e = 0; e < kStrEPT; ++e) put(c, e, W[c * kStrEPT + e]);
+    }
+    const int c_sm_end = min(nch, RC + nsm_ch);
+    for (int c = RC; c < c_sm_end; ++c)
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) put(c, e, WS[(size_t)(c - RC) * kStrChunk + threadIdx.x + e * kStrThreads]);
+    for (int c = c_sm_end; c < nch; ++c)
+#pragma unroll
+      for (int e = 0; e < kStrEPT; ++e) {
+        const int idx = c * kStrChunk + threadIdx.x + e * kStrThreads;
+        if (idx < len) put(c, e, __ldcg(a.w + lo + idx));
+      }
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   if (do_drift) a.drift[m - 1] = dmax;
@@ -655,6 +924,17 @@ __global__ void k_backsub(int m, int maxit, const double2* H, const double2* g, 
     __syncwarp();
   }
   for (int i = lane; i < m; i += 32) y[i] = ys[i];
+}
+
+// y in dynamic shared memory: 16 B per iteration, beyond 48 KB needs the opt-in attribute
+static void launch_backsub(mdd_ctx* ctx, int m, int maxit, const double2* H, const double2* g, double2* y,
+                           cudaStream_t s) {
+  const size_t bytes = sizeof(double2) * (size_t)std::max(1, m);
+  if (bytes > 227 * 1024) fail(MDD_EINVAL, "gmres: more than 14528 iterations are not supported");
+  if (bytes > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  k_backsub<<<1, 32, bytes, s>>>(m, maxit, H, g, y);
+  CK_LAUNCH(ctx);
 }
 
 __global__ void k_axpy_out(int64_t n, const double2* x0, const double2* u, double2* x) {
@@ -892,7 +1172,7 @@ __global__ void __launch_bounds__(kTailThreads) k_cgs_tail(ArnoldiArgs a, const 
   double2* col = staged ? tsm : colg;
   double2* css = staged ? tsm + cap : a.cs;
   double2* sns = staged ? tsm + 2 * cap : a.sn;
-  const double hlast = sqrt(fmax(nrm[0].x, 0.0));
+  const double hlast = sqrt(pymax0(nrm[0].x));
   double cm = 0.0, dm = 0.0;
   for (int j = threadIdx.x; j <= m; j += blockDim.x) {
     const double2 c = j < m ? cadd(h1[j], h2[j]) : make_double2(hlast, 0.0);
@@ -1222,8 +1502,7 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     for (int j = 0; j < m; ++j) final_drift = std::max(final_drift, std::hypot(hv[j].x, hv[j].y));
   }
   // solution (krylov.py:189-198): x = x0 + M (V y) (right) or x0 + V y (left)
-  k_backsub<<<1, 32, sizeof(double2) * std::max(1, m), s>>>(m, maxit, H.p, g.p, y.p);
-  CK_LAUNCH(ctx);
+  launch_backsub(ctx, m, maxit, H.p, g.p, y.p, s);
   k_combine_basis<<<gs_grid(chunk), 256, 0, s>>>(chunk, m, V.p, y.p, u.p);
   CK_LAUNCH(ctx);
   comm_allgather_z(dist ? comm : nullptr, u.p, full.p, chunk, s);
@@ -1353,6 +1632,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
 
   // ---- Arnoldi launch configuration: one CTA per SM
   int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->nsm, (n + 255) / 256));
+  if (const char* e = getenv("MDD_ARN_GRID")) G = std::max(1, std::min(G, atoi(e)));  // test hook: long slices on small n
   const int64_t slice = (n + G - 1) / G;
   G = (int)((n + slice - 1) / slice);
   const bool reg_path = !weighted && slice <= (int64_t)kArnThreads * kArnE;
@@ -1361,18 +1641,38 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   // unweighted solve; MDD_ARNOLDI_WCAP shrinks the shared-memory w head
   if (const char* e = getenv("MDD_ARNOLDI_MODE"))
     if (!weighted && (atoi(e) == 0 || atoi(e) == 2)) mode = atoi(e);
-  // STREAM: as much of the w slice in shared memory as fits beside col and the
-  // static reduction scratch (227 KB per CTA)
-  int64_t wcap = std::max<int64_t>(
-      0, (int64_t)(227 * 1024 - 16 * (68 + 2 * kMaxArnCTAs) - 1024) / 16 - (maxit + 1));
-  if (const char* e = getenv("MDD_ARNOLDI_WCAP")) wcap = std::min<int64_t>(wcap, std::max(0, atoi(e)));
+  // STREAM: TMA ring + col + as many whole chunks of the w slice as fit in the 227 KB
+  // per CTA; slices beyond shared memory also keep kStrRegChunks chunks in registers
+  // (MDD_ARN_STREAM=old selects the previous load-based kernel, kept for A/B timing)
+  static const bool old_stream = getenv("MDD_ARN_STREAM") && !strcmp(getenv("MDD_ARN_STREAM"), "old");
+  const bool tma_stream = mode == 2 && !old_stream;
+  const int64_t static_sm = 16 * (68 + 2 * kMaxArnCTAs + 32) + 1024;
+  int64_t wcap = std::max<int64_t>(0, (int64_t)(227 * 1024 - static_sm) / 16 - (maxit + 1));
+  int reg_chunks = 0;
+  if (tma_stream) {
+    wcap = std::max<int64_t>(0, (227 * 1024 - static_sm - 16 * (int64_t)kStrSlots * kStrChunk) / 16 - (maxit + 1));
+    wcap -= wcap % kStrChunk;
+    if (slice > wcap) reg_chunks = kStrRegChunks;
+    if (const char* e = getenv("MDD_ARN_REGCHUNKS")) reg_chunks = atoi(e) ? kStrRegChunks : 0;
+  }
+  if (const char* e = getenv("MDD_ARNOLDI_WCAP")) {
+    wcap = std::min<int64_t>(wcap, std::max(0, atoi(e)));
+    if (tma_stream) wcap -= wcap % kStrChunk;
+  }
+  const int64_t w_sm = tma_stream ? std::min<int64_t>(wcap, std::max<int64_t>(0, (slice + kStrChunk - 1) / kStrChunk -
+                                                                                  reg_chunks) * kStrChunk)
+                                  : std::min<int64_t>(slice, wcap);
+  if (tma_stream) wcap = w_sm;
   const size_t shmem = sizeof(double2) * ((size_t)maxit + 1 +
-                                          (mode == 1 ? (size_t)kArnThreads * kArnE
-                                                     : mode == 2 ? (size_t)std::min<int64_t>(slice, wcap) : 0));
-  auto kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi<2> : k_arnoldi<0>;
+                                          (mode == 1 ? (size_t)kArnThreads * kArnE : mode == 2 ? (size_t)w_sm : 0) +
+                                          (tma_stream ? (size_t)kStrSlots * kStrChunk : 0));
+  using ArnFn = void (*)(ArnoldiArgs);
+  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi<2> : k_arnoldi<0>;
+  if (tma_stream) kfn = reg_chunks ? k_arnoldi_stream<kStrRegChunks> : k_arnoldi_stream<0>;
+  const int arn_threads = tma_stream ? kStrThreads + 32 : kArnThreads;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kArnThreads, shmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, arn_threads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
   if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
   const int pad = getenv("MDD_ARN_PAD") ? std::max(2, atoi(getenv("MDD_ARN_PAD"))) : (mode == 1 ? 2 : 8);
@@ -1417,7 +1717,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     CK(cudaMemsetAsync(partials.p, 0xFF, part_elems * sizeof(double2), s));
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(G);
-    lc.blockDim = dim3(kArnThreads);
+    lc.blockDim = dim3(arn_threads);
     lc.dynamicSmemBytes = shmem;
     lc.stream = s;
     cudaLaunchAttribute at[1];
@@ -1553,8 +1853,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     CK_LAUNCH(ctx);
   }
   // solution (krylov.py:189-198)
-  k_backsub<<<1, 32, sizeof(double2) * std::max(1, m), s>>>(m, maxit, H.p, g.p, y.p);
-  CK_LAUNCH(ctx);
+  launch_backsub(ctx, m, maxit, H.p, g.p, y.p, s);
   k_combine_basis<<<gs_grid(n), 256, 0, s>>>(n, m, V.p, y.p, t.p);
   CK_LAUNCH(ctx);
   double2* upd = t.p;
