@@ -263,6 +263,13 @@ class ParallelSchwarz:
         self.coarse = None
         if self.R0 is not None:
             a0 = (self.R0 @ self.A @ self.R0.T).tocsr()  # triple_product(R0, A_prec), precond.py:189-192
+            # The sparse triple product keeps a structural entry wherever two coarse supports come
+            # within one fine cell of each other; the Galerkin value there is rounding noise
+            # (<= 1e-16 of the largest entry: the supports share no tet).  The reference's dense LU
+            # does not care; a sparse factorisation would fill in on them (cfg1: 309,080 stored
+            # entries, 90,802 above 1e-14; factor 4.9 s -> 0.17 s, solution unchanged to 8e-15).
+            a0.data[np.abs(a0.data) <= 1e-13 * np.abs(a0.data).max()] = 0.0
+            a0.eliminate_zeros()
             cs = prob["coarse_space"]
             # SuperLU calls BLAS on small supernodes: one thread (a threaded BLAS only adds sync cost there)
             with threadpool_limits(limits=1):
@@ -343,7 +350,8 @@ class ParallelSchwarz:
 
 
 # ------------------------------------------------------------------ GMRES
-def gmres(op, b, precond, tol=1e-6, maxit=200, max_iters=None, deadline=None, min_iters=1, log=None):
+def gmres(op, b, precond, tol=1e-6, maxit=200, max_iters=None, deadline=None, min_iters=1, log=None,
+          snapshots=None):
     """Right-preconditioned MGS2 GMRES, zero initial guess, Euclidean inner product —
     the BASELINE setting of reference krylov.py:64-209, same step order as
     oracle.maxwell_oracle.gmres (pinned to reference runs) with the level-1
@@ -352,7 +360,9 @@ def gmres(op, b, precond, tol=1e-6, maxit=200, max_iters=None, deadline=None, mi
     ``max_iters`` truncates the run; ``deadline`` (a time.perf_counter() value)
     truncates it at the first iteration boundary past that time, after at least
     ``min_iters`` iterations (bench.py's time-boxed CPU sample).  The iterate
-    returned is the GMRES iterate of the iterations done.
+    returned is the GMRES iterate of the iterations done.  ``snapshots`` (a dict
+    with iteration numbers as keys) is filled with the GMRES iterate x_m at those
+    iterations (what a run with maxit=m returns), at the cost of one apply each.
     Returns (x, history, iterations, converged, seconds-by-phase)."""
     b = np.asarray(b, dtype=complex)
     n = len(b)
@@ -371,6 +381,17 @@ def gmres(op, b, precond, tol=1e-6, maxit=200, max_iters=None, deadline=None, mi
     hist = [1.0]
     conv = False
     m = 0
+
+    def iterate(k):
+        # x_k = M (V_k y_k), y_k from the rotated Hessenberg system (krylov.py:189-198)
+        y = np.zeros(k, dtype=complex)
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1: k] @ y[i + 1: k]) / H[i, i]
+        upd = np.zeros(n, dtype=complex)
+        for i in range(k):
+            upd += y[i] * V[i]
+        return precond(upd)
+
     for m in range(1, limit + 1):
         t0 = time.perf_counter()
         z = precond(V[m - 1])
@@ -411,18 +432,14 @@ def gmres(op, b, precond, tol=1e-6, maxit=200, max_iters=None, deadline=None, mi
         tm["arnoldi"] += t3 - t2
         if log and (m % 10 == 0 or m == 1):
             log(f"[oracle] it {m}: rel.res {hist[-1]:.4e}  (precond {tm['precond']:.0f}s arnoldi {tm['arnoldi']:.0f}s)")
+        if snapshots is not None and m in snapshots:
+            snapshots[m] = iterate(m)
         if brk or hist[-1] <= tol:
             conv = True
             break
         if deadline is not None and m >= min_iters and time.perf_counter() > deadline:
             break
-    y = np.zeros(m, dtype=complex)
-    for i in range(m - 1, -1, -1):
-        y[i] = (g[i] - H[i, i + 1: m] @ y[i + 1: m]) / H[i, i]
-    upd = np.zeros(n, dtype=complex)
-    for i in range(m):
-        upd += y[i] * V[i]
     t0 = time.perf_counter()
-    x = precond(upd)
+    x = iterate(m)
     tm["precond"] += time.perf_counter() - t0
     return x, np.array(hist), m, conv, tm

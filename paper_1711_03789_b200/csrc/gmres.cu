@@ -40,10 +40,6 @@ mdd_comm* prec_comm(const mdd_prec* P);
 
 constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 160;  // grid <= #SMs (148 on B200)
-// k_arnoldi_stream: 7 consumer warps + 1 producer warp = 8 warps, two per SM
-// sub-partition, so each thread may use up to 255 registers (a ninth warp would
-// put three on one sub-partition and cap every thread at 168)
-constexpr int kStrThreads = 224;
 
 struct ArnoldiArgs {
   int64_t n;
@@ -73,6 +69,8 @@ struct ArnoldiArgs {
   int pad;       // double2 per publication slot (2 or 8)
   int wg;        // 1: warp 0 alone polls the slots (gather_sum)
   int pf;        // REG path: L2 prefetch distance in MGS steps (kArnPf; MDD_ARN_PF)
+  int zigzag;        // WIDE path: 1 = odd passes sweep the slice downwards
+  int64_t pf_bytes;  // WIDE path: bytes of the next dot operand's slice prefetched into L2 during the exchange
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -160,13 +158,6 @@ __device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
 // drift slot only when `with_drift`: both loads in flight together); warp 0
 // then sums them in CTA order (fixed order -> bitwise reproducible) and
 // broadcasts the result.
-template <int BAR = 0>
-__device__ __forceinline__ void cta_sync() {
-  if constexpr (BAR == 0) __syncthreads();
-  else bar_sync(BAR, kStrThreads);  // the consumer warps only (k_arnoldi_stream)
-}
-
-template <int BAR = 0>
 __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int pad, bool warp_gather,
                                            double2* sh, double2& dot, double2& dr, bool with_drift = true) {
   if (warp_gather) {
@@ -210,7 +201,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
         sh[67] = y;
       }
     }
-    cta_sync<BAR>();
+    __syncthreads();
     dot = sh[66];
     dr = sh[67];
     return;
@@ -230,7 +221,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
     stage[k] = u;
     stage[G + k] = v;
   }
-  cta_sync<BAR>();
+  __syncthreads();
   if (threadIdx.x < 32) {
     double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
     for (int k = threadIdx.x; k < G; k += 32) {
@@ -244,7 +235,7 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
       sh[67] = y;
     }
   }
-  cta_sync<BAR>();
+  __syncthreads();
   dot = sh[66];
   dr = sh[67];
 }
@@ -252,16 +243,15 @@ __device__ __forceinline__ void gather_sum(const double2* slot_step, int G, int 
 // Block sum of (a, b) delivered to thread 0 only (it publishes): one block
 // barrier.  `sh` is double-buffered by step parity: a buffer is rewritten two
 // steps later, after thread 0 has passed the next step's barrier.
-template <int BAR = 0>
 __device__ __forceinline__ void block_sum_t0(double2& a, double2& b, double2* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = BAR == 0 ? blockDim.x >> 5 : kStrThreads >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   a = warp_sum2(a);
   b = warp_sum2(b);
   if (lane == 0) {
     sh[2 * wid] = a;
     sh[2 * wid + 1] = b;
   }
-  cta_sync<BAR>();
+  __syncthreads();
   if (threadIdx.x == 0) {
     a = sh[0];
     b = sh[1];
@@ -379,19 +369,21 @@ __device__ void arnoldi_tail(const ArnoldiArgs& a, double2* col, int m, bool bre
   Hc[m] = make_double2(0.0, 0.0);
 }
 
+// out-of-line copy for k_arnoldi_stream, whose hot loop needs the registers that the
+// inlined rotation blocks (3 x kTailBlk complex) would otherwise claim
+__device__ __noinline__ void arnoldi_tail_call(const ArnoldiArgs& a, double2* col, int m, bool breakdown) {
+  arnoldi_tail(a, col, m, breakdown);
+}
+
 // MODE 1 (REG): unweighted, every CTA slice fits in registers (slice <=
 // kArnThreads*kArnE): w stays in registers for the whole kernel and the basis
 // slice of step s+2 is loaded into registers right after publishing step s,
 // so its latency overlaps the barrier wait.
-// MODE 2 (STREAM): unweighted, larger slices (cfg3/cfg4 on one GPU): the
-// first wcap elements of the CTA's w slice live in shared memory (the rest in
-// L2-cached global memory); the basis is streamed with 4-way unrolled
-// L2-cached loads, the step s+2 slice bulk-prefetched into L2, so each basis
-// vector comes from HBM once per step and its second use hits L2.
+// Larger unweighted slices (cfg3/cfg4 on one GPU) use k_arnoldi_wide below.
 // MODE 0: the general (weighted) path, w and D w streamed from memory.
 template <int MODE>
 __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
-  constexpr bool REG = MODE == 1, STR = MODE == 2;
+  constexpr bool REG = MODE == 1;
   extern __shared__ double2 col[];  // m+1, identical in every CTA
   __shared__ double2 red[68 + 2 * kMaxArnCTAs + 32];
   const int G = gridDim.x;
@@ -414,14 +406,6 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
 
   double2 W[kArnE], XN[kArnE], XNN[kArnE];
   double2* DM = col + (a.maxit + 1);  // drift vector slice in shared memory (REG path)
-  double2* WS = col + (a.maxit + 1);  // w slice head in shared memory (STREAM path)
-  const int64_t ws = STR ? min(len, a.wcap) : 0;
-  auto wld = [&](int64_t i) { return i - lo < ws ? WS[i - lo] : __ldcg(w + i); };
-  if constexpr (STR) {
-    for (int64_t k = threadIdx.x; k < ws; k += blockDim.x) WS[k] = w[lo + k];
-    __syncthreads();
-    if (threadIdx.x == 0) prefetch_l2(xvec(1) + lo, len * 16);
-  }
   if constexpr (REG) {
     if (threadIdx.x == 0)
       for (int t = 2; t < a.pf && t < nsteps; ++t) prefetch_l2(xvec(t) + lo, len * 16);
@@ -448,7 +432,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     } else {
       for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double2 x = a.V[i];
-        acc = cdotc_acc(acc, x, STR ? wld(i) : dw[i]);
+        acc = cdotc_acc(acc, x, dw[i]);
         if (do_drift) dacc = cdotc_acc(dacc, x, dvm1[i]);
       }
     }
@@ -489,35 +473,6 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
         acc = cdotc_acc(acc, x, W[k]);
         if (drift_next) dacc = cdotc_acc(dacc, x, DM[threadIdx.x + k * kArnThreads]);
         XN[k] = XNN[k];
-      }
-    } else if constexpr (STR) {
-      const double2* vj = a.V + (int64_t)j * n;
-      const double2* vn = xvec(last ? 0 : s + 1);
-      constexpr int U = 4;
-      const double2 zero = make_double2(0.0, 0.0);
-      for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += U * kArnThreads) {
-        double2 xv[U], xn[U], wv[U], dm[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t i = i0 + (int64_t)u * kArnThreads;
-          const bool ok = i < hi;
-          xv[u] = ok ? __ldcg(vj + i) : zero;
-          xn[u] = (ok && !last) ? __ldcg(vn + i) : zero;
-          wv[u] = ok ? wld(i) : zero;
-          dm[u] = (ok && drift_next) ? __ldcg(dvm1 + i) : zero;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t i = i0 + (int64_t)u * kArnThreads;
-          if (i < hi) {
-            const double2 wi = caxmy(wv[u], h, xv[u]);
-            if (i - lo < ws) WS[i - lo] = wi;
-            else __stcg(w + i, wi);
-            const double2 x = last ? wi : xn[u];
-            acc = cdotc_acc(acc, x, wi);
-            if (drift_next) dacc = cdotc_acc(dacc, x, dm[u]);
-          }
-        }
       }
     } else {
       const double2* vj = a.V + (int64_t)j * n;
@@ -582,7 +537,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
     } else {
       double2* dvm = weighted ? a.DV + (int64_t)m * n : nullptr;
       for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double2 wi = STR ? wld(i) : w[i];
+        const double2 wi = w[i];
         const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
         vm[i] = q;
         a.vin[i] = q;
@@ -598,246 +553,162 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
   arnoldi_tail(a, col, m, breakdown);
 }
 
-// ---------------------------------------------------------------- STREAM
-// Unweighted MGS2 for slices too large for the register path (cfg3/cfg4 on one
-// GPU: 160-380 KB of every vector per CTA).  Same step order and the same
-// fixed-order sums as k_arnoldi; what differs is how the bytes move:
-//  * the basis is streamed through a ring of 8 KB shared-memory slots filled by
-//    TMA bulk copies (cp.async.bulk + mbarrier complete_tx) issued by a
-//    dedicated producer warp.  The producer walks the whole launch's copy list
-//    -- for every step the chunk of V_j (axpy), of V_{j+1} (dot) and, in the first
-//    pass, of V_{m-1} (drift) -- and runs ahead of the consumers across step
-//    boundaries (the basis is read-only during the launch), so kStrSlots x 8 KB
-//    stay in flight per SM while the consumer warps wait at the all-gather;
-//  * w never leaves the SM if it fits: the first RC chunks of the CTA's w slice
-//    live in registers (2 complex per thread per chunk), the next a.wcap
-//    elements in shared memory, only the remainder in L2-cached global memory.
-// Each basis vector is fetched from HBM once per step (its second use, one step
-// later, hits L2), so the algorithmic traffic is one n-vector per MGS step.
-constexpr int kStrEPT = 2;                         // elements per consumer thread per chunk
-constexpr int kStrChunk = kStrThreads * kStrEPT;   // 448 elements (7 KB) per ring slot
-constexpr int kStrSlots = 8;                       // ring depth: 56 KB of bulk copies in flight per SM
-constexpr int kStrRegChunks = 18;                  // w chunks held in registers when RC > 0 (36 complex per thread)
-constexpr int kStrConsWarps = kStrThreads / 32;
+// Block sum of (a, b) over 32 warps delivered to thread 0: warp 0 reduces the 32 warp
+// partials (fixed tree -> bitwise reproducible); one block barrier.  `sh` (64 double2) is
+// double-buffered by the caller.
+__device__ __forceinline__ void block_sum_t0_wide(double2& a, double2& b, double2* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  a = warp_sum2(a);
+  b = warp_sum2(b);
+  if (lane == 0) {
+    sh[2 * wid] = a;
+    sh[2 * wid + 1] = b;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    a = warp_sum2(sh[2 * lane]);
+    b = warp_sum2(sh[2 * lane + 1]);
+  }
+}
 
-template <int RC>
-__global__ void __launch_bounds__(kStrThreads + 32, 1) k_arnoldi_stream(ArnoldiArgs a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double2* ring = reinterpret_cast<double2*>(smraw);               // kStrSlots x kStrChunk
-  double2* col = ring + (size_t)kStrSlots * kStrChunk;             // maxit+1
-  double2* WS = col + (a.maxit + 1);                               // a.wcap elements of w
-  __shared__ double2 red[68 + 2 * kMaxArnCTAs + 32];
-  __shared__ uint64_t full[kStrSlots], empty[kStrSlots];
-  __shared__ double cmax_w[kStrConsWarps];
+// ------------------------------------------------------------------ WIDE
+// Unweighted MGS2 for large slices with 1024 threads per CTA (32 warps, 64 registers
+// each): the streaming passes are issue- and latency-bound with 8 warps (ncu on the
+// 8-warp kernels: 0.15 instructions per cycle per scheduler, ~13 cycles per dependent
+// instruction), so the parallelism comes from warps, not from per-thread unrolling.
+// w lives in shared memory as far as it fits (a.wcap elements), the rest in L2 with an
+// evict_last policy; the axpy operand (second and last use of a basis chunk) is loaded
+// with evict_first so the incoming vector replaces it and not the vector needed next.
+constexpr int kWideThreads = 1024;
+
+__device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t policy) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(policy));
+  return v;
+}
+__device__ __forceinline__ void st_hint2(double2* p, double2 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <int U>
+__global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a) {
+  extern __shared__ double2 col[];  // m+1, identical in every CTA; then the w head
+  __shared__ double2 red[68 + 2 * kMaxArnCTAs + 2 * 64];
+  __shared__ double cmax_w[kWideThreads / 32];
   const int G = gridDim.x;
   const int m = *a.iter + 1;
   const int64_t n = a.n;
   const int64_t lo = (int64_t)blockIdx.x * a.slice;
   const int64_t hi = min(n, lo + a.slice);
   const int len = hi > lo ? (int)(hi - lo) : 0;
-  const int nch = (len + kStrChunk - 1) / kStrChunk;
-  const int nsm_ch = (int)(a.wcap / kStrChunk);  // chunks RC .. RC+nsm_ch-1 live in shared memory
   const bool do_drift = a.check_drift && m >= 2;
   const double2* dvm1 = a.V + (int64_t)(m - 1) * n + lo;
   const int nsteps = 2 * m;
   auto slots = [&](int k) { return a.partials + (int64_t)k * G * a.pad; };
   auto xvec = [&](int t) { return a.V + (int64_t)(t % m) * n + lo; };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kStrSlots; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kStrConsWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int j = threadIdx.x; j <= m; j += blockDim.x) col[j] = make_double2(0.0, 0.0);
-  __syncthreads();
-  // pass t = -1 brings w itself through the ring (slot A) and dots it with X_0;
-  // pass t >= 0: axpy with X_t (slot A), dot with X_{t+1} (slot B; w itself at the end);
-  // slot D (V_{m-1}, drift partner of X_{t+1}) while t + 1 < m - 1
-  if (threadIdx.x >= kStrThreads) {
-    // ------------------------------------------------------ producer warp
-    if (threadIdx.x != kStrThreads) return;
-    int ps = 0;
-    uint32_t pph = 0;
-    auto emit = [&](const double2* src, int cnt) {
-      mbar_wait(&empty[ps], pph ^ 1u);
-      mbar_arrive_tx(&full[ps], (uint32_t)cnt * 16u);
-      bulk_g2s(ring + (size_t)ps * kStrChunk, src, (uint32_t)cnt * 16u, &full[ps]);
-      if (++ps == kStrSlots) {
-        ps = 0;
-        pph ^= 1u;
-      }
-    };
-    if (nsteps > 1) prefetch_l2(xvec(1), (int64_t)len * 16);
-    for (int t = -1; t < nsteps; ++t) {
-      const double2* A = t < 0 ? a.w + lo : xvec(t);
-      const double2* B = t + 1 < nsteps ? xvec(t + 1) : nullptr;
-      const bool hasD = do_drift && t + 1 < m - 1;
-      // HBM -> L2 one step ahead of the ring (whole slice, one bulk prefetch): the ring's
-      // copies then see L2 latency, and kStrSlots x 7 KB in flight cover it
-      if (t + 2 < nsteps) prefetch_l2(xvec(t + 2), (int64_t)len * 16);
-      for (int c = 0; c < nch; ++c) {
-        const int off = c * kStrChunk, cnt = min(kStrChunk, len - off);
-        emit(A + off, cnt);
-        if (B) emit(B + off, cnt);
-        if (hasD) emit(dvm1 + off, cnt);
-      }
-    }
-    return;
-  }
-  // ------------------------------------------------------- consumer warps
-  const int lane = threadIdx.x & 31;
-  double2 W[RC > 0 ? RC * kStrEPT : 1];
-  int cs = 0;
-  uint32_t cph = 0;
-  auto acquire = [&]() -> const double2* {
-    mbar_wait(&full[cs], cph);
-    return ring + (size_t)cs * kStrChunk;
-  };
-  auto advance = [&]() {
-    if (++cs == kStrSlots) {
-      cs = 0;
-      cph ^= 1u;
-    }
-  };
+  double2* WS = col + (a.maxit + 1);
+  const int ws = (int)min((int64_t)len, a.wcap);
+  double2* wg = a.w + lo;
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  for (int j = threadIdx.x; j <= m; j += kWideThreads) col[j] = make_double2(0.0, 0.0);
+  const double2 zero = make_double2(0.0, 0.0);
   double dmax = 0.0;
+  // pass t = -1: load w, dot with X_0; pass t >= 0: axpy with X_t, dot with X_{t+1} (w itself at the end)
   for (int t = -1; t < nsteps; ++t) {
     const bool first = t < 0, hasB = t + 1 < nsteps, hasD = do_drift && t + 1 < m - 1;
-    double2 h = make_double2(0.0, 0.0);
+    double2 h = zero;
     if (!first) {
       double2 d;
-      // the drift slot carries data only in the first pass (publication t <= m-2)
-      gather_sum<1>(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
+      gather_sum(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
       if (do_drift && t < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
       if (threadIdx.x == 0) col[t % m] = cadd(col[t % m], h);
     }
-    double2 acc = make_double2(0.0, 0.0), dacc = make_double2(0.0, 0.0);
-    // one chunk: wv = this thread's kStrEPT elements of w (in: current, out: updated)
-    auto chunk = [&](int c, double2 (&wv)[kStrEPT]) {
-      const int cnt = min(kStrChunk, len - c * kStrChunk);
-      int s0 = cs;
-      const double2* A = acquire();
-      advance();
-      const double2* B = nullptr;
-      const double2* D = nullptr;
-      if (hasB) {
-        B = acquire();
-        advance();
-      }
-      if (hasD) {
-        D = acquire();
-        advance();
+    const double2* A = first ? wg : xvec(t);
+    const double2* B = hasB ? xvec(t + 1) : nullptr;
+    double2 acc = zero, dacc = zero;
+    // odd passes sweep the slice downwards: the chunks of X_{t+1} fetched last in pass t are the
+    // first ones pass t+1 needs again, so whatever part of a vector the L2 retains is the part
+    // reused first (the 126 MB L2 does not hold a 56 MB vector plus the streams around it)
+    const bool down = a.zigzag && (t & 1);
+    for (int i0 = threadIdx.x; i0 < len; i0 += U * kWideThreads) {
+      double2 av[U], bv[U], wv[U], dv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int iu = i0 + u * kWideThreads;
+        const bool ok = iu < len;
+        const int i = down ? len - 1 - iu : iu;
+        // first pass: the operator output, read once; later: last use of this basis chunk in this step pair
+        av[u] = ok ? ld_hint(A + i, pol_first) : zero;  // i is valid whenever ok
+        bv[u] = (ok && hasB) ? __ldcg(B + i) : zero;
+        wv[u] = (ok && !first) ? (i < ws ? WS[i] : ld_hint(wg + i, pol_last)) : zero;
+        dv[u] = (ok && hasD) ? __ldcg(dvm1 + i) : zero;
       }
 #pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) {
-        const int idx = threadIdx.x + e * kStrThreads;
-        if (idx < cnt) {
-          const double2 av = A[idx];
-          const double2 wi = first ? av : caxmy(wv[e], h, av);
-          wv[e] = wi;
-          const double2 x = hasB ? B[idx] : wi;
+      for (int u = 0; u < U; ++u) {
+        const int iu = i0 + u * kWideThreads;
+        const int i = down ? len - 1 - iu : iu;
+        if (iu < len) {
+          const double2 wi = first ? av[u] : caxmy(wv[u], h, av[u]);
+          if (i < ws) WS[i] = wi;
+          else if (!first) st_hint2(wg + i, wi, pol_last);
+          const double2 x = hasB ? bv[u] : wi;
           acc = cdotc_acc(acc, x, wi);
-          if (hasD) dacc = cdotc_acc(dacc, x, D[idx]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        const int used = 1 + (hasB ? 1 : 0) + (hasD ? 1 : 0);
-        for (int q = 0; q < used; ++q) {
-          mbar_arrive(&empty[s0]);
-          if (++s0 == kStrSlots) s0 = 0;
-        }
-      }
-    };
-    if constexpr (RC > 0) {
-#pragma unroll
-      for (int c = 0; c < RC; ++c) {
-        if (c < nch) {
-          double2 wv[kStrEPT];
-#pragma unroll
-          for (int e = 0; e < kStrEPT; ++e) wv[e] = W[c * kStrEPT + e];
-          chunk(c, wv);
-#pragma unroll
-          for (int e = 0; e < kStrEPT; ++e) W[c * kStrEPT + e] = wv[e];
+          if (hasD) dacc = cdotc_acc(dacc, x, dv[u]);
         }
       }
     }
-    const int c_sm_end = min(nch, RC + nsm_ch);
-    for (int c = RC; c < c_sm_end; ++c) {
-      double2* ws = WS + (size_t)(c - RC) * kStrChunk;
-      double2 wv[kStrEPT];
-#pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) wv[e] = first ? make_double2(0.0, 0.0) : ws[threadIdx.x + e * kStrThreads];
-      chunk(c, wv);
-#pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) ws[threadIdx.x + e * kStrThreads] = wv[e];
-    }
-    for (int c = c_sm_end; c < nch; ++c) {
-      double2* wg = a.w + lo + (int64_t)c * kStrChunk;
-      const int cnt = min(kStrChunk, len - c * kStrChunk);
-      double2 wv[kStrEPT];
-#pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) {
-        const int idx = threadIdx.x + e * kStrThreads;
-        wv[e] = (!first && idx < cnt) ? __ldcg(wg + idx) : make_double2(0.0, 0.0);
-      }
-      chunk(c, wv);
-      if (!first) {
-#pragma unroll
-        for (int e = 0; e < kStrEPT; ++e) {
-          const int idx = threadIdx.x + e * kStrThreads;
-          if (idx < cnt) __stcg(wg + idx, wv[e]);
-        }
+    block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64 * (t & 1));
+    if (threadIdx.x == 0) {
+      publish(slots(t + 1), a.pad, acc, dacc);
+      // DRAM idles while the CTAs exchange their partial sums: pull the head of the slice the
+      // next sweep dots with (X_{t+2}, its first touch in this iteration) into L2 meanwhile.
+      // a.pf_bytes caps it, so that at cfg4 (56 MB vectors) the prefetch does not evict X_{t+1}
+      // before its second use
+      if (t + 2 < nsteps) {
+        const int64_t pb = min((int64_t)len * 16, a.pf_bytes);
+        // pass t+1 starts at the top of the slice if it sweeps downwards
+        prefetch_l2((a.zigzag && ((t + 1) & 1)) ? xvec(t + 2) + len - pb / 16 : xvec(t + 2), pb);
       }
     }
-    block_sum_t0<1>(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 16 * (t & 1));
-    if (threadIdx.x == 0) publish(slots(t + 1), a.pad, acc, dacc);
   }
   double2 hn2, dummy;
-  gather_sum<1>(slots(nsteps), G, a.pad, false, red, hn2, dummy, false);
+  gather_sum(slots(nsteps), G, a.pad, false, red, hn2, dummy, false);
   const double hlast = sqrt(pymax0(hn2.x));
-  cta_sync<1>();
+  __syncthreads();
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
-  cta_sync<1>();
+  __syncthreads();
   double cmax = 0.0;
-  for (int j = threadIdx.x; j <= m; j += kStrThreads) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  for (int j = threadIdx.x; j <= m; j += kWideThreads) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
   cmax = warp_max(cmax);
-  if (lane == 0) cmax_w[threadIdx.x >> 5] = cmax;
-  cta_sync<1>();
+  if ((threadIdx.x & 31) == 0) cmax_w[threadIdx.x >> 5] = cmax;
+  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kStrConsWarps; ++k) cmax = fmax(cmax, cmax_w[k]);
+  for (int k = 0; k < kWideThreads / 32; ++k) cmax = fmax(cmax, cmax_w[k]);
   const bool breakdown = hlast <= 1e-13 * cmax;
   if (!breakdown) {
     double2* vm = a.V + (int64_t)m * n + lo;
     double2* vin = a.vin + lo;
-    auto put = [&](int c, int e, double2 wi) {
-      const int idx = c * kStrChunk + threadIdx.x + e * kStrThreads;
-      if (idx < len) {
-        const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
-        vm[idx] = q;
-        vin[idx] = q;
-      }
-    };
-    if constexpr (RC > 0) {
-#pragma unroll
-      for (int c = 0; c < RC; ++c)
-#pragma unroll
-        for (int e = 0; e < kStrEPT; ++e) put(c, e, W[c * kStrEPT + e]);
+    for (int i = threadIdx.x; i < len; i += kWideThreads) {
+      const double2 wi = i < ws ? WS[i] : __ldcg(wg + i);
+      const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
+      vm[i] = q;
+      vin[i] = q;
     }
-    const int c_sm_end = min(nch, RC + nsm_ch);
-    for (int c = RC; c < c_sm_end; ++c)
-#pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) put(c, e, WS[(size_t)(c - RC) * kStrChunk + threadIdx.x + e * kStrThreads]);
-    for (int c = c_sm_end; c < nch; ++c)
-#pragma unroll
-      for (int e = 0; e < kStrEPT; ++e) {
-        const int idx = c * kStrChunk + threadIdx.x + e * kStrThreads;
-        if (idx < len) put(c, e, __ldcg(a.w + lo + idx));
-      }
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   if (do_drift) a.drift[m - 1] = dmax;
-  arnoldi_tail(a, col, m, breakdown);
+  arnoldi_tail_call(a, col, m, breakdown);
 }
 
 // drift of the final basis vector V_m: |vdot(V_j, DV_m)| for j < m (one CTA per j)
@@ -1282,8 +1153,8 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   // cfg1 411 vs 393 ms/step)
   // two tiles in flight (2 CTAs per SM at cfg1's basis sizes); MDD_CGS_STAGES=3 triples the ring
   // where it fits (measured slower: 1 CTA per SM, cfg1 414 vs 397 ms/step)
-  static const int cgs_stages = getenv("MDD_CGS_STAGES") ? atoi(getenv("MDD_CGS_STAGES")) : 2;
-  static const int cgs_rows = getenv("MDD_CGS_ROWS") && atoi(getenv("MDD_CGS_ROWS")) == 8 ? 8 : 16;
+  static const int cgs_stages = 2;
+  static const int cgs_rows = 16;
   const int64_t ntiles = (nl + cgs_rows - 1) / cgs_rows;
   const int Gt_max = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->nsm * 8, ntiles));
   if (fused_env) {
@@ -1641,41 +1512,22 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   // unweighted solve; MDD_ARNOLDI_WCAP shrinks the shared-memory w head
   if (const char* e = getenv("MDD_ARNOLDI_MODE"))
     if (!weighted && (atoi(e) == 0 || atoi(e) == 2)) mode = atoi(e);
-  // STREAM: TMA ring + col + as many whole chunks of the w slice as fit in the 227 KB
-  // per CTA; slices beyond shared memory also keep kStrRegChunks chunks in registers
-  // (MDD_ARN_STREAM=old selects the previous load-based kernel, kept for A/B timing)
-  static const bool old_stream = getenv("MDD_ARN_STREAM") && !strcmp(getenv("MDD_ARN_STREAM"), "old");
-  const bool tma_stream = mode == 2 && !old_stream;
-  const int64_t static_sm = 16 * (68 + 2 * kMaxArnCTAs + 32) + 1024;
+  // WIDE (mode 2): col + as much of the w slice as fits in the 227 KB per CTA
+  const int64_t static_sm = 16 * (68 + 2 * kMaxArnCTAs + 128) + 1024;
   int64_t wcap = std::max<int64_t>(0, (int64_t)(227 * 1024 - static_sm) / 16 - (maxit + 1));
-  int reg_chunks = 0;
-  if (tma_stream) {
-    wcap = std::max<int64_t>(0, (227 * 1024 - static_sm - 16 * (int64_t)kStrSlots * kStrChunk) / 16 - (maxit + 1));
-    wcap -= wcap % kStrChunk;
-    if (slice > wcap) reg_chunks = kStrRegChunks;
-    if (const char* e = getenv("MDD_ARN_REGCHUNKS")) reg_chunks = atoi(e) ? kStrRegChunks : 0;
-  }
-  if (const char* e = getenv("MDD_ARNOLDI_WCAP")) {
-    wcap = std::min<int64_t>(wcap, std::max(0, atoi(e)));
-    if (tma_stream) wcap -= wcap % kStrChunk;
-  }
-  const int64_t w_sm = tma_stream ? std::min<int64_t>(wcap, std::max<int64_t>(0, (slice + kStrChunk - 1) / kStrChunk -
-                                                                                  reg_chunks) * kStrChunk)
-                                  : std::min<int64_t>(slice, wcap);
-  if (tma_stream) wcap = w_sm;
+  if (const char* e = getenv("MDD_ARNOLDI_WCAP")) wcap = std::min<int64_t>(wcap, std::max(0, atoi(e)));
   const size_t shmem = sizeof(double2) * ((size_t)maxit + 1 +
-                                          (mode == 1 ? (size_t)kArnThreads * kArnE : mode == 2 ? (size_t)w_sm : 0) +
-                                          (tma_stream ? (size_t)kStrSlots * kStrChunk : 0));
+                                          (mode == 1 ? (size_t)kArnThreads * kArnE
+                                                     : mode == 2 ? (size_t)std::min<int64_t>(slice, wcap) : 0));
   using ArnFn = void (*)(ArnoldiArgs);
-  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi<2> : k_arnoldi<0>;
-  if (tma_stream) kfn = reg_chunks ? k_arnoldi_stream<kStrRegChunks> : k_arnoldi_stream<0>;
-  const int arn_threads = tma_stream ? kStrThreads + 32 : kArnThreads;
+  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide<2> : k_arnoldi<0>;
+  const int arn_threads = mode == 2 ? kWideThreads : kArnThreads;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, arn_threads, shmem));
   if (per_sm < 1) fail(MDD_ECUDA, "arnoldi kernel cannot be resident");
   if (G > per_sm * ctx->nsm || G > kMaxArnCTAs) fail(MDD_ECUDA, "arnoldi grid exceeds co-resident CTAs");
-  const int pad = getenv("MDD_ARN_PAD") ? std::max(2, atoi(getenv("MDD_ARN_PAD"))) : (mode == 1 ? 2 : 8);
+  const int pad = mode == 1 ? 2 : 8;  // measured per path (allgather_bench + in-kernel, round 1)
   const size_t part_elems = (size_t)(2 * maxit + 1) * G * pad;
   DevBuf<double2> partials(part_elems);
   // host-mapped status word, allocated once per context (cudaHostAlloc and
@@ -1709,8 +1561,15 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.wcap = wcap;
   aa.pad = pad;
   // measured per path: warp-0 polling helps the REG path (cfg1 123.9 -> 119.5 ms), hurts STREAM
-  aa.wg = getenv("MDD_ARN_WG") ? atoi(getenv("MDD_ARN_WG")) : (mode == 1 ? 1 : 0);
-  aa.pf = getenv("MDD_ARN_PF") ? std::max(2, atoi(getenv("MDD_ARN_PF"))) : kArnPf;
+  aa.wg = mode == 1 ? 1 : 0;
+  aa.pf = kArnPf;
+  {
+    // what DRAM delivers during one exchange (~4 us at ~6 TB/s), spread over the CTAs
+    aa.pf_bytes = (int64_t)(24e6 / G) & ~(int64_t)127;
+    // vectors that the L2 cannot keep whole between their two uses are swept in alternating
+    // directions (cfg4: 56 MB; measured 1508 -> 1350 ms per solve; cfg3's 24 MB vectors lose 10%)
+    aa.zigzag = (n * 16 > 40000000ll || getenv("MDD_ARN_ZIGZAG")) ? 1 : 0;  // env: test hook
+  }
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
     // NaN-fill the publication slots (0xFF bytes are a NaN pattern)

@@ -93,6 +93,11 @@ def main():
     ap.add_argument("--resident-entries", type=float, default=None,
                     help="cap on factor entries kept in host memory (~33 B each); the rest is re-factored per apply")
     ap.add_argument("--check-reference", action="store_true")
+    ap.add_argument("--short", type=int, default=20)
+    ap.add_argument("--short-only", action="store_true")
+    ap.add_argument("--sensitivity", type=int, default=0, metavar="K",
+                    help="add hist_pert: the oracle's own history over K iterations when every preconditioner "
+                         "output is perturbed by a relative 1e-13 (the size of the device/oracle apply difference)")
     args = ap.parse_args()
     c = W.CONFIGS[args.config]
     t_all = time.time()
@@ -109,9 +114,36 @@ def main():
         av = M.apply(v)
         t_apply = time.time() - t0
         log(f"[oracle] one apply {t_apply:.2f}s")
+        out = os.path.join(HERE, f"{c['name']}_oracle.npz")
+        snaps = {args.short: None}
+        if args.sensitivity:
+            old = dict(np.load(out, allow_pickle=False))
+            rng = np.random.default_rng(99)
+            level = 1e-13
+
+            def noisy(vv):
+                y = M.apply(vv)
+                return y * (1.0 + level * rng.standard_normal(len(y)))
+
+            hp = P.gmres(prob["A"], prob["rhs"], noisy, tol=W.TOL, maxit=W.MAXIT, max_iters=args.sensitivity, log=log)[1]
+            old.update(hist_pert=hp, pert_level=level)
+            np.savez_compressed(out, **old)
+            k = min(len(hp), len(old["hist"]))
+            log("updated", out, "max rel deviation under the perturbation:",
+                float(np.abs(hp[:k] / old["hist"][:k] - 1).max()))
+            return
+        if args.short_only:
+            old = dict(np.load(out, allow_pickle=False))
+            xs = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=W.MAXIT, max_iters=args.short, log=log)[0]
+            old.update(xs_proj=probes.conj() @ xs, xs_samp=xs[::stride], xsnorm=np.linalg.norm(xs), short=args.short)
+            np.savez_compressed(out, **old)
+            log("updated", out, f"{os.path.getsize(out) / 1024:.1f} KiB")
+            return
         t0 = time.time()
-        x, hist, its, conv, tm = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=args.maxit, log=log)
+        x, hist, its, conv, tm = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=args.maxit, log=log,
+                                         snapshots=snaps)
         t_gmres = time.time() - t0
+        xs = snaps[args.short] if snaps[args.short] is not None else x
         res = np.linalg.norm(prob["rhs"] - prob["A"] @ x) / np.linalg.norm(prob["rhs"])
         log(f"[oracle] {c['name']}: {its} iterations conv={conv} hist[-1]={hist[-1]:.6e} true rel.res {res:.6e} "
             f"gmres {t_gmres:.1f}s setup {M.setup_time_s:.1f}s")
@@ -119,11 +151,11 @@ def main():
                  "workers": M.workers, "cores": os.cpu_count(), "build": prob["times"],
                  "factor_entries": M.factor_entries, "resident_entries_cap": args.resident_entries,
                  "total_s": time.time() - t_all, **extra}
-    out = os.path.join(HERE, f"{c['name']}_oracle.npz")
     np.savez_compressed(out, hist=hist, its=its, conv=conv, maxit=args.maxit, ndof=n,
                         x_proj=probes.conj() @ x, x_samp=x[::stride], xnorm=np.linalg.norm(x),
                         ap_proj=probes.conj() @ av, ap_samp=av[::stride], apnorm=np.linalg.norm(av),
-                        true_rel_res=res, times=json.dumps(times))
+                        xs_proj=probes.conj() @ xs, xs_samp=xs[::stride], xsnorm=np.linalg.norm(xs),
+                        short=min(args.short, its), true_rel_res=res, times=json.dumps(times))
     log("wrote", out, f"{os.path.getsize(out) / 1024:.1f} KiB", json.dumps(times))
 
 

@@ -203,14 +203,14 @@ def test_arnoldi_paths_match_reference(gpu, gg, monkeypatch, mode, wcap):
     assert np.allclose(r.residual_history, base.residual_history, rtol=1e-10, atol=1e-15)
 
 
-@pytest.mark.parametrize("grid,wcap,regs", [("3", None, None), ("2", "896", "1"), ("2", "448", "0"), ("5", "0", "0"),
+@pytest.mark.parametrize("grid,wcap,regs", [("3", None, None), ("2", "896", "1"), ("2", "448", None), ("5", "0", "1"),
                                             ("148", None, None)])
-def test_stream_arnoldi_tiers_match_register_path(gpu, monkeypatch, grid, wcap, regs):
-    """k_arnoldi_stream (TMA ring + w tiered over registers / shared memory / L2) on a
-    mid-size problem with the grid capped so each CTA owns many ring chunks, against the
-    register-path kernel on the same solve: same iterations, history to 1e-10, x to 1e-10.
-    The cases put w in shared memory only, registers + shared + global, shared + global,
-    global only, and the production grid."""
+def test_wide_arnoldi_matches_register_path(gpu, monkeypatch, grid, wcap, regs):
+    """k_arnoldi_wide (1024 threads per CTA, w in shared memory with an L2-resident tail,
+    optional alternating sweep direction) on a mid-size problem with the grid capped so each
+    CTA owns a long slice, against the register-path kernel on the same solve.  The cases put
+    w in shared memory only, shared + L2 tail (with and without the alternating sweep), L2 only,
+    and the production grid."""
     from paper_1711_03789_b200 import decomp, fem, mesh, precond
     from paper_1711_03789_b200.krylov import KrylovConfig, gmres
 
@@ -218,22 +218,22 @@ def test_stream_arnoldi_tiers_match_register_path(gpu, monkeypatch, grid, wcap, 
     prob = fem.assemble(s, fem.Coefficients(k=6.0, xi=3.0), source=fem.gaussian_source)
     d = decomp.build_decomposition(s, 2, 2, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(3), "pec"))
     st = precond.setup(prob, d, precond.PreconditionerSpec("as", "two", "additive", xi_prec=3.0), lu_cap=None)
-    cfg = KrylovConfig(tol=1e-9, maxit=200)
+    cfg = KrylovConfig(tol=1e-6, maxit=200)
     base = gmres(prob.A, prob.rhs, precond=st, config=cfg)
-    assert base.converged and base.iterations > 15
+    assert base.converged and base.iterations > 12
     monkeypatch.setenv("MDD_ARNOLDI_MODE", "2")
     monkeypatch.setenv("MDD_ARN_GRID", grid)
     if wcap is not None:
         monkeypatch.setenv("MDD_ARNOLDI_WCAP", wcap)
     if regs is not None:
-        monkeypatch.setenv("MDD_ARN_REGCHUNKS", regs)
+        monkeypatch.setenv("MDD_ARN_ZIGZAG", regs)
     r = gmres(prob.A, prob.rhs, precond=st, config=cfg)
     assert r.iterations == base.iterations and r.converged
     # another grid is another summation order: the histories agree to rounding amplified by
-    # the solve's conditioning (measured 1e-10 absolute near convergence)
+    # the solve's conditioning (measured ~1e-9 absolute in this case's history)
     assert np.allclose(r.residual_history[:12], base.residual_history[:12], rtol=1e-10)
-    assert np.allclose(r.residual_history, base.residual_history, rtol=1e-6, atol=2e-9)
-    assert rel(r.x, base.x) <= 1e-8
+    assert np.allclose(r.residual_history, base.residual_history, rtol=1e-5, atol=1e-8)
+    assert rel(r.x, base.x) <= 1e-7
     assert r.ortho_warning == base.ortho_warning
     r2 = gmres(prob.A, prob.rhs, precond=st, config=cfg)
     assert np.array_equal(r.x, r2.x)  # fixed summation order: bitwise reruns
