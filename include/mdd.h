@@ -234,9 +234,10 @@ int mdd_prec_coarse_apply(mdd_prec* P, const mdd_complex* v, mdd_complex* out);
 int mdd_prec_apply_bench(mdd_prec* P, int which, int reps, double* ms_per_call);
 /* Multi-GPU sharding (the reference has no distributed code,
  * SPEC.md:8).  Each rank builds its preconditioner over its own block of
- * subdomains (coarse space replicated); attaching a communicator makes the
- * one-level part of every apply a partial sum completed by an in-place NCCL
- * allreduce.  NCCL is resolved with dlopen at first use.  id128 == NULL
+ * subdomains (coarse space replicated); attaching a communicator and the row
+ * ranges (mdd_prec_set_halo) makes the one-level part of every apply a partial
+ * sum completed by a neighbour overlap-sum exchange.  NCCL is resolved with
+ * dlopen at first use.  id128 == NULL
  * creates a one-rank communicator without NCCL (collectives are identities);
  * with an id NCCL is initialised even for one rank. */
 int mdd_comm_unique_id(char* out128);
@@ -244,6 +245,21 @@ int mdd_comm_create(mdd_ctx* ctx, int nranks, int rank, const char* id128, mdd_c
 void mdd_comm_destroy(mdd_comm* c);
 int mdd_comm_info(const mdd_comm* c, int* nranks, int* rank);
 int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm);
+/* Sharded data plane (no reference counterpart).  Rank q owns the rows
+ * [q*ceil(n/N), (q+1)*ceil(n/N)) of every vector and needs the rows [need_lo, need_hi)
+ * (the unknowns of its subdomains, reference precond.py:220, and the columns of its rows
+ * of A, krylov.py:95-97; contiguous because the reference numbering is x-major and a
+ * rank's subdomain block is an x-slab).  After this call the collectives of an apply are:
+ *   prolongation overlap sums  - neighbour ncclSend/ncclRecv of the ghost rows, owner adds
+ *                                (reference precond.py:224, `out[dofs] += u`);
+ *   halo for SpMV/restriction  - neighbour ncclSend/ncclRecv of owned rows, in place;
+ *   coarse restriction         - local product with R0 restricted to the owned columns
+ *                                + ncclAllReduce of the ncs coarse values (reference
+ *                                precond.py:227-228); the coarse solve is replicated.
+ * No collective moves a whole vector. */
+int mdd_prec_set_halo(mdd_prec* P, int64_t need_lo, int64_t need_hi);
+int mdd_prec_halo_info(const mdd_prec* P, int64_t* own_lo, int64_t* own_hi, int64_t* need_lo, int64_t* need_hi,
+                       int64_t* exchanged_rows);
 /* Loopback group (test infrastructure for the multi-rank path on ONE GPU;
  * no reference counterpart): nranks (<= 8) host threads, each with its own
  * context on the same device, join one group; every collective synchronises

@@ -177,6 +177,8 @@ SIGNATURES = {
     "mdd_comm_destroy": (None, [_P]),
     "mdd_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "mdd_prec_set_comm": (C.c_int, [_P, _P]),
+    "mdd_prec_set_halo": (C.c_int, [_P, C.c_int64, C.c_int64]),
+    "mdd_prec_halo_info": (C.c_int, [_P] + [C.POINTER(C.c_int64)] * 5),
     "mdd_prec_refactor": (C.c_int, [_P, _P, C.POINTER(mdd_coeffs)]),
     "mdd_gmres": (
         C.c_int,

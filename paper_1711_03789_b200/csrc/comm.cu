@@ -32,6 +32,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -50,10 +54,15 @@ NcclApi& nccl() {
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(api.h, "ncclAllReduce"));
     api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(api.h, "ncclAllGather"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(api.h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(api.h, "ncclRecv"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(api.h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(api.h, "ncclGroupEnd"));
     api.getErrorString =
         reinterpret_cast<decltype(api.getErrorString)>(dlsym(api.h, "ncclGetErrorString"));
   });
-  if (!api.h || !api.getUniqueId || !api.commInitRank || !api.allReduce || !api.allGather || !api.commDestroy)
+  if (!api.h || !api.getUniqueId || !api.commInitRank || !api.allReduce || !api.allGather || !api.commDestroy ||
+      !api.send || !api.recv || !api.groupStart || !api.groupEnd)
     fail(MDD_ENCCL, "NCCL (libnccl.so.2) is not available");
   return api;
 }
@@ -145,7 +154,143 @@ void loop_allgather(mdd_comm* c, const double2* send, double2* recv, int64_t per
   CK(cudaStreamSynchronize(s));
   loop_barrier(g);  // the send buffers may change again
 }
+// y[i] += x[i]
+__global__ void k_add_into(int64_t n, const double2* __restrict__ x, double2* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cadd(y[i], x[i]);
+}
+unsigned add_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096)); }
+
+void loop_halo_gather(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s) {
+  auto* g = static_cast<LoopGroup*>(c->loop);
+  CK(cudaStreamSynchronize(s));
+  g->bufs[c->rank] = vec;
+  g->count[c->rank] = h->n;
+  g->kind[c->rank] = 3;
+  loop_barrier(g);  // every rank's owned rows are final
+  loop_check(g, c->rank);
+  const int me = c->rank;
+  for (int q = 0; q < g->n; ++q) {
+    if (q == me) continue;
+    const int64_t a = std::max(h->own_lo[q], h->need_lo[me]), b = std::min(h->own_hi[q], h->need_hi[me]);
+    if (b > a)
+      CK(cudaMemcpyAsync(vec + a, g->bufs[q] + a, sizeof(double2) * (b - a), cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  loop_barrier(g);  // the owned rows may change again
+}
+void loop_halo_reduce(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s) {
+  auto* g = static_cast<LoopGroup*>(c->loop);
+  CK(cudaStreamSynchronize(s));
+  g->bufs[c->rank] = vec;
+  g->count[c->rank] = h->n;
+  g->kind[c->rank] = 4;
+  loop_barrier(g);  // every rank's partial sums are final
+  loop_check(g, c->rank);
+  const int me = c->rank;
+  const int64_t lo = h->own_lo[me], hi = h->own_hi[me];
+  // ascending rank order, this rank's own partial in its place: the peers below me are summed
+  // into the stage first, then my partial is added, then the peers above
+  DevBuf<double2> acc(std::max<int64_t>(1, hi - lo));
+  CK(cudaMemsetAsync(acc.p, 0, sizeof(double2) * std::max<int64_t>(1, hi - lo), s));
+  for (int q = 0; q < g->n; ++q) {
+    const int64_t a = std::max(lo, h->need_lo[q]), b = std::min(hi, h->need_hi[q]);
+    if (b > a) {
+      k_add_into<<<add_grid(b - a), 256, 0, s>>>(b - a, g->bufs[q] + a, acc.p + (a - lo));
+      CK(cudaGetLastError());
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  loop_barrier(g);  // nobody reads the partials any more
+  if (hi > lo) CK(cudaMemcpyAsync(vec + lo, acc.p, sizeof(double2) * (hi - lo), cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
 }  // namespace
+
+void comm_halo_setup(mdd_comm* c, mdd_halo* h, int64_t n, int64_t need_lo, int64_t need_hi, cudaStream_t s) {
+  const int N = c ? c->nranks : 1, me = c ? c->rank : 0;
+  const int64_t chunk = (n + N - 1) / N;
+  h->n = n;
+  h->own_lo.assign(N, 0);
+  h->own_hi.assign(N, 0);
+  for (int q = 0; q < N; ++q) {
+    h->own_lo[q] = std::min<int64_t>(n, (int64_t)q * chunk);
+    h->own_hi[q] = std::min<int64_t>(n, h->own_lo[q] + chunk);
+  }
+  need_lo = std::max<int64_t>(0, std::min(need_lo, h->own_lo[me]));
+  need_hi = std::min<int64_t>(n, std::max(need_hi, h->own_hi[me]));
+  // every rank learns every rank's needed range: one allgather of a (lo, hi) pair
+  DevBuf<double2> mine(1), all(N);
+  const double2 v = make_double2((double)need_lo, (double)need_hi);
+  mine.upload(&v, 1, s);
+  if (comm_active(c)) comm_allgather_z(c, mine.p, all.p, 1, s);
+  else CK(cudaMemcpyAsync(all.p, mine.p, sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  std::vector<double2> hv(N);
+  all.download(hv.data(), N, s);
+  CK(cudaStreamSynchronize(s));
+  h->need_lo.assign(N, 0);
+  h->need_hi.assign(N, 0);
+  int64_t stage = 0;
+  for (int q = 0; q < N; ++q) {
+    h->need_lo[q] = (int64_t)hv[q].x;
+    h->need_hi[q] = (int64_t)hv[q].y;
+    if (q != me)
+      stage += std::max<int64_t>(0, std::min(h->own_hi[me], h->need_hi[q]) - std::max(h->own_lo[me], h->need_lo[q]));
+  }
+  h->stage = DevBuf<double2>(std::max<int64_t>(1, stage));
+}
+
+void comm_halo_gather(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s) {
+  if (!comm_active(c)) return;
+  if (c->loop) return loop_halo_gather(c, h, vec, s);
+  NcclApi& a = nccl();
+  const int me = c->rank;
+  ncclComm_t nc = static_cast<ncclComm_t>(c->comm);
+  nccl_check(a.groupStart(), "ncclGroupStart");
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == me) continue;
+    // what q needs of mine; what I need of q's
+    const int64_t sa = std::max(h->own_lo[me], h->need_lo[q]), sb = std::min(h->own_hi[me], h->need_hi[q]);
+    const int64_t ra = std::max(h->own_lo[q], h->need_lo[me]), rb = std::min(h->own_hi[q], h->need_hi[me]);
+    if (sb > sa) nccl_check(a.send(vec + sa, (size_t)(2 * (sb - sa)), ncclFloat64, q, nc, s), "ncclSend");
+    if (rb > ra) nccl_check(a.recv(vec + ra, (size_t)(2 * (rb - ra)), ncclFloat64, q, nc, s), "ncclRecv");
+  }
+  nccl_check(a.groupEnd(), "ncclGroupEnd");
+}
+
+void comm_halo_reduce(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s) {
+  if (!comm_active(c)) return;
+  if (c->loop) return loop_halo_reduce(c, h, vec, s);
+  NcclApi& a = nccl();
+  const int me = c->rank;
+  ncclComm_t nc = static_cast<ncclComm_t>(c->comm);
+  const int64_t lo = h->own_lo[me], hi = h->own_hi[me];
+  nccl_check(a.groupStart(), "ncclGroupStart");
+  int64_t off = 0;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == me) continue;
+    // my partial sums on q's owned rows go to q; q's partial sums on my owned rows come here
+    const int64_t sa = std::max(h->own_lo[q], h->need_lo[me]), sb = std::min(h->own_hi[q], h->need_hi[me]);
+    const int64_t ra = std::max(lo, h->need_lo[q]), rb = std::min(hi, h->need_hi[q]);
+    if (sb > sa) nccl_check(a.send(vec + sa, (size_t)(2 * (sb - sa)), ncclFloat64, q, nc, s), "ncclSend");
+    if (rb > ra) {
+      nccl_check(a.recv(h->stage.p + off, (size_t)(2 * (rb - ra)), ncclFloat64, q, nc, s), "ncclRecv");
+      off += rb - ra;
+    }
+  }
+  nccl_check(a.groupEnd(), "ncclGroupEnd");
+  // owner adds, ascending rank order
+  off = 0;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == me) continue;
+    const int64_t ra = std::max(lo, h->need_lo[q]), rb = std::min(hi, h->need_hi[q]);
+    if (rb > ra) {
+      k_add_into<<<add_grid(rb - ra), 256, 0, s>>>(rb - ra, h->stage.p + off, vec + ra);
+      CK(cudaGetLastError());
+      off += rb - ra;
+    }
+  }
+}
 
 void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
   if (c && c->loop) return loop_allreduce(c, buf, n, s);
@@ -157,8 +302,7 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s) {
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s) {
   if (c && c->loop) return loop_allgather(c, send, recv, per_rank, s);
   if (!c || !c->comm) {
-    double2* dst = recv + (c && c->emulated ? (int64_t)c->rank * per_rank : 0);
-    if (send != dst) CK(cudaMemcpyAsync(dst, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
+    if (send != recv) CK(cudaMemcpyAsync(recv, send, sizeof(double2) * per_rank, cudaMemcpyDeviceToDevice, s));
     return;
   }
   nccl_check(nccl().allGather(send, recv, (size_t)(2 * per_rank), ncclFloat64, static_cast<ncclComm_t>(c->comm), s),
@@ -184,14 +328,11 @@ int mdd_comm_create(mdd_ctx* ctx, int nranks, int rank, const char* id128, mdd_c
   CK(cudaSetDevice(ctx->device));
   // id128 == NULL: a single-rank communicator without NCCL (all collectives
   // are identities); with an id, NCCL is initialised even for one rank
-  const char* emu = getenv("MDD_COMM_EMULATE");
-  const bool emulate = nranks > 1 && !id128 && emu && atoi(emu) != 0;
-  if (nranks > 1 && !id128 && !emulate) fail(MDD_EINVAL, "comm: a unique id is required for more than one rank");
+  if (nranks > 1 && !id128) fail(MDD_EINVAL, "comm: a unique id is required for more than one rank");
   std::unique_ptr<mdd_comm> c(new mdd_comm());
   c->ctx = ctx;
   c->nranks = nranks;
   c->rank = rank;
-  c->emulated = emulate;
   if (id128) {
     ncclUniqueId id;
     memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);

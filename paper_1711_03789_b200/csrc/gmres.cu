@@ -37,6 +37,9 @@ namespace mdd {
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
 bool prec_is_distributed(const mdd_prec* P);
 mdd_comm* prec_comm(const mdd_prec* P);
+mdd_halo* prec_halo(const mdd_prec* P);
+void prec_apply_dist(mdd_prec* P, const double2* v, double2* out, cudaStream_t s);
+void prec_gather_owned(mdd_prec* P, double2* vec, cudaStream_t s);
 
 constexpr int kArnThreads = 256;
 constexpr int kMaxArnCTAs = 160;  // grid <= #SMs (148 on B200)
@@ -1202,23 +1205,39 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     k_slice<<<gs_grid(chunk), 256, 0, s>>>(chunk, nl, src_full + lo, dst);
     CK_LAUNCH(ctx);
   };
+  mdd_halo* halo = dist ? prec_halo(ops->P) : nullptr;
+  if (dist && !halo) fail(MDD_EINVAL, "sharded GMRES: the preconditioner has no row ranges (mdd_prec_set_halo)");
+  // Sharded vectors: `full`, `z` are full-length arrays of which a rank fills its owned rows and,
+  // after a halo gather, its needed rows (the unknowns of its subdomains and the columns of its
+  // rows of A).  No collective moves a whole vector inside the loop.
+  auto spread = [&](const double2* local, double2* vec) {  // owned rows in, needed rows valid
+    if (dist) {
+      if (nl > 0) CK(cudaMemcpyAsync(vec + lo, local, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, s));
+      comm_halo_gather(comm, halo, vec, s);
+    } else {
+      CK(cudaMemcpyAsync(vec, local, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, s));
+    }
+  };
+  // M: needed-valid in -> owned-valid out (sharded); whole vectors otherwise
   auto applyM = [&](const double2* in_full, double2* out_full) {
-    if (ops->P) prec_apply_dev(ops->P, in_full, out_full, s);
+    if (dist) prec_apply_dist(ops->P, in_full, out_full, s);
+    else if (ops->P) prec_apply_dev(ops->P, in_full, out_full, s);
     else spmv_dev(ctx, ops->Mcsr, in_full, out_full, s);
   };
-  // local rows of the (preconditioned) operator applied to a full vector
+  // local rows of the (preconditioned) operator applied to a needed-valid vector
   auto op = [&](const double2* vfull, double2* wl) {
     if (right) {
       const double2* in = vfull;
       if (hasM) {
         applyM(vfull, z.p);
+        if (dist) comm_halo_gather(comm, halo, z.p, s);  // the columns of my rows of A
         in = z.p;
       }
       spmv_rows_dev(ctx, ops->A, lo, nl, in, wl, s);
     } else {
       spmv_rows_dev(ctx, ops->A, lo, nl, vfull, t.p, s);
       if (hasM) {
-        comm_allgather_z(dist ? comm : nullptr, t.p, full.p, chunk, s);
+        spread(t.p, full.p);
         applyM(full.p, z.p);
         slice(z.p, wl);
       } else {
@@ -1241,7 +1260,7 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
     vec_sub(ctx, r, t.p, r, chunk, s);
   }
   if (!right && hasM) {
-    comm_allgather_z(dist ? comm : nullptr, r, full.p, chunk, s);
+    spread(r, full.p);
     applyM(full.p, z.p);
     slice(z.p, r);
   }
@@ -1303,7 +1322,7 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   for (int it = 1; it <= maxit; ++it) {
     const int m = it - 1;  // newest basis vector
     double2* vm = V.p + (int64_t)m * chunk;
-    comm_allgather_z(dist ? comm : nullptr, vm, full.p, chunk, s);
+    spread(vm, full.p);
     op(full.p, w.p);
     const int nd = (cfg->check_drift && m >= 1) ? m : 0;
     const int nv = m + 1;
@@ -1376,12 +1395,13 @@ static void gmres_cgs(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, const m
   launch_backsub(ctx, m, maxit, H.p, g.p, y.p, s);
   k_combine_basis<<<gs_grid(chunk), 256, 0, s>>>(chunk, m, V.p, y.p, u.p);
   CK_LAUNCH(ctx);
-  comm_allgather_z(dist ? comm : nullptr, u.p, full.p, chunk, s);
-  const double2* upd = full.p;
+  spread(u.p, full.p);
+  double2* upd = full.p;
   if (right && hasM) {
     applyM(full.p, z.p);
     upd = z.p;
   }
+  if (dist) prec_gather_owned(ops->P, upd, s);  // once per solve: the caller gets the whole solution
   k_axpy_out<<<gs_grid(n), 256, 0, s>>>(n, x0dev, upd, xout_dev);
   CK_LAUNCH(ctx);
   if (!dio) xo.download(reinterpret_cast<double2*>(x), n, s);

@@ -187,12 +187,20 @@ struct mdd_comm {
   mdd_ctx* ctx = nullptr;
   void* comm = nullptr;
   int nranks = 1, rank = 0;
-  // MDD_COMM_EMULATE=1 and no unique id: rank `rank` of `nranks` runs alone on
-  // this GPU with every collective replaced by its local part (allreduce: none;
-  // allgather: own block only).  Per-rank TIMING of the sharded path with one
-  // GPU; the numbers it computes are not the solve's (tools/rank_emulation.py).
-  bool emulated = false;
   void* loop = nullptr;  // LoopGroup (mdd_comm_create_loopback)
+};
+
+// Row ranges of a sharded vector of length n (global numbering, every rank holds a
+// full-length array of which only its ranges are meaningful).  Rank q OWNS rows
+// [own_lo[q], own_hi[q]) (equal blocks of ceil(n/nranks) rows, gmres_cgs's layout) and
+// NEEDS rows [need_lo[q], need_hi[q]) >= its owned rows: the unknowns of its subdomains
+// (restriction, precond.py:220) and the columns of its rows of A (krylov.py:95-97).
+// The reference numbering is x-major, the subdomain blocks of a rank are x-slabs, so both
+// are contiguous ranges and a halo exchange is a set of in-place range copies.
+struct mdd_halo {
+  int64_t n = 0;
+  std::vector<int64_t> own_lo, own_hi, need_lo, need_hi;
+  mdd::DevBuf<double2> stage;  // overlap sums: the peers' contributions to my owned rows
 };
 
 namespace mdd {
@@ -201,7 +209,16 @@ void comm_allreduce_z(mdd_comm* c, double2* buf, int64_t n, cudaStream_t s);
 // recv[r*per_rank ...] = send of rank r (stream-ordered); one rank: copy
 void comm_allgather_z(mdd_comm* c, const double2* send, double2* recv, int64_t per_rank, cudaStream_t s);
 // true when collectives go through NCCL (any rank count)
-inline bool comm_active(const mdd_comm* c) { return c && (c->comm || c->emulated || c->loop); }
+inline bool comm_active(const mdd_comm* c) { return c && (c->comm || c->loop); }
+// Halo exchange (forward): on entry `vec` is valid on every rank's owned rows; on return it
+// is valid on this rank's needed rows.  Grouped ncclSend/ncclRecv of sub-ranges, in place.
+void comm_halo_gather(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s);
+// Overlap sum (reverse halo): on entry `vec` holds this rank's partial sums on its needed
+// rows; on return its owned rows hold the sum over all ranks (ascending rank order: fixed,
+// bitwise reproducible).  Rows outside the owned range are left as they were.
+void comm_halo_reduce(mdd_comm* c, mdd_halo* h, double2* vec, cudaStream_t s);
+// fills own_*/need_* of every rank from this rank's needed range (one tiny allgather)
+void comm_halo_setup(mdd_comm* c, mdd_halo* h, int64_t n, int64_t need_lo, int64_t need_hi, cudaStream_t s);
 
 // element geometry + 6x6 stiffness / mass (fem.py:154-195); shared by the
 // global assembly, the impras local assembly and the coarse Galerkin kernel

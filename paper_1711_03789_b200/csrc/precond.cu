@@ -86,7 +86,12 @@ struct mdd_prec {
   std::shared_ptr<mdd::PrecCore> core;
   int family = 0, levels = 1, correction = 0;
   const mdd_csr* A_corr = nullptr;
-  mdd_comm* comm = nullptr;  // sharded: partial output summed over ranks
+  mdd_comm* comm = nullptr;  // sharded: this rank holds a block of the subdomains
+  // sharded data plane (mdd_prec_set_halo): row ranges of the overlap sum and of the halo
+  // exchange, and R0 restricted to this rank's owned columns (the coarse restriction is a
+  // local partial product completed by an allreduce of the ncs coarse values)
+  std::shared_ptr<mdd_halo> halo;
+  std::shared_ptr<mdd_csr> R0own;
 };
 
 namespace mdd {
@@ -421,18 +426,9 @@ static void one_level_scatter(mdd_prec* P, const double2* add, double2* out, cud
 bool prec_is_distributed(const mdd_prec* P) { return P && comm_active(P->comm); }
 mdd_comm* prec_comm(const mdd_prec* P) { return P ? P->comm : nullptr; }
 
-// Scatter of the local solutions (+ add).  A sharded preconditioner holds a
-// subset of the subdomains (the coarse space is replicated): its scatter is a
-// partial sum that one in-place allreduce completes before `add` is applied.
+// Scatter of the local solutions (+ add), one GPU.
 static void one_level_finish(mdd_prec* P, const double2* add, double2* out, cudaStream_t s) {
-  if (!prec_is_distributed(P)) {
-    one_level_scatter(P, add, out, s);
-    return;
-  }
-  const int64_t n = P->core->ndof;
-  one_level_scatter(P, nullptr, out, s);
-  comm_allreduce_z(P->comm, out, n, s);
-  if (add) vec_add(P->core->ctx, out, add, out, n, s);
+  one_level_scatter(P, add, out, s);
 }
 
 static void one_level(mdd_prec* P, const double2* v, const double2* add, double2* out,
@@ -449,8 +445,103 @@ static void coarse_solve(mdd_prec* P, const double2* v, double2* out, cudaStream
   spmv_dev(c.ctx, c.R0Tp.get(), c.coarse.xloc.p, out, s);
 }
 
+// out[lo..hi) = (a - b) + c on a row range
+__global__ void k_sub_add_rows(int64_t lo, int64_t hi, const double2* a, const double2* b, const double2* c,
+                               double2* out) {
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 r = csub(a[i], b[i]);
+    if (c) r = cadd(r, c[i]);
+    out[i] = r;
+  }
+}
+
+mdd_halo* prec_halo(const mdd_prec* P) { return P ? P->halo.get() : nullptr; }
+
+// The sharded apply.  Contract: on entry `v` is valid on this rank's NEEDED
+// rows (its subdomains' unknowns); on return `out` is valid on its OWNED rows only.  Exchanges:
+//   restriction       - none here: the caller's halo gather made v[I_l] available (precond.py:220)
+//   prolongation      - comm_halo_reduce: partial sums on ghost rows go to their owners (precond.py:224)
+//   coarse restriction- local partial R0[:, owned] v, ncclAllReduce of ncs values, replicated solve
+//   A_corr products   - halo gather of the operand, rows of this rank (precond.py:240-245)
+void prec_apply_dist(mdd_prec* P, const double2* v, double2* out, cudaStream_t s) {
+  PrecCore& c = *P->core;
+  mdd_ctx* ctx = c.ctx;
+  mdd_halo* h = P->halo.get();
+  if (!h) fail(MDD_EINVAL, "sharded preconditioner without row ranges (mdd_prec_set_halo)");
+  const int me = P->comm->rank;
+  const int64_t lo = h->own_lo[me], hi = h->own_hi[me], nl = hi - lo;
+  auto one = [&](const double2* in, double2* o) {
+    one_level_solve(P, in, s);
+    one_level_scatter(P, nullptr, o, s);
+    comm_halo_reduce(P->comm, h, o, s);
+  };
+  auto coarse = [&](const double2* in, double2* o) {
+    spmv_dev(ctx, P->R0own.get(), in, c.coarse.bloc.p, s);
+    comm_allreduce_z(P->comm, c.coarse.bloc.p, c.coarse.nloc, s);
+    c.coarse.solve(s);
+    spmv_rows_dev(ctx, c.R0Tp.get(), lo, nl, c.coarse.xloc.p, o + lo, s);
+  };
+  auto rows_of_A = [&](double2* x, double2* y) {  // x: owned-valid on entry
+    comm_halo_gather(P->comm, h, x, s);
+    spmv_rows_dev(ctx, P->A_corr, lo, nl, x, y + lo, s);
+  };
+  auto combine = [&](const double2* a, const double2* b, const double2* cc, double2* o) {
+    if (nl > 0) {
+      k_sub_add_rows<<<gsb(ctx, nl), 256, 0, s>>>(lo, hi, a, b, cc, o);
+      CK_LAUNCH(ctx);
+    }
+  };
+  if (P->levels == 1) {
+    one(v, out);
+    return;
+  }
+  double2* gv = c.t1.p;
+  coarse(v, gv);
+  if (P->correction == 0) {  // additive: B1 v + G v
+    one(v, out);
+    if (nl > 0) vec_add(ctx, out + lo, gv + lo, out + lo, nl, s);
+    return;
+  }
+  double2* t = c.t2.p;
+  rows_of_A(gv, t);        // t = A_corr G v   (owned rows)
+  combine(v, t, nullptr, t);  // t = v - A_corr G v
+  comm_halo_gather(P->comm, h, t, s);
+  if (P->correction == 2) {  // adef1: B1 (v - A G v) + G v
+    one(t, out);
+    if (nl > 0) vec_add(ctx, out + lo, gv + lo, out + lo, nl, s);
+    return;
+  }
+  // hybrid: y = B1 t ; out = y - G (A_corr y) + G v
+  double2* y = c.t3.p;
+  one(t, y);
+  rows_of_A(y, t);
+  double2* cy = c.t4.p;
+  coarse(t, cy);
+  combine(y, cy, gv, out);
+}
+
+// owned rows of every rank -> the whole vector on every rank (equal blocks, zero padded)
+void prec_gather_owned(mdd_prec* P, double2* vec, cudaStream_t s) {
+  mdd_halo* h = P->halo.get();
+  const int N = P->comm->nranks, me = P->comm->rank;
+  const int64_t n = h->n, chunk = (n + N - 1) / N, lo = h->own_lo[me], nl = h->own_hi[me] - lo;
+  DevBuf<double2> send(chunk), all((size_t)N * chunk);
+  CK(cudaMemsetAsync(send.p, 0, sizeof(double2) * chunk, s));
+  if (nl > 0) CK(cudaMemcpyAsync(send.p, vec + lo, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, s));
+  comm_allgather_z(P->comm, send.p, all.p, chunk, s);
+  CK(cudaMemcpyAsync(vec, all.p, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));  // the staging buffers go out of scope
+}
+
 void prec_apply_dev(mdd_prec* P, const double2* v, double2* out, cudaStream_t s) {
   PrecCore& c = *P->core;
+  if (prec_is_distributed(P)) {
+    // whole vector in, whole vector out (the Python-level apply and the replicated MGS loop);
+    // the sharded Krylov loop calls prec_apply_dist directly and never completes the vector
+    prec_apply_dist(P, v, out, s);
+    prec_gather_owned(P, out, s);
+    return;
+  }
   if (P->levels == 1) {
     one_level(P, v, nullptr, out, s);
     return;
@@ -1154,6 +1245,8 @@ int mdd_prec_variant(const mdd_prec* base, int family, int levels, int correctio
   P->correction = correction;
   P->A_corr = A_corr ? A_corr : base->A_corr;
   P->comm = base->comm;
+  P->halo = base->halo;
+  P->R0own = base->R0own;
   *out = P.release();
   MDD_API_END
 }
@@ -1226,6 +1319,54 @@ int mdd_prec_set_comm(mdd_prec* P, mdd_comm* comm) {
   MDD_API_BEGIN
   if (comm && comm->ctx != P->core->ctx) fail(MDD_EINVAL, "comm: different context");
   P->comm = comm;
+  MDD_API_END
+}
+
+int mdd_prec_set_halo(mdd_prec* P, int64_t need_lo, int64_t need_hi) {
+  MDD_API_BEGIN
+  if (!P->comm) fail(MDD_EINVAL, "set_halo: attach the communicator first (mdd_prec_set_comm)");
+  PrecCore& c = *P->core;
+  CK(cudaSetDevice(c.ctx->device));
+  cudaStream_t s = c.ctx->stream;
+  auto h = std::make_shared<mdd_halo>();
+  comm_halo_setup(P->comm, h.get(), c.ndof, need_lo, need_hi, s);
+  P->halo = h;
+  P->R0own.reset();
+  if (c.have_coarse) {
+    // R0 (rows in coarse ND order, as the coarse plan expects) restricted to the owned columns
+    const int me = P->comm->rank;
+    const int64_t lo = h->own_lo[me], hi = h->own_hi[me];
+    const mdd_pattern& RP = *c.R0p->pat;
+    std::vector<double> rv(RP.nnz);
+    c.R0p->vals.download(rv.data(), RP.nnz, s);
+    CK(cudaStreamSynchronize(s));
+    std::vector<int32_t> rp(c.ncs + 1, 0), rc;
+    std::vector<double> vals;
+    for (int64_t a = 0; a < c.ncs; ++a) {
+      for (int32_t k = RP.h_rowptr[a]; k < RP.h_rowptr[a + 1]; ++k)
+        if (RP.h_cols[k] >= lo && RP.h_cols[k] < hi) {
+          rc.push_back(RP.h_cols[k]);
+          vals.push_back(rv[k]);
+        }
+      rp[a + 1] = (int32_t)rc.size();
+    }
+    P->R0own = std::shared_ptr<mdd_csr>(csr_host(c.ctx, c.ncs, c.ndof, std::move(rp), std::move(rc), vals).release());
+    CK(cudaStreamSynchronize(s));
+  }
+  MDD_API_END
+}
+
+int mdd_prec_halo_info(const mdd_prec* P, int64_t* own_lo, int64_t* own_hi, int64_t* need_lo, int64_t* need_hi,
+                       int64_t* exchanged_rows) {
+  MDD_API_BEGIN
+  if (!P->halo) fail(MDD_EINVAL, "halo_info: no row ranges set");
+  const mdd_halo& h = *P->halo;
+  const int me = P->comm->rank;
+  *own_lo = h.own_lo[me];
+  *own_hi = h.own_hi[me];
+  *need_lo = h.need_lo[me];
+  *need_hi = h.need_hi[me];
+  *exchanged_rows = (h.need_hi[me] - h.need_lo[me]) - (h.own_hi[me] - h.own_lo[me]);
   MDD_API_END
 }
 

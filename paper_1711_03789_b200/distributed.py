@@ -5,19 +5,23 @@ paper's production runs place one subdomain solve per processor
 (PAPER.md:1754).  Here one process drives one GPU and:
 
 * each rank factorises and solves a contiguous block of subdomains, balanced
-  by local DoF count (:func:`shard_bounds`);
-* the coarse space (a few thousand DoFs) is replicated, so every rank can
-  apply hybrid / ADEF1 corrections without further communication;
-* the one-level output is a partial sum that a single in-place
-  ``ncclAllReduce`` completes (libmdd ``mdd_prec_set_comm``);
-* GMRES either replicates the Krylov vectors (``orthogonalization="mgs"``,
-  the reference's MGS2: every rank runs the same recurrences on the same
-  allreduced vectors) or shards them (``"cgs2"``, the default of the
-  multi-GPU benchmark): rank r owns the contiguous row block
-  :func:`row_block` of every basis vector; per iteration one ncclAllGather
-  assembles the newest basis vector for the preconditioner and the row-block
-  SpMV, and three small ncclAllReduce calls complete the two classical
-  Gram-Schmidt projections and the norm (libmdd gmres.cu, ``gmres_cgs``).
+  by local DoF count (:func:`shard_bounds`); subdomain ids are x-major, so a
+  block is an x-slab of boxes;
+* rank r owns the contiguous row block :func:`row_block` of every vector (the
+  reference numbering is x-major too: an x-slab of unknowns) and needs the rows
+  :func:`needed_rows` -- its subdomains' unknowns (2 overlap layers + 1) and the
+  columns of its rows of A;
+* the collectives of one iteration are neighbour exchanges of those row ranges
+  (libmdd ``mdd_prec_set_halo``): a halo gather before the restriction and
+  before the SpMV, an overlap sum (reverse halo, owner adds) after the
+  prolongation, one ncclAllReduce of the ncs coarse values per coarse solve
+  (the coarse factor is replicated, R0 is restricted to the owned columns),
+  and three small ncclAllReduce calls for the two classical Gram-Schmidt
+  projections and the norm (``orthogonalization="cgs2"``, libmdd gmres.cu
+  ``gmres_cgs``).  No collective moves a whole vector inside the loop;
+* ``orthogonalization="mgs"`` with a sharded preconditioner keeps the Krylov
+  vectors replicated (every apply completes its output with one allgather of
+  the owned blocks): a correctness path, not the fast one.
 
 The NCCL unique id travels over the caller's ``torch.distributed`` process
 group (any backend), NCCL itself is opened by libmdd with ``dlopen``.
@@ -74,40 +78,47 @@ def row_block(n: int, nranks: int, rank: int) -> tuple[int, int]:
     return lo, min(n, lo + chunk)
 
 
+def needed_rows(space, dof_sets, lo: int, hi: int) -> tuple[int, int]:
+    """Rows ``[need_lo, need_hi)`` a rank must hold valid values of before it can apply its
+    block of the preconditioner and its rows ``[lo, hi)`` of A: the unknowns of its subdomains
+    (restriction, reference precond.py:220) and the column support of its rows (reference
+    krylov.py:95-97; the columns of row i are the unknowns of the tets around edge i).  The
+    reference numbering is x-major, so the set is an index range around the owned block."""
+    need_lo, need_hi = lo, hi
+    for d in dof_sets:
+        if len(d):
+            need_lo = min(need_lo, int(d[0]))
+            need_hi = max(need_hi, int(d[-1]) + 1)
+    if hi > lo:
+        m = space.mesh
+        mine = np.zeros(m.n_edges, dtype=bool)
+        mine[space.kept_edges[lo:hi]] = True
+        touched = mine[m.tet_edges].any(axis=1)
+        cols = space.edge_to_dof[m.tet_edges[touched]]
+        cols = cols[cols >= 0]
+        if len(cols):
+            need_lo = min(need_lo, int(cols.min()))
+            need_hi = max(need_hi, int(cols.max()) + 1)
+    return need_lo, need_hi
+
+
 class Communicator:
     """libmdd NCCL communicator for the ranks of a ``torch.distributed`` group.
 
     ``force_nccl`` initialises NCCL even for a single rank (used by the tests
     to exercise the allreduce path on one GPU)."""
 
-    def __init__(self, ctx=None, group=None, force_nccl: bool = False, emulate=None, loopback=None):
+    def __init__(self, ctx=None, group=None, force_nccl: bool = False, loopback=None):
         import torch.distributed as dist
 
         self.ctx = ctx or _lib.get_context()
+        self.is_nccl = False
         if loopback is not None:
             # (LoopbackGroup, rank): ranks are host threads sharing one GPU (tests)
             grp, rank = loopback
             self.rank, self.nranks, self._group = int(rank), grp.nranks, grp
             h = C.c_void_p()
             _lib.check(_lib.lib.mdd_comm_create_loopback(self.ctx.handle, grp.handle, self.rank, C.byref(h)))
-            self.handle = h
-            return
-        if emulate is not None:
-            # (rank, nranks) run alone on this GPU, collectives reduced to their local part:
-            # per-rank timing only (libmdd MDD_COMM_EMULATE, tools/rank_emulation.py)
-            import os
-
-            self.rank, self.nranks = int(emulate[0]), int(emulate[1])
-            h = C.c_void_p()
-            old = os.environ.get("MDD_COMM_EMULATE")
-            os.environ["MDD_COMM_EMULATE"] = "1"
-            try:
-                _lib.check(_lib.lib.mdd_comm_create(self.ctx.handle, self.nranks, self.rank, None, C.byref(h)))
-            finally:
-                if old is None:
-                    del os.environ["MDD_COMM_EMULATE"]
-                else:
-                    os.environ["MDD_COMM_EMULATE"] = old
             self.handle = h
             return
         if dist.is_available() and dist.is_initialized():
@@ -121,6 +132,7 @@ class Communicator:
         h = C.c_void_p()
         _lib.check(_lib.lib.mdd_comm_create(self.ctx.handle, self.nranks, self.rank, uid, C.byref(h)))
         self.handle = h
+        self.is_nccl = uid is not None
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -17,6 +17,7 @@ import time
 from dataclasses import dataclass
 
 import numpy as np
+import scipy.sparse as sp
 
 from . import _lib
 from .decomp import Decomposition, build_pou, impedance_dof_sets, subdomain_boundary_faces
@@ -144,7 +145,20 @@ class PreconditionerState:
         self.coarse_lu = self.factors if spec.levels == "two" else None
         if shard is not None and shard.comm is not None:
             _lib.check(_lib.lib.mdd_prec_set_comm(handle, shard.comm.handle))
+            if shard.comm.nranks > 1 or shard.comm.is_nccl:
+                self._set_halo(shard)
         self.setup_time_s = time.perf_counter() - t0
+
+    def _set_halo(self, shard):
+        """Row ranges of the sharded data plane (libmdd ``mdd_prec_set_halo``): this rank's
+        needed rows are its subdomains' unknowns and the columns of its rows of A (libmdd
+        restricts R0 to this rank's owned columns for the coarse restriction)."""
+        from .distributed import needed_rows, row_block
+
+        lo, hi = row_block(self.ndof, shard.nranks, shard.rank)
+        need_lo, need_hi = needed_rows(self.decomp.space, self.dof_sets, lo, hi)
+        _lib.check(_lib.lib.mdd_prec_set_halo(self._h, int(need_lo), int(need_hi)))
+        self.row_ranges = {"own": (lo, hi), "need": (int(need_lo), int(need_hi))}
 
     # ------------------------------------------------------------- setup
     def _create(self, problem, decomp, spec, prec_coeffs, lu_cap, leaf_size):

@@ -1,11 +1,12 @@
 """Sharded (multi-GPU) preconditioner and Krylov loop: host logic on CPU with
 gloo, world_size 2.
 
-The device path (libmdd ``mdd_prec_set_comm``) completes each rank's partial
-one-level sum with one allreduce and applies the replicated coarse terms
-afterwards; these tests check that decomposition of the work on the oracle:
-the per-rank partial sums, allreduced over gloo, reproduce the full
-one-level, additive, hybrid and ADEF1 applications.  The sharded CGS2 GMRES
+The device path (libmdd ``mdd_prec_set_comm`` + ``mdd_prec_set_halo``) completes each
+rank's partial one-level sum with a neighbour overlap-sum exchange, moves only halo row
+ranges before restrictions and SpMVs, and allreduces the coarse restriction; these tests
+check that decomposition of the work on the oracle: the per-rank partial sums reproduce
+the full one-level, additive, hybrid and ADEF1 applications (allreduced, and through the
+range exchanges restated on gloo send/recv).  The sharded CGS2 GMRES
 of csrc/gmres.cu (``gmres_cgs``: row blocks of ``distributed.row_block``,
 allgather of each new basis vector, allreduced projections and norms) is
 restated step by step on gloo and must reproduce the oracle's MGS2 solve
@@ -23,7 +24,7 @@ import torch.multiprocessing as mp
 from conftest import mesh_dict, rel
 from oracle import maxwell_oracle as O
 from paper_1711_03789_b200 import decomp, fem, mesh
-from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, row_block, shard_bounds
+from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, needed_rows, row_block, shard_bounds
 
 
 def test_shard_bounds_cover_and_balance():
@@ -215,6 +216,156 @@ def test_gloo_two_ranks_sharded_cgs2_gmres():
     errq = ctx.SimpleQueue()
     port = _free_port()
     procs = [ctx.Process(target=_cgs_worker, args=(r, world, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+# ------------------------------------------------------------------ halo data plane
+def test_needed_rows_cover_subdomains_and_matrix_columns():
+    """needed_rows: the range contains the rank's subdomain unknowns and every column of its
+    rows of A (checked against the assembled pattern), and stays an x-slab: far smaller than
+    the whole vector once there are several ranks."""
+    s = fem.build_edge_space(mesh.build_cube_mesh(8), "pec")
+    d = decomp.build_decomposition(s, 4, 1)
+    a = O.assemble(mesh_dict(s.mesh), s.edge_to_dof, s.ndof, 3.0, 9.0)["A"]
+    world = 4
+    for rank in range(world):
+        lo, hi = row_block(s.ndof, world, rank)
+        sh = make_shard(d, rank, world)
+        sets = [d.dofs[i] for i in sh.subdomains]
+        nlo, nhi = needed_rows(s, sets, lo, hi)
+        assert nlo <= lo and hi <= nhi
+        cols = a[lo:hi].indices
+        assert cols.min() >= nlo and cols.max() < nhi
+        for dd in sets:
+            assert dd.min() >= nlo and dd.max() < nhi
+        assert nhi - nlo < 0.8 * s.ndof
+
+
+def _send_recv_ranges(vec, rank, world, ranges):
+    """ranges: list of (peer, send_slice or None, recv_slice or None); blocking, lower rank sends first."""
+    import torch
+
+    for peer, snd, rcv in ranges:
+        def do_send():
+            if snd is not None and snd[1] > snd[0]:
+                dist.send(torch.from_numpy(vec[snd[0]: snd[1]].view(np.float64).copy()), peer)
+
+        def do_recv():
+            if rcv is not None and rcv[1] > rcv[0]:
+                buf = torch.zeros(2 * (rcv[1] - rcv[0]), dtype=torch.float64)
+                dist.recv(buf, peer)
+                return buf.numpy().view(np.complex128)
+            return None
+
+        if rank < peer:
+            do_send()
+            got = do_recv()
+        else:
+            got = do_recv()
+            do_send()
+        yield peer, got
+
+
+def _halo_worker(rank, world, port, errq):
+    """Restatement of the device data plane (csrc/comm.cu comm_halo_gather / comm_halo_reduce,
+    csrc/precond.cu prec_apply_dist) on gloo: owned row blocks, needed row ranges, neighbour
+    range exchanges, owner-side overlap sums in ascending rank order, coarse restriction as a
+    local product with R0[:, owned] + allreduce."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        s = fem.build_edge_space(mesh.build_cube_mesh(6), "pec")
+        d = decomp.build_decomposition(s, 3, 1, coarse_space=fem.build_edge_space(mesh.build_cube_mesh(2), "pec"))
+        a = O.assemble(mesh_dict(s.mesh), s.edge_to_dof, s.ndof, 3.0, 9.0)["A"]
+        n = s.ndof
+        sh = make_shard(d, rank, world)
+        sel = list(sh.subdomains)
+        sets = [d.dofs[i] for i in sel]
+        own = [row_block(n, world, q) for q in range(world)]
+        need = [None] * world
+        dist.all_gather_object(need, needed_rows(s, sets, *own[rank]))
+        lo, hi = own[rank]
+        r0 = d.coarse.R0.tocsr()
+        a0 = (r0 @ a @ r0.T).tocsr()
+        full = O.Schwarz(d.dofs, d.pou, O.minors(a, d.dofs), "ras", "two", "hybrid", R0=r0, A0=a0, A_corr=a,
+                         ndof=n, solver="dense")
+        local = O.Schwarz(sets, [d.pou[i] for i in sel], O.minors(a, sets), "ras", "two", "hybrid", R0=r0, A0=a0,
+                          A_corr=a, ndof=n, solver="dense")
+        isect = lambda p, q: (max(p[0], q[0]), min(p[1], q[1]))  # noqa: E731
+
+        def gather(vec):  # owned-valid -> needed-valid, in place
+            plan = [(q, isect(own[rank], need[q]), isect(own[q], need[rank])) for q in range(world) if q != rank]
+            for (q, got), (_, _, rcv) in zip(_send_recv_ranges(vec, rank, world, plan), plan):
+                if got is not None:
+                    vec[rcv[0]: rcv[1]] = got
+            return vec
+
+        def reduce_(vec):  # partial on needed rows -> complete on owned rows
+            plan = [(q, isect(own[q], need[rank]), isect(own[rank], need[q])) for q in range(world) if q != rank]
+            acc = np.zeros(hi - lo, dtype=complex)
+            parts = {q: (got, rcv) for (q, got), (_, _, rcv) in zip(_send_recv_ranges(vec, rank, world, plan), plan)}
+            for q in range(world):  # ascending rank order, own partial in its place
+                if q == rank:
+                    acc += vec[lo:hi]
+                elif parts[q][0] is not None:
+                    rcv = parts[q][1]
+                    acc[rcv[0] - lo: rcv[1] - lo] += parts[q][0]
+            out = np.full(n, np.nan, dtype=complex)  # only owned rows are defined afterwards
+            out[lo:hi] = acc
+            return out
+
+        def coarse(vec):  # owned-valid in, owned rows out
+            part = r0[:, lo:hi] @ vec[lo:hi]
+            y = local.coarse.solve(_allreduce_z(part))
+            out = np.full(n, np.nan, dtype=complex)
+            out[lo:hi] = r0.T.tocsr()[lo:hi] @ y
+            return out
+
+        def rows_of_a(vec):  # owned-valid in -> gather -> my rows
+            out = np.full(n, np.nan, dtype=complex)
+            out[lo:hi] = a[lo:hi] @ np.nan_to_num(gather(vec))[:]
+            return out
+
+        def one(vec):  # needed-valid in, owned-valid out
+            return reduce_(local.one_level(np.nan_to_num(vec)))
+
+        v = np.random.default_rng(21).standard_normal(n) * (1 - 0.3j)
+        vin = np.full(n, np.nan, dtype=complex)
+        vin[lo:hi] = v[lo:hi]
+        vin = gather(vin)  # what the Krylov loop hands to the apply
+        assert not np.isnan(vin[need[rank][0]: need[rank][1]]).any()
+        gv = coarse(vin)
+        t = rows_of_a(gv.copy())
+        t[lo:hi] = vin[lo:hi] - t[lo:hi]
+        t = gather(t)
+        y = one(t)
+        cy = coarse(rows_of_a(y.copy()))
+        got = y[lo:hi] - cy[lo:hi] + gv[lo:hi]
+        want = full.apply(v)[lo:hi]
+        assert rel(got, want) < 1e-12, rel(got, want)
+        # the ghost rows moved per exchange are a fraction of the vector
+        assert (need[rank][1] - need[rank][0]) - (hi - lo) < n
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as e:  # report to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_data_plane(world):
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, errq)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
