@@ -320,9 +320,12 @@ def run_mine(args, rank, world):
             "workload": describe(c, n, spec.label()),
             "ndof": n, "subdomains": len(dec.dofs), "iterations": its, "converged": bool(rep.converged),
             "final_rel_residual": float(hist[-1]),
-            "parallelism": (f"subdomains sharded over {world} GPUs (NCCL allreduce per apply), coarse replicated, "
-                            + ("Krylov vectors sharded by row blocks (CGS2: allgather per iteration + 3 small "
-                               "allreduces)" if ortho == "cgs2" else "MGS2 GMRES replicated"))
+            "parallelism": (f"subdomains sharded over {world} GPUs as x-slabs of boxes, rows owned in blocks; per "
+                            "apply: neighbour halo gather (ncclSend/Recv) for restriction and SpMV, neighbour "
+                            "overlap sum for prolongation, allreduce of the coarse restriction (coarse factor "
+                            "replicated); "
+                            + ("Krylov vectors sharded by owned rows (CGS2: 3 small allreduces per iteration)"
+                               if ortho == "cgs2" else "MGS2 GMRES replicated (whole-vector completion per apply)"))
                            if world > 1 else "single-gpu",
             "orthogonalization": ortho,
             "local_subdomains": int(len(st.dof_sets)),
@@ -507,7 +510,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-box", type=float, default=75.0,
+    ap.add_argument("--cpu-box", type=float, default=120.0,
                     help="time box (s) of the cpu_baseline leg's real CPU step (setup + first GMRES iterations)")
     ap.add_argument("--ref-box", type=float, default=180.0,
                     help="time box (s) of the --impl reference arm's one real CPU step")

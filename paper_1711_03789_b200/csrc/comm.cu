@@ -43,9 +43,12 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    // MDD_NCCL_LIB: the NCCL library file to load (a system build instead of a bundled one;
+    // tools/rank_emulation.py points it at its timing stand-in)
+    const char* names[] = {getenv("MDD_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
-      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (!n || !*n) continue;
+      api.h = dlopen(n, RTLD_NOW | RTLD_LOCAL);
       if (api.h) break;
     }
     if (!api.h) return;

@@ -36,7 +36,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["Communicator", "LoopbackGroup", "Shard", "shard_bounds", "make_shard", "setup_sharded", "row_block"]
+__all__ = ["Communicator", "LoopbackGroup", "Shard", "shard_bounds", "shard_blocks", "make_shard", "setup_sharded",
+           "row_block", "needed_rows"]
 
 
 def shard_bounds(costs, nranks: int) -> np.ndarray:
@@ -108,11 +109,19 @@ class Communicator:
     ``force_nccl`` initialises NCCL even for a single rank (used by the tests
     to exercise the allreduce path on one GPU)."""
 
-    def __init__(self, ctx=None, group=None, force_nccl: bool = False, loopback=None):
-        import torch.distributed as dist
-
+    def __init__(self, ctx=None, group=None, force_nccl: bool = False, loopback=None, standalone=None):
         self.ctx = ctx or _lib.get_context()
         self.is_nccl = False
+        if standalone is not None:
+            # (rank, nranks, unique id): ranks that found each other without torch.distributed
+            self.rank, self.nranks, uid = int(standalone[0]), int(standalone[1]), bytes(standalone[2])
+            h = C.c_void_p()
+            _lib.check(_lib.lib.mdd_comm_create(self.ctx.handle, self.nranks, self.rank, uid, C.byref(h)))
+            self.handle = h
+            self.is_nccl = True
+            return
+        import torch.distributed as dist
+
         if loopback is not None:
             # (LoopbackGroup, rank): ranks are host threads sharing one GPU (tests)
             grp, rank = loopback
@@ -192,9 +201,31 @@ class Shard:
     comm: Communicator | None = None
 
 
+def shard_blocks(dof_sets, ndof: int, nranks: int) -> np.ndarray:
+    """Boundaries of the contiguous subdomain blocks of the ranks.
+
+    Preferred: subdomain l goes to the rank whose owned row block (:func:`row_block`) holds
+    the median unknown of I_l, so a rank's subdomains sit on top of the rows it owns and its
+    needed row range (:func:`needed_rows`) exceeds them by the overlap only (cfg4 on 8 ranks:
+    64 boxes = one x-layer per rank).  When that leaves a rank with less than half the
+    average number of subdomains (more ranks than x-layers of boxes), fall back to blocks
+    balanced by local DoF count (:func:`shard_bounds`)."""
+    nsub = len(dof_sets)
+    if nranks == 1:
+        return np.array([0, nsub], dtype=np.int64)
+    chunk = -(-ndof // nranks)
+    med = np.array([d[len(d) // 2] if len(d) else 0 for d in dof_sets], dtype=np.int64)
+    owner = np.minimum(med // chunk, nranks - 1)
+    if np.all(np.diff(owner) >= 0):
+        b = np.searchsorted(owner, np.arange(nranks + 1)).astype(np.int64)
+        if np.diff(b).min() >= max(1, nsub // (2 * nranks)):
+            return b
+    return shard_bounds([len(d) for d in dof_sets], nranks)
+
+
 def make_shard(decomp, rank: int, nranks: int, comm: Communicator | None = None) -> Shard:
-    """Contiguous block of ``decomp``'s subdomains for ``rank`` (cost = local DoFs)."""
-    b = shard_bounds([len(d) for d in decomp.dofs], nranks)
+    """Contiguous block of ``decomp``'s subdomains for ``rank`` (:func:`shard_blocks`)."""
+    b = shard_blocks(decomp.dofs, decomp.space.ndof, nranks)
     return Shard(rank, nranks, np.arange(b[rank], b[rank + 1], dtype=np.int64), comm)
 
 

@@ -95,6 +95,7 @@ def main():
     ap.add_argument("--check-reference", action="store_true")
     ap.add_argument("--short", type=int, default=20)
     ap.add_argument("--short-only", action="store_true")
+    ap.add_argument("--update", action="store_true", help="with --sensitivity: add to the existing file, no main run")
     ap.add_argument("--sensitivity", type=int, default=0, metavar="K",
                     help="add hist_pert: the oracle's own history over K iterations when every preconditioner "
                          "output is perturbed by a relative 1e-13 (the size of the device/oracle apply difference)")
@@ -116,26 +117,27 @@ def main():
         log(f"[oracle] one apply {t_apply:.2f}s")
         out = os.path.join(HERE, f"{c['name']}_oracle.npz")
         snaps = {args.short: None}
-        if args.sensitivity:
-            old = dict(np.load(out, allow_pickle=False))
+        def perturbed_history(k):
             rng = np.random.default_rng(99)
-            level = 1e-13
 
             def noisy(vv):
                 y = M.apply(vv)
-                return y * (1.0 + level * rng.standard_normal(len(y)))
+                return y * (1.0 + 1e-13 * rng.standard_normal(len(y)))
 
-            hp = P.gmres(prob["A"], prob["rhs"], noisy, tol=W.TOL, maxit=W.MAXIT, max_iters=args.sensitivity, log=log)[1]
-            old.update(hist_pert=hp, pert_level=level)
-            np.savez_compressed(out, **old)
-            k = min(len(hp), len(old["hist"]))
-            log("updated", out, "max rel deviation under the perturbation:",
-                float(np.abs(hp[:k] / old["hist"][:k] - 1).max()))
-            return
-        if args.short_only:
+            return P.gmres(prob["A"], prob["rhs"], noisy, tol=W.TOL, maxit=W.MAXIT, max_iters=k, log=log)[1]
+
+        if args.short_only or (args.sensitivity and args.update):
             old = dict(np.load(out, allow_pickle=False))
-            xs = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=W.MAXIT, max_iters=args.short, log=log)[0]
-            old.update(xs_proj=probes.conj() @ xs, xs_samp=xs[::stride], xsnorm=np.linalg.norm(xs), short=args.short)
+            if args.short_only:
+                xs = P.gmres(prob["A"], prob["rhs"], M.apply, tol=W.TOL, maxit=W.MAXIT, max_iters=args.short,
+                             log=log)[0]
+                old.update(xs_proj=probes.conj() @ xs, xs_samp=xs[::stride], xsnorm=np.linalg.norm(xs),
+                           short=args.short)
+            if args.sensitivity:
+                hp = perturbed_history(args.sensitivity)
+                old.update(hist_pert=hp, pert_level=1e-13)
+                k = min(len(hp), len(old["hist"]))
+                log("max rel deviation under the perturbation:", float(np.abs(hp[:k] / old["hist"][:k] - 1).max()))
             np.savez_compressed(out, **old)
             log("updated", out, f"{os.path.getsize(out) / 1024:.1f} KiB")
             return
@@ -144,6 +146,7 @@ def main():
                                          snapshots=snaps)
         t_gmres = time.time() - t0
         xs = snaps[args.short] if snaps[args.short] is not None else x
+        hist_pert = perturbed_history(args.sensitivity) if args.sensitivity else None
         res = np.linalg.norm(prob["rhs"] - prob["A"] @ x) / np.linalg.norm(prob["rhs"])
         log(f"[oracle] {c['name']}: {its} iterations conv={conv} hist[-1]={hist[-1]:.6e} true rel.res {res:.6e} "
             f"gmres {t_gmres:.1f}s setup {M.setup_time_s:.1f}s")
@@ -155,7 +158,8 @@ def main():
                         x_proj=probes.conj() @ x, x_samp=x[::stride], xnorm=np.linalg.norm(x),
                         ap_proj=probes.conj() @ av, ap_samp=av[::stride], apnorm=np.linalg.norm(av),
                         xs_proj=probes.conj() @ xs, xs_samp=xs[::stride], xsnorm=np.linalg.norm(xs),
-                        short=min(args.short, its), true_rel_res=res, times=json.dumps(times))
+                        short=min(args.short, its), true_rel_res=res, times=json.dumps(times),
+                        **({"hist_pert": hist_pert, "pert_level": 1e-13} if hist_pert is not None else {}))
     log("wrote", out, f"{os.path.getsize(out) / 1024:.1f} KiB", json.dumps(times))
 
 

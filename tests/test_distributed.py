@@ -24,7 +24,8 @@ import torch.multiprocessing as mp
 from conftest import mesh_dict, rel
 from oracle import maxwell_oracle as O
 from paper_1711_03789_b200 import decomp, fem, mesh
-from paper_1711_03789_b200.distributed import broadcast_unique_id, make_shard, needed_rows, row_block, shard_bounds
+from paper_1711_03789_b200.distributed import (broadcast_unique_id, make_shard, needed_rows, row_block, shard_blocks,
+                                               shard_bounds)
 
 
 def test_shard_bounds_cover_and_balance():
@@ -375,3 +376,20 @@ def test_gloo_halo_data_plane(world):
         errs.append(errq.get())
     assert not errs, errs
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def test_shard_blocks_follow_the_row_blocks():
+    """8^3 boxes on 8 and 4 ranks: whole x-layers of boxes per rank, on top of the owned rows;
+    on 8 ranks with 2^3 boxes the layers cannot be split, so the DoF-balanced blocks are used."""
+    s = fem.build_edge_space(mesh.build_cube_mesh(16), "pec")
+    d = decomp.build_decomposition(s, 8, 1)
+    assert list(shard_blocks(d.dofs, s.ndof, 8)) == [64 * r for r in range(9)]
+    assert list(shard_blocks(d.dofs, s.ndof, 4)) == [128 * r for r in range(5)]
+    for world in (4, 8):
+        for rank in range(world):
+            lo, hi = row_block(s.ndof, world, rank)
+            nlo, nhi = needed_rows(s, [d.dofs[i] for i in make_shard(d, rank, world).subdomains], lo, hi)
+            assert (nhi - nlo) <= 2.6 * (hi - lo)  # owned rows + one overlap layer either side (boxes of 2 cells)
+    d2 = decomp.build_decomposition(fem.build_edge_space(mesh.build_cube_mesh(8), "pec"), 2, 1)
+    b = shard_blocks(d2.dofs, d2.space.ndof, 8)
+    assert list(b) == list(range(9))
