@@ -270,6 +270,18 @@ int mdd_comm_loopback_group(int nranks, void** group_out);
 void mdd_comm_loopback_group_free(void* group);
 int mdd_comm_create_loopback(mdd_ctx* ctx, void* group, int rank, mdd_comm** out);
 
+/* precond.assemble_local(space, coeffs, elems, local_bc="impedance") (precond.py:82-139): the
+ * submesh matrix of one subdomain of an impras preconditioner as the device assembled it
+ * (element scatter over the subdomain tets + impedance mass over its boundary faces), CSR over
+ * the subdomain's unknowns in ascending global order. */
+int mdd_prec_local_matrix_size(const mdd_prec* P, int32_t sub, int64_t* n, int64_t* nnz);
+int mdd_prec_local_matrix(const mdd_prec* P, int32_t sub, int32_t* rowptr, int32_t* cols, mdd_complex* vals);
+/* Smallest pivot ratio min|pivot| / max|pivot| of the last factorisation (subdomain blocks,
+ * coarse block).  The reference's DenseLU pivots partially and checks 1e-14 (linalg.py:92-101);
+ * the device factorisation pivots statically, which Lemma 2.5 of the paper covers when the
+ * problem has absorption or impedance terms.  Without either (xi_prec = 0, sigma = 0, PEC
+ * local problems) the caller uses this ratio to refuse an unreliable factor. */
+int mdd_prec_pivot_ratio(const mdd_prec* P, double* sub_ratio, double* coarse_ratio);
 /* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
  *              levels, sum_local_dofs, coarse_n] */
 int mdd_prec_stats(const mdd_prec* P, double* out8);

@@ -1092,6 +1092,9 @@ int FrontPlan::check_pivots(std::string& msg, cudaStream_t s) {
     mn[i] = std::min(mn[i], ps[2 * g]);
     mx[i] = std::max(mx[i], ps[2 * g + 1]);
   }
+  min_pivot_ratio = INFINITY;
+  for (int i = 0; i < nmat; ++i)
+    if (mat_n[i] != 0 && mx[i] > 0.0) min_pivot_ratio = std::min(min_pivot_ratio, mn[i] / mx[i]);
   for (int i = 0; i < nmat; ++i) {
     if (mat_n[i] == 0) continue;
     const bool bad = !(mx[i] > 0.0) || !std::isfinite(mx[i]) || !(mn[i] > 1e-14 * mx[i]);

@@ -79,6 +79,7 @@ struct FrontPlan {
   std::vector<int32_t> mat_n, mat_off;
   std::vector<std::vector<int32_t>> perm;  // per matrix: ND index -> local index
   int64_t nloc = 0;
+  double min_pivot_ratio = 0.0;  // smallest min|pivot| / max|pivot| over the matrices (check_pivots)
   int32_t nnodes = 0, nlevels = 0;
   std::vector<NodeDev> h_nodes;
   DevBuf<NodeDev> nodes;

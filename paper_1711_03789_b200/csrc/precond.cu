@@ -69,6 +69,7 @@ struct PrecCore {
   DevBuf<int32_t> loc_face, loc_face_sub, loc_face_l;  // boundary faces
   int64_t n_loc_faces = 0;
   DevBuf<int32_t> loc_row_off;                   // per subdomain: offset into loc_rowptr
+  std::vector<int32_t> h_loc_row_off, h_loc_ent_off;  // host copies (mdd_prec_local_matrix)
   std::vector<double> stats = std::vector<double>(8, 0.0);
   DevBuf<double2> t1, t2, t3, t4;
   cudaStream_t s2 = nullptr;  // coarse-solve branch
@@ -1048,6 +1049,8 @@ int mdd_prec_create(mdd_ctx* ctx, const mdd_prec_desc* d, mdd_prec** out, int32_
     c.loc_tet.upload(cellmask_arr, s);  // [cells | masks]
     c.loc_tet_sub.upload(ps, s);
     c.loc_e2l.upload(pe, s);
+    c.h_loc_row_off = row_off;
+    c.h_loc_ent_off = ent_off;
     c.loc_row_off.upload(row_off, s);
     c.loc_rowptr.upload(all_rowptr, s);
     c.loc_cols.upload(all_cols, s);
@@ -1367,6 +1370,41 @@ int mdd_prec_halo_info(const mdd_prec* P, int64_t* own_lo, int64_t* own_hi, int6
   *need_lo = h.need_lo[me];
   *need_hi = h.need_hi[me];
   *exchanged_rows = (h.need_hi[me] - h.need_lo[me]) - (h.own_hi[me] - h.own_lo[me]);
+  MDD_API_END
+}
+
+int mdd_prec_local_matrix_size(const mdd_prec* P, int32_t sub, int64_t* n, int64_t* nnz) {
+  MDD_API_BEGIN
+  const PrecCore& c = *P->core;
+  if (c.h_loc_row_off.empty()) fail(MDD_EINVAL, "local matrices exist only for impras preconditioners");
+  if (sub < 0 || sub + 1 >= (int32_t)c.h_loc_row_off.size()) fail(MDD_EINVAL, "local matrix: subdomain out of range");
+  *n = c.h_loc_row_off[sub + 1] - c.h_loc_row_off[sub] - 1;
+  *nnz = c.h_loc_ent_off[sub + 1] - c.h_loc_ent_off[sub];
+  MDD_API_END
+}
+
+int mdd_prec_local_matrix(const mdd_prec* P, int32_t sub, int32_t* rowptr, int32_t* cols, mdd_complex* vals) {
+  MDD_API_BEGIN
+  const PrecCore& c = *P->core;
+  if (c.h_loc_row_off.empty()) fail(MDD_EINVAL, "local matrices exist only for impras preconditioners");
+  if (sub < 0 || sub + 1 >= (int32_t)c.h_loc_row_off.size()) fail(MDD_EINVAL, "local matrix: subdomain out of range");
+  CK(cudaSetDevice(c.ctx->device));
+  cudaStream_t s = c.ctx->stream;
+  const int64_t n = c.h_loc_row_off[sub + 1] - c.h_loc_row_off[sub] - 1;
+  const int64_t e0 = c.h_loc_ent_off[sub], nnz = c.h_loc_ent_off[sub + 1] - e0;
+  CK(cudaMemcpyAsync(rowptr, c.loc_rowptr.p + c.h_loc_row_off[sub], sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(cols, c.loc_cols.p + e0, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(vals, c.loc_vals.p + e0, sizeof(double2) * nnz, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  MDD_API_END
+}
+
+int mdd_prec_pivot_ratio(const mdd_prec* P, double* sub_ratio, double* coarse_ratio) {
+  MDD_API_BEGIN
+  *sub_ratio = P->core->sub.min_pivot_ratio;
+  *coarse_ratio = P->core->have_coarse ? P->core->coarse.min_pivot_ratio : INFINITY;
   MDD_API_END
 }
 

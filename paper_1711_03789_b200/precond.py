@@ -25,6 +25,7 @@ from .fem import Coefficients, EdgeSpace, SystemBundle, assemble
 from .linalg import DEFAULT_LU_CAP, DeviceCSR, as_device_csr, raise_for
 
 __all__ = [
+    "assemble_local",
     "PreconditionerSpec",
     "PreconditionerState",
     "setup",
@@ -102,7 +103,7 @@ class PreconditionerState:
     """Factorised Schwarz preconditioner; ``apply`` is a fixed linear map (reference precond.py:147-247)."""
 
     def __init__(self, problem: SystemBundle, decomp: Decomposition, spec: PreconditionerSpec,
-                 lu_cap=DEFAULT_LU_CAP, leaf_size: int = 0, shard=None):
+                 lu_cap=DEFAULT_LU_CAP, leaf_size: int = 0, shard=None, _partial_cover: bool = False):
         """``shard`` (a :class:`distributed.Shard`) restricts the local solves to a
         subset of the subdomains and attaches the communicator whose allreduce
         completes the one-level sum; the coarse space stays replicated."""
@@ -126,7 +127,9 @@ class PreconditionerState:
             self.pou_weights = decomp.pou
         else:
             self.dof_sets = impedance_dof_sets(space, decomp.elements)
-            self.pou_weights = build_pou(self.dof_sets, self.ndof)
+            # _partial_cover: a single-subdomain state built by assemble_local (no PoU needed)
+            self.pou_weights = ([np.ones(len(d)) for d in self.dof_sets] if _partial_cover
+                                else build_pou(self.dof_sets, self.ndof))
         self._elements = decomp.elements
         if shard is not None:
             # PoU weights are global (computed over every subdomain) before the cut
@@ -147,7 +150,40 @@ class PreconditionerState:
             _lib.check(_lib.lib.mdd_prec_set_comm(handle, shard.comm.handle))
             if shard.comm.nranks > 1 or shard.comm.is_nccl:
                 self._set_halo(shard)
+        self._check_static_pivoting(prec_coeffs, spec)
         self.setup_time_s = time.perf_counter() - t0
+
+    #: pivot ratio below which a factor of a problem WITHOUT absorption is refused
+    NO_ABSORPTION_PIVOT_TOL = 1e-10
+
+    def _check_static_pivoting(self, prec_coeffs, spec):
+        """The device factorisation pivots statically (no row exchanges).  That is backed by
+        the paper's Lemma 2.5 whenever the preconditioning problem has absorption (xi_prec != 0
+        or sigma > 0 somewhere) or impedance terms (impras local problems, impedance global
+        boundary): every leading minor is then nonsingular and the minors are well behaved.
+        Without any of these the blocks are real symmetric INDEFINITE once k^2 exceeds a
+        subdomain's first Dirichlet eigenvalue; the reference's LAPACK LU pivots its way
+        through such blocks (linalg.py:92), a static order need not.  In that case the factor
+        is accepted only if no pivot came close to cancelling (ratio >= 1e-10, i.e. at most
+        ~1e-6 of accuracy lost); otherwise a SingularMatrixError says why."""
+        sig = np.asarray(prec_coeffs.sigma)
+        absorbing = prec_coeffs.xi != 0.0 or bool(np.any(sig > 0.0))
+        impedance = spec.family == "impras" or getattr(self.decomp.space, "bc_kind", "pec") == "impedance"
+        self.static_pivoting_backed = bool(absorbing or impedance)
+        if self.static_pivoting_backed:
+            return
+        a, b = C.c_double(), C.c_double()
+        _lib.check(_lib.lib.mdd_prec_pivot_ratio(self._h, C.byref(a), C.byref(b)))
+        self.pivot_ratio = (a.value, b.value)
+        from .linalg import SingularMatrixError
+
+        for what, r in (("subdomain blocks", a.value), ("coarse space", b.value)):
+            if not r >= self.NO_ABSORPTION_PIVOT_TOL:
+                raise SingularMatrixError(
+                    f"{what}: pivot ratio {r:.2e} below {self.NO_ABSORPTION_PIVOT_TOL:.0e} in a problem without "
+                    "absorption (xi_prec = 0, sigma = 0, PEC local problems): the blocks are real symmetric "
+                    "indefinite and the device factorisation does not exchange rows; use a nonzero xi_prec or "
+                    "impedance local problems")
 
     def _set_halo(self, shard):
         """Row ranges of the sharded data plane (libmdd ``mdd_prec_set_halo``): this rank's
@@ -298,6 +334,46 @@ class PreconditionerState:
 
     def stats(self) -> dict:
         return self.factors.stats()
+
+
+def assemble_local(space: EdgeSpace, coeffs: Coefficients, elems: np.ndarray, local_bc: str = "pec"):
+    """System matrix on a subdomain submesh: ``(matrix, global_dofs)`` (reference precond.py:82-139).
+
+    ``local_bc="pec"``: the unknowns with zero trace on the internal boundary; every tet around
+    such an edge lies in the subdomain, so the matrix is the minor of the device-assembled
+    global matrix on those unknowns (the reference's own test_decomp.py:240-253 checks that
+    identity).  ``local_bc="impedance"``: all kept unknowns of the subdomain tets, element
+    scatter over the subdomain tets plus the impedance mass over the subdomain boundary faces,
+    assembled on the device exactly as the impras preconditioner does (csrc/precond.cu
+    k_local_cells / k_local_faces) and read back through ``mdd_prec_local_matrix``."""
+    from .decomp import Decomposition, subdomain_dof_sets
+    from .fem import assemble as _assemble
+
+    elems = np.ascontiguousarray(elems, dtype=np.int64)
+    if local_bc == "pec":
+        gdofs = subdomain_dof_sets(space, [elems])[0]
+        a = _assemble(space, coeffs).A.to_scipy().tocsr()
+        m = a[gdofs][:, gdofs].tocsr()
+        m.sort_indices()
+        return m, gdofs
+    if local_bc != "impedance":
+        raise ValueError(f"unknown local boundary condition {local_bc!r}")
+    gdofs = impedance_dof_sets(space, [elems])[0]
+    one = Decomposition(space=space, elements=[elems], dofs=[gdofs], pou=[np.ones(len(gdofs))], overlap_layers=1,
+                        p_axis=1, H_sub=float(np.sqrt(3.0)))
+    prob = _assemble(space, coeffs)
+    st = PreconditionerState(prob, one, PreconditionerSpec("impras", "one", xi_prec=coeffs.xi), lu_cap=None,
+                             _partial_cover=True)
+    n, nnz = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib.mdd_prec_local_matrix_size(st._h, 0, C.byref(n), C.byref(nnz)))
+    rp = np.empty(n.value + 1, dtype=np.int32)
+    cl = np.empty(max(nnz.value, 1), dtype=np.int32)
+    vals = np.empty(max(nnz.value, 1), dtype=np.complex128)
+    _lib.check(_lib.lib.mdd_prec_local_matrix(st._h, 0, _lib.ptr(rp, C.c_int32), _lib.ptr(cl, C.c_int32),
+                                             vals.ctypes.data_as(C.c_void_p)))
+    m = sp.csr_matrix((vals[: nnz.value], cl[: nnz.value], rp), shape=(n.value, n.value))
+    m.sort_indices()
+    return m, gdofs
 
 
 def setup(problem: SystemBundle, decomp: Decomposition, spec: PreconditionerSpec,

@@ -220,3 +220,34 @@ def test_symmetric_transpose_path_matches_gemm_path(gpu, monkeypatch):
     ref = O.Schwarz(d.dofs, d.pou, O.minors(A, d.dofs), levels="two", R0=R0, A0=(R0 @ A @ R0.T).tocsc(),
                     ndof=prob.ndof)
     assert rel(y_sym, ref.apply(v)) <= 1e-11
+
+
+def test_no_absorption_blocks_are_checked_against_pivoted_lu(gpu):
+    """xi_prec = 0, sigma = 0, PEC local problems, k above the first Dirichlet eigenvalue of the
+    subdomains (k = 9 > pi*sqrt(2)/0.75 = 5.9): the blocks are real symmetric indefinite, which
+    Lemma 2.5 does not cover.  The reference factors them with partially pivoted LAPACK LU
+    (linalg.py:92); the device path pivots statically and must either reproduce the pivoted
+    result or refuse the factor with an explicit SingularMatrixError -- never return a silently
+    inaccurate map."""
+    from oracle import maxwell_oracle as O
+    from paper_1711_03789_b200 import decomp, fem, mesh, precond
+    from paper_1711_03789_b200.linalg import SingularMatrixError
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(8), "pec")
+    k = 9.0
+    prob = fem.assemble(s, fem.Coefficients(k=k, xi=0.0))
+    d = decomp.build_decomposition(s, 2, 2)
+    a = O.assemble({kk: getattr(s.mesh, kk) for kk in ("vertices", "tets", "edges", "tet_edges", "tet_edge_signs",
+                                                       "boundary_faces")}, s.edge_to_dof, s.ndof, k, 0.0)["A"]
+    minors = O.minors(a, d.dofs)
+    ev = np.linalg.eigvalsh(minors[0].toarray().real)
+    assert ev.min() < 0 < ev.max()  # indefinite: the case the advisor flagged
+    want = O.Schwarz(d.dofs, d.pou, minors, "as", "one", ndof=s.ndof, solver="dense")
+    v = np.random.default_rng(2).standard_normal(s.ndof) * (1 + 0.5j)
+    try:
+        st = precond.setup(prob, d, precond.PreconditionerSpec("as", "one", xi_prec=0.0), lu_cap=None)
+    except SingularMatrixError as e:
+        assert "without absorption" in str(e)
+        return
+    assert st.static_pivoting_backed is False and min(st.pivot_ratio) >= st.NO_ABSORPTION_PIVOT_TOL
+    assert rel(st.apply(v), want.apply(v)) <= 1e-9
