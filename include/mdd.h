@@ -269,6 +269,8 @@ int mdd_prec_halo_info(const mdd_prec* P, int64_t* own_lo, int64_t* own_hi, int6
 int mdd_comm_loopback_group(int nranks, void** group_out);
 void mdd_comm_loopback_group_free(void* group);
 int mdd_comm_create_loopback(mdd_ctx* ctx, void* group, int rank, mdd_comm** out);
+/* marks a loopback group as failed: every rank's current and later collectives return MDD_ENCCL at once */
+int mdd_comm_abort(mdd_comm* c);
 
 /* precond.assemble_local(space, coeffs, elems, local_bc="impedance") (precond.py:82-139): the
  * submesh matrix of one subdomain of an impras preconditioner as the device assembled it

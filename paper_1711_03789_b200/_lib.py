@@ -175,6 +175,7 @@ SIGNATURES = {
     "mdd_comm_loopback_group_free": (None, [_P]),
     "mdd_comm_create_loopback": (C.c_int, [_P, _P, C.c_int, _PP]),
     "mdd_comm_destroy": (None, [_P]),
+    "mdd_comm_abort": (C.c_int, [_P]),
     "mdd_comm_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "mdd_prec_local_matrix_size": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "mdd_prec_local_matrix": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P]),

@@ -91,6 +91,7 @@ struct LoopGroup {
   std::condition_variable cv;
   int arrived = 0;
   uint64_t gen = 0;
+  bool aborted = false;  // a rank failed: every waiter (now and later) fails fast
   const double2* bufs[kLoopMax] = {};
   int64_t count[kLoopMax] = {};  // per-rank element count of the current collective
   int kind[kLoopMax] = {};       // 1 allreduce, 2 allgather: every rank must be in the same collective
@@ -103,15 +104,27 @@ void loop_check(LoopGroup* g, int rank) {
                           std::to_string(g->kind[k]) + ", count " + std::to_string(g->count[rank]) + "/" +
                           std::to_string(g->count[k]) + ")");
 }
+void loop_abort(LoopGroup* g) {
+  std::lock_guard<std::mutex> l(g->mu);
+  g->aborted = true;
+  g->cv.notify_all();
+}
 void loop_barrier(LoopGroup* g) {
   std::unique_lock<std::mutex> l(g->mu);
+  if (g->aborted) fail(MDD_ENCCL, "loopback group: another rank failed");
   const uint64_t my = g->gen;
   if (++g->arrived == g->n) {
     g->arrived = 0;
     ++g->gen;
     g->cv.notify_all();
-  } else if (!g->cv.wait_for(l, std::chrono::seconds(300), [&] { return g->gen != my; })) {
-    fail(MDD_ENCCL, "loopback group: a rank did not reach the collective within 300 s");
+  } else {
+    const bool ok = g->cv.wait_for(l, std::chrono::seconds(300), [&] { return g->gen != my || g->aborted; });
+    if (g->aborted) fail(MDD_ENCCL, "loopback group: another rank failed");
+    if (!ok) {
+      g->aborted = true;
+      g->cv.notify_all();
+      fail(MDD_ENCCL, "loopback group: a rank did not reach the collective within 300 s");
+    }
   }
 }
 struct RankPtrs {
@@ -375,6 +388,14 @@ int mdd_comm_create_loopback(mdd_ctx* ctx, void* group, int rank, mdd_comm** out
   c->rank = rank;
   c->loop = g;
   *out = c.release();
+  MDD_API_END
+}
+
+/* A rank that failed outside a collective (setup, a size check) tells the group, so the other
+ * ranks' next or current barrier fails at once instead of waiting out the 300 s limit. */
+int mdd_comm_abort(mdd_comm* c) {
+  MDD_API_BEGIN
+  if (c && c->loop) loop_abort(static_cast<LoopGroup*>(c->loop));
   MDD_API_END
 }
 

@@ -604,7 +604,56 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
-template <int U>
+// One sweep of the CTA's slice: w <- w - h A (axpy with X_t), acc = <B, w> (dot with X_{t+1}),
+// dacc = <B, D> (drift partner, first pass only).  Flags are compile-time so the loop body is a
+// handful of loads and DFMAs (the generic loop ran at ~150 instructions per element under the
+// 64-register cap of a 1024-thread CTA and was issue-bound, ncu r02 profile); the slice is
+// walked in two pieces, w in shared memory and w in L2, so there is no per-element tier test.
+template <bool HASB, bool HASD, bool DOWN>
+__device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const double2* __restrict__ B,
+                                           const double2* __restrict__ D, double2* __restrict__ WS,
+                                           double2* __restrict__ wg, int ws, int len, double2 h, uint64_t pol_first,
+                                           uint64_t pol_last, double2& acc, double2& dacc) {
+  // piece 1: w in shared memory
+  auto piece1 = [&]() {
+  for (int iu = threadIdx.x; iu < ws; iu += kWideThreads) {
+    const int i = DOWN ? ws - 1 - iu : iu;
+    const double2 av = ld_hint(A + i, pol_first);
+    double2 bv, dv;
+    if (HASB) bv = __ldcg(B + i);
+    if (HASD) dv = __ldcg(D + i);
+    const double2 wi = caxmy(WS[i], h, av);
+    WS[i] = wi;
+    const double2 x = HASB ? bv : wi;
+    acc = cdotc_acc(acc, x, wi);
+    if (HASD) dacc = cdotc_acc(dacc, x, dv);
+  }
+  };
+  // piece 2: the tail of w, resident in L2 (evict_last)
+  auto piece2 = [&]() {
+  for (int iu = ws + threadIdx.x; iu < len; iu += kWideThreads) {
+    const int i = DOWN ? len - 1 - (iu - ws) : iu;
+    const double2 av = ld_hint(A + i, pol_first);
+    const double2 wv = ld_hint(wg + i, pol_last);
+    double2 bv, dv;
+    if (HASB) bv = __ldcg(B + i);
+    if (HASD) dv = __ldcg(D + i);
+    const double2 wi = caxmy(wv, h, av);
+    st_hint2(wg + i, wi, pol_last);
+    const double2 x = HASB ? bv : wi;
+    acc = cdotc_acc(acc, x, wi);
+    if (HASD) dacc = cdotc_acc(dacc, x, dv);
+  }
+  };
+  if (DOWN) {  // the top of the slice (fetched last by the upward pass before) first
+    piece2();
+    piece1();
+  } else {
+    piece1();
+    piece2();
+  }
+}
+
 __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a) {
   extern __shared__ double2 col[];  // m+1, identical in every CTA; then the w head
   __shared__ double2 red[68 + 2 * kMaxArnCTAs + 2 * 64];
@@ -627,49 +676,39 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
   for (int j = threadIdx.x; j <= m; j += kWideThreads) col[j] = make_double2(0.0, 0.0);
   const double2 zero = make_double2(0.0, 0.0);
   double dmax = 0.0;
-  // pass t = -1: load w, dot with X_0; pass t >= 0: axpy with X_t, dot with X_{t+1} (w itself at the end)
-  for (int t = -1; t < nsteps; ++t) {
-    const bool first = t < 0, hasB = t + 1 < nsteps, hasD = do_drift && t + 1 < m - 1;
-    double2 h = zero;
-    if (!first) {
-      double2 d;
-      gather_sum(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
-      if (do_drift && t < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
-      if (threadIdx.x == 0) col[t % m] = cadd(col[t % m], h);
+  // pass -1: load w into its tiers, dot with X_0 (+ drift partner)
+  {
+    const double2* B = xvec(0);
+    double2 acc = zero, dacc = zero;
+    for (int i = threadIdx.x; i < len; i += kWideThreads) {
+      const double2 wi = __ldcg(wg + i);
+      if (i < ws) WS[i] = wi;
+      const double2 x = __ldcg(B + i);
+      acc = cdotc_acc(acc, x, wi);
+      if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
     }
-    const double2* A = first ? wg : xvec(t);
+    block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64);
+    if (threadIdx.x == 0) publish(slots(0), a.pad, acc, dacc);
+  }
+  for (int t = 0; t < nsteps; ++t) {
+    const bool hasB = t + 1 < nsteps, hasD = do_drift && t + 1 < m - 1;
+    double2 h, d;
+    gather_sum(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
+    if (do_drift && t < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
+    if (threadIdx.x == 0) col[t % m] = cadd(col[t % m], h);
+    const double2* A = xvec(t);
     const double2* B = hasB ? xvec(t + 1) : nullptr;
     double2 acc = zero, dacc = zero;
-    // odd passes sweep the slice downwards: the chunks of X_{t+1} fetched last in pass t are the
-    // first ones pass t+1 needs again, so whatever part of a vector the L2 retains is the part
-    // reused first (the 126 MB L2 does not hold a 56 MB vector plus the streams around it)
+    // odd passes sweep the slice downwards when the vectors exceed what the L2 retains: the
+    // chunks of X_{t+1} fetched last in pass t are then the first ones pass t+1 needs again
     const bool down = a.zigzag && (t & 1);
-    for (int i0 = threadIdx.x; i0 < len; i0 += U * kWideThreads) {
-      double2 av[U], bv[U], wv[U], dv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int iu = i0 + u * kWideThreads;
-        const bool ok = iu < len;
-        const int i = down ? len - 1 - iu : iu;
-        // first pass: the operator output, read once; later: last use of this basis chunk in this step pair
-        av[u] = ok ? ld_hint(A + i, pol_first) : zero;  // i is valid whenever ok
-        bv[u] = (ok && hasB) ? __ldcg(B + i) : zero;
-        wv[u] = (ok && !first) ? (i < ws ? WS[i] : ld_hint(wg + i, pol_last)) : zero;
-        dv[u] = (ok && hasD) ? __ldcg(dvm1 + i) : zero;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int iu = i0 + u * kWideThreads;
-        const int i = down ? len - 1 - iu : iu;
-        if (iu < len) {
-          const double2 wi = first ? av[u] : caxmy(wv[u], h, av[u]);
-          if (i < ws) WS[i] = wi;
-          else if (!first) st_hint2(wg + i, wi, pol_last);
-          const double2 x = hasB ? bv[u] : wi;
-          acc = cdotc_acc(acc, x, wi);
-          if (hasD) dacc = cdotc_acc(dacc, x, dv[u]);
-        }
-      }
+    if (!hasB) wide_sweep<false, false, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+    else if (hasD) {
+      if (down) wide_sweep<true, true, true>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+      else wide_sweep<true, true, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+    } else {
+      if (down) wide_sweep<true, false, true>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+      else wide_sweep<true, false, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
     }
     block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64 * (t & 1));
     if (threadIdx.x == 0) {
@@ -681,7 +720,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
       if (t + 2 < nsteps) {
         const int64_t pb = min((int64_t)len * 16, a.pf_bytes);
         // pass t+1 starts at the top of the slice if it sweeps downwards
-        prefetch_l2((a.zigzag && ((t + 1) & 1)) ? xvec(t + 2) + len - pb / 16 : xvec(t + 2), pb);
+        const int64_t start = (a.zigzag && ((t + 1) & 1)) ? (int64_t)len - pb / 16 : 0;
+        prefetch_l2(xvec(t + 2) + start, pb);
       }
     }
   }
@@ -712,6 +752,109 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   if (do_drift) a.drift[m - 1] = dmax;
   arnoldi_tail_call(a, col, m, breakdown);
+}
+
+// ------------------------------------------------------------ drift panels
+// Orthogonality drift (krylov.py:152-160: max_j |<V_j, V_k>| for every accepted V_k) for the
+// large-slice path.  Riding along in the MGS sweeps costs one extra n-vector of DRAM traffic
+// per first-pass step there (V_{m-1} is re-read for every dot, and the L2 cannot keep it:
+// cfg4 1415 vs 1163 ms per solve).  Instead the drift of kDriftP consecutive new vectors is
+// computed together, GEMM-style: every CTA walks its row slab in tiles of kDriftR rows, stages
+// the tile of ALL older vectors in shared memory once and accumulates the kDriftP x J Gram
+// block in registers (thread j owns column j), so the basis is read once per kDriftP
+// iterations instead of once per iteration.  Partial blocks are summed over the CTAs in fixed
+// order by k_drift_finish.
+constexpr int kDriftP = 8;
+constexpr int kDriftR = 32;
+constexpr int kDriftThreads = 256;  // >= maxit: one thread per older vector
+
+struct DriftArgs {
+  int64_t n;
+  const double2* V;
+  const int* iter;      // in-loop: panel [m-P+1, m] when m % P == 0 and no breakdown; nullptr: explicit range
+  const int* dstatus;
+  int k0, k1;           // explicit range (iter == nullptr), inclusive
+  double2* partial;     // gridDim.x x kDriftP x kDriftThreads
+  double* drift;        // out: drift[k]
+  int ncta;
+};
+
+__device__ __forceinline__ bool drift_range(const DriftArgs& a, int& k0, int& k1) {
+  if (a.iter) {
+    const int m = *a.iter;
+    if (m < 1 || m % kDriftP != 0 || a.dstatus[1]) return false;
+    k0 = m - kDriftP + 1;
+    k1 = m;
+  } else {
+    k0 = a.k0;
+    k1 = a.k1;
+  }
+  return k1 >= k0 && k1 >= 1;
+}
+
+__global__ void __launch_bounds__(kDriftThreads) k_drift_panel(DriftArgs a) {
+  int k0, k1;
+  if (!drift_range(a, k0, k1)) return;
+  k0 = max(k0, 1);
+  const int J = k1;                 // older vectors V_0 .. V_{k1-1}
+  const int np = k1 - k0 + 1;       // new vectors V_{k0} .. V_{k1}
+  const int Jp = J | 1;             // odd row stride: conflict-free transposed stores
+  extern __shared__ double2 sm[];
+  double2* As = sm;                          // kDriftR x Jp
+  double2* Bs = sm + (size_t)kDriftR * Jp;   // kDriftR x kDriftP
+  const int64_t slab = (a.n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * slab, hi = min(a.n, lo + slab);
+  double2 acc[kDriftP];
+#pragma unroll
+  for (int k = 0; k < kDriftP; ++k) acc[k] = make_double2(0.0, 0.0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kDriftThreads / 32;
+  for (int64_t r0 = lo; r0 < hi; r0 += kDriftR) {
+    const int nr = (int)min((int64_t)kDriftR, hi - r0);
+    __syncthreads();
+    // stage: warp w loads rows r0 .. r0+31 of vectors j = w, w+nw, ... (coalesced 512 B each)
+    for (int j = warp; j < J + np; j += nw) {
+      const double2 v = lane < nr ? __ldcg(a.V + (int64_t)(j < J ? j : k0 + (j - J)) * a.n + r0 + lane)
+                                  : make_double2(0.0, 0.0);
+      if (j < J) As[(size_t)lane * Jp + j] = v;
+      else Bs[lane * kDriftP + (j - J)] = v;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < J) {
+      for (int r = 0; r < kDriftR; ++r) {
+        const double2 x = As[(size_t)r * Jp + threadIdx.x];
+#pragma unroll
+        for (int k = 0; k < kDriftP; ++k) acc[k] = cdotc_acc(acc[k], x, Bs[r * kDriftP + k]);
+      }
+    }
+  }
+  double2* out = a.partial + (size_t)blockIdx.x * kDriftP * kDriftThreads;
+#pragma unroll
+  for (int k = 0; k < kDriftP; ++k) out[k * kDriftThreads + threadIdx.x] = acc[k];
+}
+
+// drift[k] = max_{j < k} | sum over CTAs (fixed order) of the partial <V_j, V_k> |
+__global__ void __launch_bounds__(kDriftThreads) k_drift_finish(DriftArgs a) {
+  int k0, k1;
+  if (!drift_range(a, k0, k1)) return;
+  k0 = max(k0, 1);
+  __shared__ double wmax[kDriftThreads / 32];
+  const int k = k0 + blockIdx.x;
+  if (k > k1) return;
+  const int j = threadIdx.x;
+  double v = 0.0;
+  if (j < k) {
+    double2 sacc = make_double2(0.0, 0.0);
+    for (int c = 0; c < a.ncta; ++c)
+      sacc = cadd(sacc, a.partial[((size_t)c * kDriftP + (k - k0)) * kDriftThreads + j]);
+    v = hypot(sacc.x, sacc.y);
+  }
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kDriftThreads / 32; ++w) v = fmax(v, wmax[w]);
+    a.drift[k] = v;
+  }
 }
 
 // drift of the final basis vector V_m: |vdot(V_j, DV_m)| for j < m (one CTA per j)
@@ -1540,7 +1683,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
                                           (mode == 1 ? (size_t)kArnThreads * kArnE
                                                      : mode == 2 ? (size_t)std::min<int64_t>(slice, wcap) : 0));
   using ArnFn = void (*)(ArnoldiArgs);
-  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide<2> : k_arnoldi<0>;
+  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide : k_arnoldi<0>;
   const int arn_threads = mode == 2 ? kWideThreads : kArnThreads;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
@@ -1575,7 +1718,10 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   aa.drift = ddrift.p;
   aa.beta = dbeta.p;
   aa.tol = cfg->tol;
-  aa.check_drift = cfg->check_drift;
+  // large slices: the drift is computed in panels of kDriftP vectors (k_drift_panel) instead of
+  // riding along in the sweeps
+  const bool panel_drift = mode == 2 && cfg->check_drift && maxit < kDriftThreads;
+  aa.check_drift = panel_drift ? 0 : cfg->check_drift;
   aa.iter = diter.p;
   aa.dstatus = dstat.p;
   aa.wcap = wcap;
@@ -1605,6 +1751,28 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, kfn, args));
+    CK_LAUNCH(ctx);
+  };
+  const int drift_ctas = 2 * ctx->nsm;
+  DevBuf<double2> drift_partial(panel_drift ? (size_t)drift_ctas * kDriftP * kDriftThreads : 1);
+  const size_t drift_smem = sizeof(double2) * ((size_t)kDriftR * (maxit | 1) + (size_t)kDriftR * kDriftP);
+  if (panel_drift)
+    CK(cudaFuncSetAttribute(k_drift_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)drift_smem));
+  // in_loop: the kernels decide from the device iteration counter whether a panel is complete
+  auto launch_drift = [&](bool in_loop, int k0, int k1) {
+    DriftArgs da{};
+    da.n = n;
+    da.V = V.p;
+    da.iter = in_loop ? diter.p : nullptr;
+    da.dstatus = dstat.p;
+    da.k0 = k0;
+    da.k1 = k1;
+    da.partial = drift_partial.p;
+    da.drift = ddrift.p;
+    da.ncta = drift_ctas;
+    k_drift_panel<<<drift_ctas, kDriftThreads, drift_smem, s>>>(da);
+    CK_LAUNCH(ctx);
+    k_drift_finish<<<kDriftP, kDriftThreads, 0, s>>>(da);
     CK_LAUNCH(ctx);
   };
   // one iteration's operator part: w = A M vin (right) or M A vin (left)
@@ -1660,6 +1828,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     ga.cond = cond;
     ga.use_cond = 1;
     launch_arnoldi(ga);
+    if (panel_drift) launch_drift(true, 0, 0);
     cudaGraph_t captured = nullptr;
     CK(cudaStreamEndCapture(s, &captured));
     body_launches = ctx->launches - l0;
@@ -1701,6 +1870,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
       if (ctx->timing) CK(cudaEventRecord(ev[2], s));
       hstatus[0] = 0;
       launch_arnoldi(ha);
+      if (panel_drift) launch_drift(true, 0, 0);
       if (ctx->timing) CK(cudaEventRecord(ev[3], s));
       CK(cudaStreamSynchronize(s));
       if (ctx->timing) {
@@ -1725,7 +1895,12 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   if (m < 1) fail(MDD_ECUDA, "gmres: no iteration completed");
   if (use_graph) ctx->launches += body_launches * (m - 1);  // graph replays of the loop body
   // drift of the final appended vector (krylov.py:152-160)
-  if (cfg->check_drift && !breakdown) {
+  if (panel_drift) {
+    // the vectors after the last complete panel (a panel ending in a breakdown iteration was skipped)
+    const int done_upto = (breakdown && m % kDriftP == 0) ? m - kDriftP : (m / kDriftP) * kDriftP;
+    const int hi_k = breakdown ? m - 1 : m;
+    if (hi_k > done_upto) launch_drift(false, done_upto + 1, hi_k);
+  } else if (cfg->check_drift && !breakdown) {
     k_final_drift<<<m, 256, 0, s>>>(n, m, V.p, (weighted ? DV.p : V.p) + (int64_t)m * n, dtmp.p);
     CK_LAUNCH(ctx);
     k_max_into<<<1, 32, 0, s>>>(dtmp.p, m, ddrift.p + m);

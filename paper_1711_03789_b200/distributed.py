@@ -143,6 +143,11 @@ class Communicator:
         self.handle = h
         self.is_nccl = uid is not None
 
+    def abort(self):
+        """Loopback groups: mark the group failed so the other ranks stop waiting (call from an
+        ``except`` around a rank's work)."""
+        _lib.lib.mdd_comm_abort(self.handle)
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h:

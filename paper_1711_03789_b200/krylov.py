@@ -25,6 +25,9 @@ from .linalg import DeviceCSR, as_device_csr, raise_for
 __all__ = ["KrylovConfig", "KrylovReport", "gmres"]
 
 
+_last_drift = None
+
+
 @dataclass(frozen=True)
 class KrylovConfig:
     """Reference krylov.py:25-43 (+ ``check_orthogonality``, default on as in the reference).
@@ -230,6 +233,8 @@ def gmres(operator, rhs, precond=None, config: KrylovConfig | None = None, *, ou
         raise_for(e)
     m = its.value
     history = hist[: m + 1].copy() if m > 0 else np.array([0.0])
+    global _last_drift
+    _last_drift = drift[: m + 1].copy()  # per-step drift values of the last solve (tests, diagnostics)
     ortho = False
     for step in range(1, m + 1):
         dv = drift[step]

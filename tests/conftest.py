@@ -11,6 +11,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# tests/ref_suite holds the reference's own test files (git-ignored copies) and the `maxwelldd`
+# shim; they are run by tests/test_reference_suite.py in a subprocess, never collected directly
+collect_ignore = ["ref_suite"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libmdd.so")

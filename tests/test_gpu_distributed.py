@@ -120,17 +120,22 @@ def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
     out, errors = [None] * nranks, []
 
     def rank_main(r):
+        comm = None
         try:
             with _lib.use_context(_lib.Context(0)) as ctx:
                 # device objects (spaces, matrices, factors) of this rank live on its own context
                 pr, dr = _case_objects()
-                st = setup_sharded(pr, dr, spec, comm=Communicator(ctx, loopback=(group, r)))
+                comm = Communicator(ctx, loopback=(group, r))
+                st = setup_sharded(pr, dr, spec, comm=comm)
                 applied = st.apply(v)
                 rep = gmres(pr.A, pr.rhs, precond=st, config=cfg)
                 ctx.synchronize()
-                out[r] = (len(st.shard.subdomains), applied, rep)
+                ghost = (st.row_ranges["need"][1] - st.row_ranges["need"][0]) - (st.row_ranges["own"][1] - st.row_ranges["own"][0])
+                out[r] = (len(st.shard.subdomains), applied, rep, ghost)
         except Exception as exc:  # surfaced below
             errors.append((r, exc))
+            if comm is not None:
+                comm.abort()  # the other ranks fail fast instead of waiting at a barrier
 
     threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(nranks)]
     for t in threads:
@@ -139,8 +144,10 @@ def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
         t.join(timeout=900)
     assert not errors, errors
     assert sum(o[0] for o in out) == d.n_subdomains
+    if nranks > 1:  # the exchanges move row ranges, not vectors
+        assert all(o[3] < prob.space.ndof for o in out), [o[3] for o in out]
     first = out[0][2]
-    for _, applied, rep in out:
+    for _, applied, rep, _g in out:
         assert rel(applied, want_apply) < 1e-13
         assert rep.iterations == first.iterations and np.array_equal(rep.x, first.x)
         assert np.array_equal(rep.residual_history, first.residual_history)

@@ -239,6 +239,41 @@ def test_wide_arnoldi_matches_register_path(gpu, monkeypatch, grid, wcap, regs):
     assert np.array_equal(r.x, r2.x)  # fixed summation order: bitwise reruns
 
 
+@pytest.mark.parametrize("maxit", [13, 16, 40])
+def test_panel_drift_matches_ride_along_drift(gpu, monkeypatch, maxit):
+    """The large-slice path computes the orthogonality drift (krylov.py:152-160) in panels of 8
+    new vectors (k_drift_panel: one pass over the basis per 8 iterations); the register path
+    computes it inside the sweeps.  For runs that end inside a panel, on a panel boundary and
+    after several panels, every step 1..m gets a value, and it is the direct definition
+    max_j |<V_j, V_k>| evaluated on the kept basis.  With MGS2 these inner products are pure
+    rounding (1e-17), so each implementation's own rounding is as large as the value: the
+    comparison is absolute, on the scale of the 1e-8 warning threshold they feed."""
+    from paper_1711_03789_b200 import decomp, fem, krylov, mesh, precond
+    from paper_1711_03789_b200.krylov import KrylovConfig, gmres
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(10), "pec")
+    prob = fem.assemble(s, fem.Coefficients(k=6.0, xi=2.0), source=fem.gaussian_source)
+    d = decomp.build_decomposition(s, 2, 2)
+    st = precond.setup(prob, d, precond.PreconditionerSpec("as", "one", xi_prec=2.0), lu_cap=None)
+
+    def direct(V):
+        return np.array([np.abs(V[:, :k].conj().T @ V[:, k]).max() for k in range(1, V.shape[1])])
+
+    cfg = KrylovConfig(tol=1e-14, maxit=maxit, keep_basis=True)
+    base = gmres(prob.A, prob.rhs, precond=st, config=cfg)
+    d_reg = krylov._last_drift.copy()
+    assert base.iterations == maxit and np.isfinite(d_reg[1:]).all()
+    assert np.abs(d_reg[1:] - direct(base.basis)).max() <= 2e-15
+    monkeypatch.setenv("MDD_ARNOLDI_MODE", "2")
+    monkeypatch.setenv("MDD_ARN_GRID", "7")
+    r = gmres(prob.A, prob.rhs, precond=st, config=cfg)
+    d_panel = krylov._last_drift.copy()
+    assert r.iterations == maxit and len(d_panel) == maxit + 1
+    assert np.isfinite(d_panel[1:]).all() and (d_panel[1:] > 0).all()
+    assert np.abs(d_panel[1:] - direct(r.basis)).max() <= 2e-15
+    assert d_panel[1:].max() <= 1e-13 and r.ortho_warning == base.ortho_warning
+
+
 def test_nan_operator_gives_nan_history_not_a_hang(gpu):
     """A NaN in the operator output flows into the residual history as in the reference
     (krylov.py:137-187: NaN dots, `min(nan, prev)` keeps the NaN, the loop runs to maxit);
