@@ -1,0 +1,47 @@
+#!/bin/bash
+# The gpurun recipes of this repo in one place (B200_PROFILING.md rules: ncu only after the same
+# command exited 0 without it; one ncu tool per call).  Usage, from the repo root:
+#   gpurun --timeout 3000 -- 'bash tools/gpu_session.sh check'        GPU suite, smoke, default bench, reference arm
+#   gpurun --timeout 3600 -- 'bash tools/gpu_session.sh launchlist 4' ncu launch list (time + DRAM bytes) of one cfgN bench step
+#   gpurun --timeout 1800 -- 'bash tools/gpu_session.sh arnoldi 4'    ncu --set full of the Arnoldi kernel at cfgN, m ~ 101
+#   gpurun --timeout 1800 -- 'bash tools/gpu_session.sh emulate 4'    per-rank timing against tools/nccl_stub
+#   gpurun --timeout 2000 -- 'bash tools/gpu_session.sh sanitize memcheck'
+mkdir -p gpurun_out
+what=$1; cfg=${2:-4}
+case "$what" in
+check)
+  timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a gpurun_out/pytest_gpu.log
+  tail -n 3 gpurun_out/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -n 1 gpurun_out/smoke.log
+  timeout 1500 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "reference arm rc=$?"
+  timeout 1500 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+  ;;
+launchlist)
+  export MDD_NO_GRAPH=1   # kernels inside the conditional graph node are invisible to ncu
+  timeout 900 python bench.py --config $cfg --steps 1 --warmup 0 --no-cpu > gpurun_out/ll_plain.json 2> gpurun_out/ll_plain.err &&
+  timeout 3000 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -c ${3:-40000} --csv --log-file gpurun_out/launches_cfg$cfg.csv python bench.py --config $cfg --steps 1 --warmup 0 --no-cpu \
+      > gpurun_out/ll_ncu.json 2> gpurun_out/ll_ncu.err
+  echo "ncu rc=$?"
+  python tools/launch_shares.py gpurun_out/launches_cfg$cfg.csv > gpurun_out/launches_cfg${cfg}_summary.md 2>&1
+  cat gpurun_out/launches_cfg${cfg}_summary.md
+  ;;
+arnoldi)
+  python tools/prof_arnoldi.py $cfg 120 > gpurun_out/arn_plain.log 2>&1 &&
+  ncu --set full --clock-control none --import-source on -k regex:k_arnoldi -s 100 -c 1 \
+      -o gpurun_out/prof_arnoldi_cfg$cfg -f python tools/prof_arnoldi.py $cfg 120 > gpurun_out/arn_ncu.log 2>&1
+  echo "ncu rc=$?"; tail -n 2 gpurun_out/arn_plain.log gpurun_out/arn_ncu.log
+  ;;
+emulate)
+  timeout 1500 python tools/rank_emulation.py --config $cfg --ranks 1,2,4,8 --sample-ranks 2 --steps 1 > gpurun_out/rank_emulation_cfg$cfg.log 2>&1
+  echo "rc=$?"; tail -n 12 gpurun_out/rank_emulation_cfg$cfg.log | cut -c1-300
+  ;;
+sanitize)
+  # compute-sanitizer, one tool per call (memcheck | racecheck | synccheck | initcheck); closed on this pool in round 2
+  tool=${2:-memcheck}
+  timeout 300 python tools/sanitize_case.py > gpurun_out/san_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 3 python tools/sanitize_case.py > gpurun_out/san_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -n 12 gpurun_out/san_$tool.log | cut -c1-200
+  ;;
+*) echo "unknown recipe $what"; exit 2;;
+esac
