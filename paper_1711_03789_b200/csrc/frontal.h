@@ -59,6 +59,7 @@ struct LvlTask {
   int64_t out_off;  // forward: uvec index of row r0; backward: xloc index of row r0
   int64_t aux_off;  // forward: gather map (gmap_abs); backward: update list (upd)
   int64_t base;     // local vector index of the node's first pivot
+  int64_t zoff;     // >= 0: the node's vector z was gathered once into zbuf (k_level_gather); -1: gather in the task
   int32_t mat_off, r0, nrow, len, np, m, nch, pad;
 };
 constexpr int kTSolveTaskElems = 2048;  // factor entries per solve task (32 KB)
@@ -128,6 +129,11 @@ struct FrontPlan {
   int64_t upk_total = 0;
   DevBuf<LvlTask> ltasks;
   std::vector<int64_t> lvl_off, lvl_dcap, lvl_zcap;  // forward levels ascending, then backward descending
+  // levels whose fronts are cut into many tasks gather each node's vector once (k_level_gather)
+  // instead of once per task: node descriptors per level and the shared z buffer
+  DevBuf<LvlTask> gnodes;
+  std::vector<int64_t> gnode_off;   // per solve level: [gnode_off[k], gnode_off[k+1]) into gnodes (empty: fused gathers)
+  DevBuf<double2> zbuf;
   void build_solve(const std::vector<std::vector<int32_t>>& lev);
 
   // build from analysed matrices

@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(256, MINB) k_solve_tma(const LvlTask* __restri
                                                    const double2* __restrict__ v,
                                                    const int32_t* __restrict__ gidx,
                                                    double2* __restrict__ fpst, double2* __restrict__ uvec,
-                                                   double2* __restrict__ xloc, int dcap) {
+                                                   double2* __restrict__ xloc, int dcap,
+                                                   const double2* __restrict__ zbuf) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ double2 red[8];
@@ -123,7 +124,15 @@ __global__ void __launch_bounds__(256, MINB) k_solve_tma(const LvlTask* __restri
   // everything below reads vectors written by the previous level (or the
   // kernels before the solve): wait for the prerequisite grid to complete
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (FWD) {
+  if (tk.zoff >= 0) {
+    // the node's vector was assembled once by k_level_gather: a contiguous copy
+    const double2* zn = zbuf + tk.zoff;
+    if (FWD) {
+      for (int q = threadIdx.x; q < np + nrow; q += blockDim.x) z[q] = zn[q < np ? q : tk.r0 + q];
+    } else {
+      for (int q = threadIdx.x; q < tk.m; q += blockDim.x) z[q] = zn[q];
+    }
+  } else if (FWD) {
     const int32_t* ga = gabs + tk.aux_off;
     const int m = tk.m;
     for (int q = threadIdx.x; q < np + nrow; q += blockDim.x) {
@@ -156,23 +165,61 @@ __global__ void __launch_bounds__(256, MINB) k_solve_tma(const LvlTask* __restri
   }
 }
 
-// ------------------------------------------------------------- host side
-static int64_t env_int(const char* name, int64_t dflt) {
-  const char* s = getenv(name);
-  return s ? std::max<int64_t>(1, atoll(s)) : dflt;
+// One CTA per node of a level whose fronts are cut into many tasks: the node's vector z
+// (forward: [f_P ; children's updates on the U rows], backward: [f_P ; x_U]) is assembled
+// once here instead of once per task (a front with np = 1000 has ~350 forward tasks, each of
+// which would repeat the same gathers through the children's maps).
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_level_gather(const LvlTask* __restrict__ nodes, int64_t first,
+                                                      const int32_t* __restrict__ gabs,
+                                                      const int32_t* __restrict__ upd,
+                                                      const double2* __restrict__ bloc,
+                                                      const double2* __restrict__ v,
+                                                      const int32_t* __restrict__ gidx, double2* __restrict__ fpst,
+                                                      const double2* __restrict__ uvec,
+                                                      const double2* __restrict__ xloc, double2* __restrict__ zbuf) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const LvlTask tk = nodes[first + blockIdx.x];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double2* zn = zbuf + tk.zoff;
+  const int np = tk.np, m = tk.m;
+  const int64_t base = tk.base;
+  if (FWD) {
+    const int32_t* ga = gabs + tk.aux_off;
+    for (int pos = threadIdx.x; pos < m; pos += blockDim.x) {
+      double2 f = make_double2(0.0, 0.0);
+      if (pos < np) f = v ? v[gidx[base + pos]] : bloc[base + pos];
+      for (int ci = 0; ci < tk.nch; ++ci) {
+        const int g = ga[(int64_t)ci * m + pos];
+        if (g >= 0) f = cadd(f, uvec[g]);
+      }
+      zn[pos] = f;
+      if (pos < np) fpst[base + pos] = f;
+    }
+  } else {
+    const int32_t* up = upd + tk.aux_off;
+    const int64_t moff = tk.mat_off;
+    for (int q = threadIdx.x; q < m; q += blockDim.x) zn[q] = q < np ? fpst[base + q] : xloc[moff + up[q - np]];
+  }
 }
 
+// ------------------------------------------------------------- host side
 void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
-  const int64_t te = env_int("MDD_TSOLVE_ELEMS", kTSolveTaskElems);
+  const int64_t te = kTSolveTaskElems;
   // backward tasks gather the node's whole z (m entries) per task: a floor on
   // the rows per task bounds that overhead for large fronts
-  const int64_t minrows = env_int("MDD_TSOLVE_MINROWS", kTSolveMinRows);
-  std::vector<LvlTask> ht;
+  const int64_t minrows = kTSolveMinRows;
+  std::vector<LvlTask> ht, hg;
+  gnode_off.assign(1, 0);
+  int64_t zmax = 1;
   lvl_off.assign(1, 0);
   lvl_dcap.clear();
   lvl_zcap.clear();
   auto level_tasks = [&](int L, int kind) {
     int64_t dcap = 8, zc = 8;
+    const size_t first_task = ht.size();
+    int64_t zoff = 0;
+    std::vector<LvlTask> nodes_here;
     for (int32_t g : lev[L]) {
       const NodeDev& nd = h_nodes[g];
       const int len = kind == 0 ? nd.np : nd.m;
@@ -180,9 +227,21 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
       int rows = (int)std::max<int64_t>(1, len > 0 ? te / len : te);
       if (kind == 1) rows = (int)std::max<int64_t>(rows, std::min<int64_t>(minrows, (200 * 1024 / 16 - len) / std::max(1, len)));
       int r = 0;
+      {
+        LvlTask nt{};  // node descriptor for k_level_gather
+        nt.base = (int64_t)nd.mat_off + nd.pivb;
+        nt.aux_off = kind == 0 ? nd.gmap_off : nd.upd_off;
+        nt.mat_off = nd.mat_off;
+        nt.np = nd.np;
+        nt.m = nd.m;
+        nt.nch = nd.nch;
+        nt.zoff = zoff;
+        nodes_here.push_back(nt);
+      }
       do {  // a zero-row forward task still assembles fp (fpst) for its node
         const int r1 = std::min(nrows, r + rows);
         LvlTask t{};
+        t.zoff = zoff;
         t.off = (kind == 0 ? nd.upk_off : nd.front_off) + (int64_t)r * len;
         t.base = (int64_t)nd.mat_off + nd.pivb;
         t.out_off = kind == 0 ? nd.uvec_off + r : t.base + r;
@@ -199,7 +258,19 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
         zc = std::max<int64_t>(zc, kind == 0 ? (int64_t)nd.np + (r1 - r) : nd.m);
         r = r1;
       } while (r < nrows);
+      zoff += nd.m;
     }
+    // gather once per node where the fronts are cut into many tasks; otherwise the tasks keep
+    // their fused gathers (one task per small front: nothing is repeated)
+    const size_t ntask = ht.size() - first_task;
+    // threshold swept on cfg4 (apply per solve: off 2056, 2x 2010, 4x 1983, 8x 1980 ms)
+    if (!nodes_here.empty() && ntask >= 6 * nodes_here.size()) {
+      hg.insert(hg.end(), nodes_here.begin(), nodes_here.end());
+      zmax = std::max(zmax, zoff);
+    } else {
+      for (size_t k = first_task; k < ht.size(); ++k) ht[k].zoff = -1;
+    }
+    gnode_off.push_back((int64_t)hg.size());
     lvl_off.push_back((int64_t)ht.size());
     lvl_dcap.push_back((dcap + 7) / 8 * 8);
     lvl_zcap.push_back(zc);
@@ -208,6 +279,8 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
   for (int L = 0; L < nlevels; ++L) level_tasks(L, 0);
   for (int L = nlevels - 1; L >= 0; --L) level_tasks(L, 1);
   ltasks.upload(ht, ctx->stream);
+  if (!hg.empty()) gnodes.upload(hg, ctx->stream);
+  zbuf = DevBuf<double2>(zmax);
   static bool attr = false;  // per-function attribute shared by every plan
   if (!attr) {
     CK(cudaFuncSetAttribute(k_solve_tma<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -223,13 +296,30 @@ void FrontPlan::build_solve(const std::vector<std::vector<int32_t>>& lev) {
 void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
   if (nnodes == 0) return;
   const int nl = nlevels;
-  static const int pf = (int)env_int("MDD_TSOLVE_PF", kTSolvePrefetch);
-  static const bool pdl = !getenv("MDD_PDL") || atoi(getenv("MDD_PDL")) != 0;  // MDD_PDL=0: plain launches
-  static const int minb = getenv("MDD_SOLVE_MINB") ? atoi(getenv("MDD_SOLVE_MINB")) : 6;  // register cap (40 regs: 6 CTAs/SM; measured best)
+  const int pf = kTSolvePrefetch;
+  const bool pdl = true;  // programmatic dependent launch between the level kernels (measured 1.296 -> 1.233 ms per cfg1 apply)
+  const int minb = 6;     // register cap: 40 registers, 6 CTAs per SM (swept 0/6/8 in round 1)
   const int64_t total = lvl_off[2 * nl];
   for (int k = 0; k < 2 * nl; ++k) {
     const int64_t n = lvl_off[k + 1] - lvl_off[k];
     if (!n) continue;
+    const int64_t ng = gnode_off[k + 1] - gnode_off[k];
+    if (ng > 0) {
+      cudaLaunchConfig_t gc = {};
+      gc.gridDim = dim3((unsigned)ng);
+      gc.blockDim = dim3(256);
+      gc.stream = s;
+      cudaLaunchAttribute ga[1];
+      ga[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      ga[0].val.programmaticStreamSerializationAllowed = 1;
+      gc.attrs = ga;
+      gc.numAttrs = pdl ? 1 : 0;
+      auto gfn = k < nl ? k_level_gather<true> : k_level_gather<false>;
+      CK(cudaLaunchKernelEx(&gc, gfn, (const LvlTask*)gnodes.p, gnode_off[k], (const int32_t*)gmap_abs.p,
+                            (const int32_t*)upd.p, (const double2*)bloc.p, v, gidx, fpst.p, (const double2*)uvec.p,
+                            (const double2*)xloc.p, zbuf.p));
+      CK_LAUNCH(ctx);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)n);
     cfg.blockDim = dim3(256);
@@ -244,7 +334,7 @@ void FrontPlan::solve(cudaStream_t s, const double2* v, const int32_t* gidx) {
                       : (minb == 8 ? k_solve_tma<false, 8> : minb == 6 ? k_solve_tma<false, 6> : k_solve_tma<false, 0>);
     CK(cudaLaunchKernelEx(&cfg, kfn, (const LvlTask*)ltasks.p, lvl_off[k], total, pf, (const int32_t*)gmap_abs.p,
                           (const int32_t*)upd.p, (const double2*)fronts.p, (const double2*)bloc.p, v, gidx, fpst.p,
-                          uvec.p, xloc.p, (int)lvl_dcap[k]));
+                          uvec.p, xloc.p, (int)lvl_dcap[k], (const double2*)zbuf.p));
     CK_LAUNCH(ctx);
   }
 }
