@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kArnThreads, 1) k_arnoldi(ArnoldiArgs a) {
 // partials (fixed tree -> bitwise reproducible); one block barrier.  `sh` (64 double2) is
 // double-buffered by the caller.
 __device__ __forceinline__ void block_sum_t0_wide(double2& a, double2& b, double2* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   a = warp_sum2(a);
   b = warp_sum2(b);
   if (lane == 0) {
@@ -569,8 +569,9 @@ __device__ __forceinline__ void block_sum_t0_wide(double2& a, double2& b, double
   }
   __syncthreads();
   if (wid == 0) {
-    a = warp_sum2(sh[2 * lane]);
-    b = warp_sum2(sh[2 * lane + 1]);
+    const double2 zero = make_double2(0.0, 0.0);
+    a = warp_sum2(lane < nw ? sh[2 * lane] : zero);
+    b = warp_sum2(lane < nw ? sh[2 * lane + 1] : zero);
   }
 }
 
@@ -609,41 +610,64 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 // handful of loads and DFMAs (the generic loop ran at ~150 instructions per element under the
 // 64-register cap of a 1024-thread CTA and was issue-bound, ncu r02 profile); the slice is
 // walked in two pieces, w in shared memory and w in L2, so there is no per-element tier test.
-template <bool HASB, bool HASD, bool DOWN>
+// Template parameters: T threads per CTA; E > 0: the tail of w (beyond shared memory) lives in
+// registers, E elements per thread (T x E must cover it: cfg4's 23.8k-element slices = 13.6k in
+// shared memory + 512 x 20 in registers), so w never touches the L2 and the L2 is left to the
+// basis; E = 0: the tail stays in L2 under an evict_last policy (any slice length).
+template <int T, int E, bool HASB, bool HASD, bool DOWN>
 __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const double2* __restrict__ B,
                                            const double2* __restrict__ D, double2* __restrict__ WS,
-                                           double2* __restrict__ wg, int ws, int len, double2 h, uint64_t pol_first,
-                                           uint64_t pol_last, double2& acc, double2& dacc) {
+                                           double2* __restrict__ wg, double2 (&W)[E > 0 ? E : 1], int ws, int len,
+                                           double2 h, uint64_t pol_first, uint64_t pol_last, double2& acc,
+                                           double2& dacc) {
   // piece 1: w in shared memory
   auto piece1 = [&]() {
-  for (int iu = threadIdx.x; iu < ws; iu += kWideThreads) {
-    const int i = DOWN ? ws - 1 - iu : iu;
-    const double2 av = ld_hint(A + i, pol_first);
-    double2 bv, dv;
-    if (HASB) bv = __ldcg(B + i);
-    if (HASD) dv = __ldcg(D + i);
-    const double2 wi = caxmy(WS[i], h, av);
-    WS[i] = wi;
-    const double2 x = HASB ? bv : wi;
-    acc = cdotc_acc(acc, x, wi);
-    if (HASD) dacc = cdotc_acc(dacc, x, dv);
-  }
+    for (int iu = threadIdx.x; iu < ws; iu += T) {
+      const int i = DOWN ? ws - 1 - iu : iu;
+      const double2 av = ld_hint(A + i, pol_first);
+      double2 bv, dv;
+      if (HASB) bv = __ldcg(B + i);
+      if (HASD) dv = __ldcg(D + i);
+      const double2 wi = caxmy(WS[i], h, av);
+      WS[i] = wi;
+      const double2 x = HASB ? bv : wi;
+      acc = cdotc_acc(acc, x, wi);
+      if (HASD) dacc = cdotc_acc(dacc, x, dv);
+    }
   };
-  // piece 2: the tail of w, resident in L2 (evict_last)
+  // piece 2: the tail of w
   auto piece2 = [&]() {
-  for (int iu = ws + threadIdx.x; iu < len; iu += kWideThreads) {
-    const int i = DOWN ? len - 1 - (iu - ws) : iu;
-    const double2 av = ld_hint(A + i, pol_first);
-    const double2 wv = ld_hint(wg + i, pol_last);
-    double2 bv, dv;
-    if (HASB) bv = __ldcg(B + i);
-    if (HASD) dv = __ldcg(D + i);
-    const double2 wi = caxmy(wv, h, av);
-    st_hint2(wg + i, wi, pol_last);
-    const double2 x = HASB ? bv : wi;
-    acc = cdotc_acc(acc, x, wi);
-    if (HASD) dacc = cdotc_acc(dacc, x, dv);
-  }
+    if constexpr (E > 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = ws + (int)threadIdx.x + e * T;
+        if (i < len) {
+          const double2 av = ld_hint(A + i, pol_first);
+          double2 bv, dv;
+          if (HASB) bv = __ldcg(B + i);
+          if (HASD) dv = __ldcg(D + i);
+          const double2 wi = caxmy(W[e], h, av);
+          W[e] = wi;
+          const double2 x = HASB ? bv : wi;
+          acc = cdotc_acc(acc, x, wi);
+          if (HASD) dacc = cdotc_acc(dacc, x, dv);
+        }
+      }
+    } else {
+      for (int iu = ws + threadIdx.x; iu < len; iu += T) {
+        const int i = DOWN ? len - 1 - (iu - ws) : iu;
+        const double2 av = ld_hint(A + i, pol_first);
+        const double2 wv = ld_hint(wg + i, pol_last);
+        double2 bv, dv;
+        if (HASB) bv = __ldcg(B + i);
+        if (HASD) dv = __ldcg(D + i);
+        const double2 wi = caxmy(wv, h, av);
+        st_hint2(wg + i, wi, pol_last);
+        const double2 x = HASB ? bv : wi;
+        acc = cdotc_acc(acc, x, wi);
+        if (HASD) dacc = cdotc_acc(dacc, x, dv);
+      }
+    }
   };
   if (DOWN) {  // the top of the slice (fetched last by the upward pass before) first
     piece2();
@@ -654,10 +678,11 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
   }
 }
 
-__global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a) {
+template <int T, int E>
+__global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
   extern __shared__ double2 col[];  // m+1, identical in every CTA; then the w head
   __shared__ double2 red[68 + 2 * kMaxArnCTAs + 2 * 64];
-  __shared__ double cmax_w[kWideThreads / 32];
+  __shared__ double cmax_w[T / 32];
   const int G = gridDim.x;
   const int m = *a.iter + 1;
   const int64_t n = a.n;
@@ -672,20 +697,42 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
   double2* WS = col + (a.maxit + 1);
   const int ws = (int)min((int64_t)len, a.wcap);
   double2* wg = a.w + lo;
-  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-  for (int j = threadIdx.x; j <= m; j += kWideThreads) col[j] = make_double2(0.0, 0.0);
+  double2 W[E > 0 ? E : 1];
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();  // (evict_normal for the w tail: cfg4 Arnoldi 1265 -> 1290 ms)
+  for (int j = threadIdx.x; j <= m; j += T) col[j] = make_double2(0.0, 0.0);
   const double2 zero = make_double2(0.0, 0.0);
   double dmax = 0.0;
   // pass -1: load w into its tiers, dot with X_0 (+ drift partner)
   {
     const double2* B = xvec(0);
     double2 acc = zero, dacc = zero;
-    for (int i = threadIdx.x; i < len; i += kWideThreads) {
+    for (int i = threadIdx.x; i < ws; i += T) {
       const double2 wi = __ldcg(wg + i);
-      if (i < ws) WS[i] = wi;
+      WS[i] = wi;
       const double2 x = __ldcg(B + i);
       acc = cdotc_acc(acc, x, wi);
       if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
+    }
+    if constexpr (E > 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = ws + (int)threadIdx.x + e * T;
+        W[e] = zero;
+        if (i < len) {
+          const double2 wi = __ldcg(wg + i);
+          W[e] = wi;
+          const double2 x = __ldcg(B + i);
+          acc = cdotc_acc(acc, x, wi);
+          if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
+        }
+      }
+    } else {
+      for (int i = ws + threadIdx.x; i < len; i += T) {
+        const double2 wi = __ldcg(wg + i);
+        const double2 x = __ldcg(B + i);
+        acc = cdotc_acc(acc, x, wi);
+        if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
+      }
     }
     block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64);
     if (threadIdx.x == 0) publish(slots(0), a.pad, acc, dacc);
@@ -702,14 +749,17 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
     // odd passes sweep the slice downwards when the vectors exceed what the L2 retains: the
     // chunks of X_{t+1} fetched last in pass t are then the first ones pass t+1 needs again
     const bool down = a.zigzag && (t & 1);
-    if (!hasB) wide_sweep<false, false, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+#define MDD_SWEEP(HB, HD, DN) \
+  wide_sweep<T, E, HB, HD, DN>(A, B, dvm1, WS, wg, W, ws, len, h, pol_first, pol_last, acc, dacc)
+    if (!hasB) MDD_SWEEP(false, false, false);
     else if (hasD) {
-      if (down) wide_sweep<true, true, true>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
-      else wide_sweep<true, true, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+      if (down) MDD_SWEEP(true, true, true);
+      else MDD_SWEEP(true, true, false);
     } else {
-      if (down) wide_sweep<true, false, true>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
-      else wide_sweep<true, false, false>(A, B, dvm1, WS, wg, ws, len, h, pol_first, pol_last, acc, dacc);
+      if (down) MDD_SWEEP(true, false, true);
+      else MDD_SWEEP(true, false, false);
     }
+#undef MDD_SWEEP
     block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64 * (t & 1));
     if (threadIdx.x == 0) {
       publish(slots(t + 1), a.pad, acc, dacc);
@@ -732,21 +782,34 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_arnoldi_wide(ArnoldiArgs a)
   if (threadIdx.x == 0) col[m] = make_double2(hlast, 0.0);
   __syncthreads();
   double cmax = 0.0;
-  for (int j = threadIdx.x; j <= m; j += kWideThreads) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
+  for (int j = threadIdx.x; j <= m; j += T) cmax = fmax(cmax, hypot(col[j].x, col[j].y));
   cmax = warp_max(cmax);
   if ((threadIdx.x & 31) == 0) cmax_w[threadIdx.x >> 5] = cmax;
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kWideThreads / 32; ++k) cmax = fmax(cmax, cmax_w[k]);
+  for (int k = 0; k < T / 32; ++k) cmax = fmax(cmax, cmax_w[k]);
   const bool breakdown = hlast <= 1e-13 * cmax;
   if (!breakdown) {
     double2* vm = a.V + (int64_t)m * n + lo;
     double2* vin = a.vin + lo;
-    for (int i = threadIdx.x; i < len; i += kWideThreads) {
-      const double2 wi = i < ws ? WS[i] : __ldcg(wg + i);
+    for (int i = threadIdx.x; i < (E > 0 ? ws : len); i += T) {
+      // the tail's last read demotes its L2 lines (evict_first): left as evict_last they sit in
+      // the L2 through the next preconditioner apply (measured: 65 ms per cfg4 solve)
+      const double2 wi = i < ws ? WS[i] : ld_hint(wg + i, pol_first);
       const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
       vm[i] = q;
       vin[i] = q;
+    }
+    if constexpr (E > 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = ws + (int)threadIdx.x + e * T;
+        if (i < len) {
+          const double2 q = make_double2(W[e].x / hlast, W[e].y / hlast);
+          vm[i] = q;
+          vin[i] = q;
+        }
+      }
     }
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -1683,7 +1746,9 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
                                           (mode == 1 ? (size_t)kArnThreads * kArnE
                                                      : mode == 2 ? (size_t)std::min<int64_t>(slice, wcap) : 0));
   using ArnFn = void (*)(ArnoldiArgs);
-  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide : k_arnoldi<0>;
+  // (a 512-thread variant holding the tail of w in 20 registers per thread instead of L2 was
+  // measured on cfg4: Arnoldi 1291 -> 1358 ms, spills and half the warps; not kept)
+  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide<kWideThreads, 0> : k_arnoldi<0>;
   const int arn_threads = mode == 2 ? kWideThreads : kArnThreads;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;
