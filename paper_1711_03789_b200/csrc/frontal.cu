@@ -78,60 +78,6 @@ __global__ void k_front_scatter(int64_t n, const int64_t* __restrict__ pos,
   }
 }
 
-// In-place Gauss-Jordan inverse of the kb x kb pivot block (no pivoting),
-// padded with the identity to 32x32; tracks pivot magnitudes.  One warp per
-// node (kInvWarps nodes per CTA), the block in shared memory, lane i owning
-// row i: per pivot, lane j scales column j of the pivot row, then every lane
-// eliminates its own row with the broadcast pivot row.  Warp-synchronous only.
-constexpr int kInvWarps = 4;
-__global__ void __launch_bounds__(32 * kInvWarps) k_invert(const NodeDev* __restrict__ nodes,
-                                                           const int32_t* __restrict__ act,
-                                                           int nact, int step,
-                                                           const double2* __restrict__ fronts,
-                                                           double2* __restrict__ pbuf,
-                                                           double* __restrict__ pivstat) {
-  extern __shared__ double2 invsm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ai = blockIdx.x * kInvWarps + w;
-  if (ai >= nact) return;  // warp-uniform; no block barriers below
-  double2(*P)[kPB + 1] = reinterpret_cast<double2(*)[kPB + 1]>(invsm + w * kPB * (kPB + 1));
-  const int node = act[ai];
-  const NodeDev nd = nodes[node];
-  const int K0 = step * kPB;
-  const int kb = min(kPB, nd.np - K0);
-  const double2* T = fronts + nd.front_off;
-  for (int r = 0; r < kPB; ++r)
-    P[r][lane] = (r < kb && lane < kb) ? T[(int64_t)(K0 + r) * nd.m + K0 + lane]
-                                       : make_double2(r == lane ? 1.0 : 0.0, 0.0);
-  __syncwarp();
-  double pmin = INFINITY, pmax = 0.0;
-  for (int p = 0; p < kb; ++p) {
-    const double2 piv = P[p][p];
-    const double2 aip = P[lane][p];
-    const double2 np_ = cdiv(lane == p ? make_double2(1.0, 0.0) : P[p][lane], piv);
-    __syncwarp();
-    P[p][lane] = np_;
-    __syncwarp();
-    if (lane != p) {
-#pragma unroll 8
-      for (int j = 0; j < kPB; ++j) {
-        const double2 base = (j == p) ? make_double2(0.0, 0.0) : P[lane][j];
-        P[lane][j] = csub(base, cmul(aip, P[p][j]));
-      }
-    }
-    const double am = hypot(piv.x, piv.y);
-    pmin = fmin(pmin, isfinite(am) ? am : 0.0);
-    pmax = fmax(pmax, isfinite(am) ? am : INFINITY);
-    __syncwarp();
-  }
-  double2* out = pbuf + (int64_t)ai * kPB * kPB;
-  for (int r = 0; r < kPB; ++r) out[r * kPB + lane] = P[r][lane];
-  if (lane == 0) {
-    pivstat[2 * node] = fmin(pivstat[2 * node], pmin);
-    pivstat[2 * node + 1] = fmax(pivstat[2 * node + 1], pmax);
-  }
-}
-
 // Whole pivot-block inverse of a small front (np <= 32 levels) in one CTA,
 // the block in shared memory: F_PP <- -F_PP^{-1} by unpivoted in-place
 // Gauss-Jordan.  Per pivot, the pivot row and column are copied to shared
@@ -187,7 +133,7 @@ __global__ void __launch_bounds__(256) k_gj_smem(const NodeDev* __restrict__ nod
 }
 
 // Inverse of the 32x32 pivot block of one sweep step, one 256-thread CTA
-// per active node (replaces the one-warp k_invert, kept as MDD_INV_WARP=1:
+// per active node (replaced the one-warp k_invert of round 1:
 // 10 us instead of 59 us
 // per step at the cfg1 root level).  The kb x kb diagonal block at
 // K0 = step*kPB, padded with the identity, is held in registers (thread
@@ -889,7 +835,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     // (k_gj_smem is issue-bound at ~30 instructions per element update; it
     // beats the sweeps for np <= 32 only, measured on the B200)
     lev_gj_nb.push_back(lnp <= 32 ? lnp : 0);
-    if (getenv("MDD_NO_GJ_SMALL")) lev_gj_nb.back() = 0;
     for (int32_t g : lev[L])
       if (lev_gj_nb.back() && h_nodes[g].np > 0) h_gjs.push_back(g);
     lev_gjs_off.push_back((int64_t)h_gjs.size());
@@ -973,8 +918,6 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
                             (int)(sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1)))));
     CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem));
     CK(cudaFuncSetAttribute(k_gj_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double2) * 96 * 96)));
-    CK(cudaFuncSetAttribute(k_invert, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(double2) * kInvWarps * kPB * (kPB + 1))));
     attr_set = true;
   }
   build_solve(lev);
@@ -1007,8 +950,6 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s, const int* sym_flag)
   k_pivinit<<<gblocks(nnodes, 256, 1024), 256, 0, s>>>(pivstat.p, nnodes);
   CK_LAUNCH(ctx);
   const size_t upd_smem = sizeof(double2) * (kTile * (kPB + 1) + kPB * (kTile + 1));
-  const size_t inv_smem = sizeof(double2) * kInvWarps * kPB * (kPB + 1);
-  static const bool inv_warp = getenv("MDD_INV_WARP") != nullptr;  // A/B: the one-warp k_invert
   for (int L = 0; L < nlevels; ++L) {
     const int64_t ni = lev_init_off[L + 1] - lev_init_off[L];
     if (ni) {
@@ -1042,11 +983,7 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s, const int* sym_flag)
       const int64_t p0 = step_panel_off[si], npn = step_panel_off[si + 1] - p0;
       const int64_t t0 = step_tile_off[si], ntl = step_tile_off[si + 1] - t0;
       if (!na) continue;
-      if (inv_warp)
-        k_invert<<<(unsigned)((na + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, inv_smem, s>>>(
-            nodes.p, act_node.p + a0, (int)na, st, fronts.p, pbuf.p, pivstat.p);
-      else
-        k_gj_small<2, true><<<(unsigned)na, 256, 0, s>>>(nodes.p, act_node.p + a0, fronts.p, pivstat.p, st, pbuf.p);
+      k_gj_small<2, true><<<(unsigned)na, 256, 0, s>>>(nodes.p, act_node.p + a0, fronts.p, pivstat.p, st, pbuf.p);
       CK_LAUNCH(ctx);
       k_panel<<<(unsigned)npn, kPanelCols, 0, s>>>(panel_tasks.p + p0, nodes.p, act_node.p + a0,
                                                    act_woff.p + a0, st, fronts.p, pbuf.p, wbuf.p);

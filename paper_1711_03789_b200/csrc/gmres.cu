@@ -576,14 +576,14 @@ __device__ __forceinline__ void block_sum_t0_wide(double2& a, double2& b, double
 }
 
 // ------------------------------------------------------------------ WIDE
-// Unweighted MGS2 for large slices with 1024 threads per CTA (32 warps, 64 registers
-// each): the streaming passes are issue- and latency-bound with 8 warps (ncu on the
+// Unweighted MGS2 for large slices with many warps per CTA: the streaming passes are issue- and latency-bound with 8 warps (ncu on the
 // 8-warp kernels: 0.15 instructions per cycle per scheduler, ~13 cycles per dependent
 // instruction), so the parallelism comes from warps, not from per-thread unrolling.
 // w lives in shared memory as far as it fits (a.wcap elements), the rest in L2 with an
 // evict_last policy; the axpy operand (second and last use of a basis chunk) is loaded
 // with evict_first so the incoming vector replaces it and not the vector needed next.
-constexpr int kWideThreads = 1024;
+constexpr int kWideThreads = 1024;  // 32 warps x 64 registers
+constexpr int kWideU = 2;          // elements per thread with their loads in flight together
 
 __device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t policy) {
   double2 v;
@@ -620,19 +620,34 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
                                            double2* __restrict__ wg, double2 (&W)[E > 0 ? E : 1], int ws, int len,
                                            double2 h, uint64_t pol_first, uint64_t pol_last, double2& acc,
                                            double2& dacc) {
-  // piece 1: w in shared memory
+  // piece 1: w in shared memory.  kWideU elements per thread are loaded before any is used: the
+  // un-unrolled loop had one element's loads in flight per thread and ran at DRAM/L2 latency
+  // per trip (ncu, profiles/r02_prof_wide_final_cfg4.ncu-rep: long scoreboard 36 warps per issue)
   auto piece1 = [&]() {
-    for (int iu = threadIdx.x; iu < ws; iu += T) {
-      const int i = DOWN ? ws - 1 - iu : iu;
-      const double2 av = ld_hint(A + i, pol_first);
-      double2 bv, dv;
-      if (HASB) bv = __ldcg(B + i);
-      if (HASD) dv = __ldcg(D + i);
-      const double2 wi = caxmy(WS[i], h, av);
-      WS[i] = wi;
-      const double2 x = HASB ? bv : wi;
-      acc = cdotc_acc(acc, x, wi);
-      if (HASD) dacc = cdotc_acc(dacc, x, dv);
+    for (int i0 = threadIdx.x; i0 < ws; i0 += kWideU * T) {
+      double2 av[kWideU], bv[kWideU], dv[kWideU];
+#pragma unroll
+      for (int u = 0; u < kWideU; ++u) {
+        // out-of-range lanes load a clamped (valid) element and are masked below: no branch
+        // around the loads, so all kWideU go out back to back
+        const int iu = min(i0 + u * T, ws - 1);
+        const int i = DOWN ? ws - 1 - iu : iu;
+        av[u] = ld_hint(A + i, pol_first);
+        if (HASB) bv[u] = __ldcg(B + i);
+        if (HASD) dv[u] = __ldcg(D + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kWideU; ++u) {
+        const int iu = i0 + u * T;
+        if (iu < ws) {
+          const int i = DOWN ? ws - 1 - iu : iu;
+          const double2 wi = caxmy(WS[i], h, av[u]);
+          WS[i] = wi;
+          const double2 x = HASB ? bv[u] : wi;
+          acc = cdotc_acc(acc, x, wi);
+          if (HASD) dacc = cdotc_acc(dacc, x, dv[u]);
+        }
+      }
     }
   };
   // piece 2: the tail of w
@@ -654,18 +669,29 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
         }
       }
     } else {
-      for (int iu = ws + threadIdx.x; iu < len; iu += T) {
-        const int i = DOWN ? len - 1 - (iu - ws) : iu;
-        const double2 av = ld_hint(A + i, pol_first);
-        const double2 wv = ld_hint(wg + i, pol_last);
-        double2 bv, dv;
-        if (HASB) bv = __ldcg(B + i);
-        if (HASD) dv = __ldcg(D + i);
-        const double2 wi = caxmy(wv, h, av);
-        st_hint2(wg + i, wi, pol_last);
-        const double2 x = HASB ? bv : wi;
-        acc = cdotc_acc(acc, x, wi);
-        if (HASD) dacc = cdotc_acc(dacc, x, dv);
+      for (int i0 = ws + threadIdx.x; i0 < len; i0 += kWideU * T) {
+        double2 av[kWideU], bv[kWideU], dv[kWideU], wv[kWideU];
+#pragma unroll
+        for (int u = 0; u < kWideU; ++u) {
+          const int iu = min(i0 + u * T, len - 1);
+          const int i = DOWN ? len - 1 - (iu - ws) : iu;
+          av[u] = ld_hint(A + i, pol_first);
+          wv[u] = ld_hint(wg + i, pol_last);
+          if (HASB) bv[u] = __ldcg(B + i);
+          if (HASD) dv[u] = __ldcg(D + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kWideU; ++u) {
+          const int iu = i0 + u * T;
+          if (iu < len) {
+            const int i = DOWN ? len - 1 - (iu - ws) : iu;
+            const double2 wi = caxmy(wv[u], h, av[u]);
+            st_hint2(wg + i, wi, pol_last);
+            const double2 x = HASB ? bv[u] : wi;
+            acc = cdotc_acc(acc, x, wi);
+            if (HASD) dacc = cdotc_acc(dacc, x, dv[u]);
+          }
+        }
       }
     }
   };
