@@ -582,6 +582,23 @@ __device__ __forceinline__ void block_sum_t0_wide(double2& a, double2& b, double
 // w lives in shared memory as far as it fits (a.wcap elements), the rest in L2 with an
 // evict_last policy; the axpy operand (second and last use of a basis chunk) is loaded
 // with evict_first so the incoming vector replaces it and not the vector needed next.
+#ifdef MDD_ARN_TRACE
+// tools build only (tools/arn_trace.py): per-CTA timeline of one k_arnoldi_wide launch
+__device__ unsigned long long g_arn_trace[(2 * 512 + 1) * kMaxArnCTAs * 2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+extern "C" int mdd_debug_arn_trace(unsigned long long* out, size_t count) {
+  return (int)cudaMemcpyFromSymbol(out, g_arn_trace, count * sizeof(unsigned long long));
+}
+#define ARN_TRACE(step, which)                                                                  \
+  if (threadIdx.x == 0 && (step) < 2 * 512 + 1)                                                  \
+    g_arn_trace[((size_t)(step) * kMaxArnCTAs + blockIdx.x) * 2 + (which)] = gtimer();
+#else
+#define ARN_TRACE(step, which)
+#endif
 constexpr int kWideThreads = 1024;  // 32 warps x 64 registers
 constexpr int kWideU = 2;          // elements per thread with their loads in flight together
 
@@ -728,6 +745,14 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
   for (int j = threadIdx.x; j <= m; j += T) col[j] = make_double2(0.0, 0.0);
   const double2 zero = make_double2(0.0, 0.0);
   double dmax = 0.0;
+#ifdef MDD_ARN_TRACE
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_arn_trace[((size_t)(2 * 512) * kMaxArnCTAs + blockIdx.x) * 2] = smid;
+    g_arn_trace[((size_t)(2 * 512) * kMaxArnCTAs + blockIdx.x) * 2 + 1] = gtimer();
+  }
+#endif
   // pass -1: load w into its tiers, dot with X_0 (+ drift partner)
   {
     const double2* B = xvec(0);
@@ -767,6 +792,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
     const bool hasB = t + 1 < nsteps, hasD = do_drift && t + 1 < m - 1;
     double2 h, d;
     gather_sum(slots(t), G, a.pad, false, red, h, d, do_drift && t < m - 1);
+    ARN_TRACE(t, 0)
     if (do_drift && t < m - 1) dmax = fmax(dmax, hypot(d.x, d.y));
     if (threadIdx.x == 0) col[t % m] = cadd(col[t % m], h);
     const double2* A = xvec(t);
@@ -787,6 +813,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
     }
 #undef MDD_SWEEP
     block_sum_t0_wide(acc, dacc, red + 68 + 2 * kMaxArnCTAs + 64 * (t & 1));
+    ARN_TRACE(t, 1)
     if (threadIdx.x == 0) {
       publish(slots(t + 1), a.pad, acc, dacc);
       // DRAM idles while the CTAs exchange their partial sums: pull the head of the slice the
