@@ -287,6 +287,13 @@ int mdd_prec_pivot_ratio(const mdd_prec* P, double* sub_ratio, double* coarse_ra
 /* statistics: [n_fronts, max_front, factor_entries, factor_flops, setup_ms,
  *              levels, sum_local_dofs, coarse_n] */
 int mdd_prec_stats(const mdd_prec* P, double* out8);
+/* Real flop counts of one numeric factorisation (subdomain blocks + coarse block):
+ * [0] 8 np m^2 summed over the fronts (full Gauss-Jordan elimination of every front, the figure
+ *     mdd_prec_stats reports), [1] what a partial LU of the same fronts needs (the zgetrf the
+ *     reference calls, linalg.py:92), [2] what the kernels executed in the last factorisation
+ *     (pivot-block inverse + F_PU / Schur GEMMs; a symmetric A_prec skips the F_UP GEMM and the
+ *     Schur tiles above the diagonal). */
+int mdd_prec_flop_counts(const mdd_prec* P, double* out3);
 /* 1 if the last factorisation found A_prec bitwise complex symmetric and
  * formed the packed F_UP blocks as F_PU^T (no second GEMM), else 0 */
 int mdd_prec_symmetric(const mdd_prec* P, int* sym);

@@ -168,6 +168,7 @@ SIGNATURES = {
     "mdd_prec_apply": (C.c_int, [_P, _pz, _pz]),
     "mdd_prec_coarse_apply": (C.c_int, [_P, _pz, _pz]),
     "mdd_prec_stats": (C.c_int, [_P, _pd]),
+    "mdd_prec_flop_counts": (C.c_int, [_P, _pd]),
     "mdd_prec_apply_bench": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
     "mdd_comm_unique_id": (C.c_int, [C.c_char_p]),
     "mdd_comm_create": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p, _PP]),

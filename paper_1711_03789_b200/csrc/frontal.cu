@@ -423,8 +423,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
 __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ tasks, double2* __restrict__ fronts,
-                                                 const double2* __restrict__ bbuf, const int* __restrict__ gate = nullptr) {
-  if (gate && *gate == 0) return;  // F_UP GEMM of a symmetric factorisation: k_transpose_up does it
+                                                 const double2* __restrict__ bbuf, const int* __restrict__ gate = nullptr,
+                                                 const int* __restrict__ mirror = nullptr) {
+  // gated launches are the work a symmetric factorisation does not need: the F_UP GEMM
+  // (k_transpose_up does it) and the strictly upper tiles of the Schur complement (mode 2 below)
+  if (gate && *gate == 0) return;
   extern __shared__ double2 sm[];
   constexpr int LA = kGemmKC + 4, LB = kTile + 2;  // padded leading dimensions
   const GemmTask tk = tasks[blockIdx.x];
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
 #pragma unroll
     for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
   const int nk = (K + kGemmKC - 1) / kGemmKC;
-  if (tk.mode == 1) {
+  if (tk.mode >= 1) {
     // accumulate mode: pull the output tile's old values toward L2 now, so the
     // epilogue's read-modify-write does not pay HBM latency after the K loop
     // (each thread covers its 2x4 blocks' 32-byte row segments)
@@ -513,7 +516,12 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
     }
     __syncthreads();  // stage kc&1 is refilled by the next iteration's load
   }
-  const bool acc = tk.mode == 1;
+  const bool acc = tk.mode >= 1;
+  // mode 2: a tile below the diagonal of the Schur complement F_UU -= C F_PU of a complex
+  // symmetric front (C = B^T, A^{-1} symmetric, so the product is symmetric): its transpose is
+  // the tile above the diagonal, which is then not computed at all (the gated launch).  Per
+  // store the 8 lanes of a column write 128 contiguous bytes of the mirrored row.
+  const bool mir = tk.mode == 2 && mirror && *mirror == 0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = r0 + wr + 8 * i + gid;
@@ -526,7 +534,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask* __restrict__ ta
         if (c >= N) continue;
         double2* o = Og + (int64_t)r * ldo + c;
         const double2 old = acc ? *o : make_double2(0.0, 0.0);
-        *o = make_double2(old.x - cre[i][j][e], old.y - cim[i][j][e]);
+        const double2 v = make_double2(old.x - cre[i][j][e], old.y - cim[i][j][e]);
+        *o = v;
+        if (mir) Og[(int64_t)c * ldo + r] = v;
       }
   }
 }
@@ -644,6 +654,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   uvec_total = 0;
   factor_flops = 0;
   schur_flops = 0;
+  lu_flops = exec_flops_full = exec_flops_sym = 0;
   factor_entries = 0;
   max_np = 0;
   max_m = 0;
@@ -675,6 +686,21 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
       max_m = std::max(max_m, nd.m);
       factor_flops += 8.0 * nd.np * (double)nd.m * nd.m;
       schur_flops += 8.0 * nd.np * (double)nd.nu * nd.nu;
+      {
+        // (a) what a partial LU of the front needs (zgetrf on the np pivot columns, 8 real
+        // flops per complex multiply-add): 8 sum_{k<np} (m-1-k)^2;
+        // (b) what the kernels here execute: Gauss-Jordan inverse of the pivot block (8 np^3),
+        // F_PU = A^{-1} B (8 np^2 nu), the Schur complement (8 np nu^2: all 64x64 tiles, or the
+        // tiles on and below the diagonal when the matrix is symmetric), and the F_UP GEMM
+        // (8 np^2 nu) only when it is not symmetric
+        auto sq = [](double x) { return x <= 0 ? 0.0 : x * (x + 1) * (2 * x + 1) / 6.0; };
+        const double np = nd.np, nu = nd.nu, m = nd.m;
+        lu_flops += 8.0 * (sq(m - 1) - sq(m - np - 1));
+        const double nt = (nd.nu + kTile - 1) / kTile;
+        const double lower = nu > 0 ? (nt * (nt + 1) / 2) / (nt * nt) : 0.0;
+        exec_flops_full += 8.0 * np * np * np + 16.0 * np * np * nu + 8.0 * np * nu * nu;
+        exec_flops_sym += 8.0 * np * np * np + 8.0 * np * np * nu + 8.0 * np * nu * nu * lower;
+      }
       factor_entries += (double)nd.m * nd.m - (double)nd.nu * nd.nu;
     }
   // packed F_UP rows for the solve kernels live after the fronts
@@ -762,7 +788,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   std::vector<int2> h_init, h_panel;
   std::vector<int4> h_tile;
   std::vector<int2> h_copyb;
-  std::vector<GemmTask> h_yz, h_yzup, h_s;
+  std::vector<GemmTask> h_yz, h_yzup, h_s, h_su;
   std::vector<int4> h_tr;
   std::vector<int32_t> h_act;
   std::vector<int64_t> h_woff;
@@ -781,6 +807,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   lev_yzup_off.clear();
   lev_tr_off.assign(1, 0);
   lev_s_off.assign(1, 0);
+  lev_sup_off.clear();
   int64_t bb_max = 0;
   w_max = 0;
   max_act = 0;
@@ -816,7 +843,16 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
         };
         tiles(h_yz, A, m, nd.bb_off, nu, 1, B, m, np, nu, 0);            // F_PU = -(-A^-1) B_orig
         tiles(h_yzup, C, m, A, m, 0, nd.upk_off, np, nu, np, 0);         // F_UP = -C_orig (-A^-1), packed
-        tiles(h_s, C, m, B, m, 0, D, m, nu, nu, 1);                      // F_UU -= C_orig F_PU
+        // F_UU -= C_orig F_PU: tiles on and below the diagonal always; the strictly upper tiles
+        // only for a non-symmetric matrix (gated), else they are mirrored from below (mode 2)
+        for (int r0 = 0; r0 < nu; r0 += kTile)
+          for (int c0 = 0; c0 < nu; c0 += kTile) {
+            GemmTask t{};
+            t.xo = C; t.ldx = m; t.wo = B; t.ldw = m; t.wsel = 0; t.oo = D; t.ldo = m;
+            t.M = nu; t.N = nu; t.K = np; t.r0 = r0; t.c0 = c0;
+            t.mode = r0 > c0 ? 2 : 1;
+            (c0 > r0 ? h_su : h_s).push_back(t);
+          }
         // symmetric matrices: packed F_UP = F_PU^T, 32x32 transpose tiles
         for (int r0 = 0; r0 < nu; r0 += 32)
           for (int c0 = 0; c0 < np; c0 += 32) h_tr.push_back(make_int4(g, r0, c0, 0));
@@ -829,6 +865,9 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
     h_yz.insert(h_yz.end(), h_yzup.begin(), h_yzup.end());
     h_yzup.clear();
     lev_yz_off.push_back((int64_t)h_yz.size());
+    lev_sup_off.push_back((int64_t)h_s.size());  // this level's gated (strictly upper) Schur tiles start here
+    h_s.insert(h_s.end(), h_su.begin(), h_su.end());
+    h_su.clear();
     lev_s_off.push_back((int64_t)h_s.size());
     lev_tr_off.push_back((int64_t)h_tr.size());
     // small pivot blocks: one k_gj_smem CTA per node instead of the sweeps
@@ -897,6 +936,7 @@ void FrontPlan::build(mdd_ctx* c, std::vector<MatrixInput>& mats, int32_t leaf) 
   {
     const int64_t nyz = (int64_t)h_yz.size();
     for (auto& o : lev_s_off) o += nyz;
+    for (auto& o : lev_sup_off) o += nyz;
     h_yz.insert(h_yz.end(), h_s.begin(), h_s.end());
     gemm_tasks.upload(h_yz, s);
   }
@@ -1010,9 +1050,16 @@ void FrontPlan::factor(const double2* vals, cudaStream_t s, const int* sym_flag)
       k_transpose_up<<<(unsigned)nt, dim3(32, 8), 0, s>>>(tr_tasks.p + r0t, nodes.p, fronts.p, sym_flag);
       CK_LAUNCH(ctx);
     }
-    const int64_t s0 = lev_s_off[L], nsg = lev_s_off[L + 1] - s0;
-    if (nsg) {  // deferred Schur complement
-      k_gemm<<<(unsigned)nsg, 256, kGemmSmem, s>>>(gemm_tasks.p + s0, fronts.p, bbuf.p);
+    // deferred Schur complement: lower + diagonal tiles (mirrored upwards when symmetric),
+    // then the strictly upper tiles unless the matrices are symmetric (device-side gate)
+    const int64_t s0 = lev_s_off[L], sup = lev_sup_off[L], s1 = lev_s_off[L + 1];
+    if (sup > s0) {
+      k_gemm<<<(unsigned)(sup - s0), 256, kGemmSmem, s>>>(gemm_tasks.p + s0, fronts.p, bbuf.p, nullptr, sym_flag);
+      CK_LAUNCH(ctx);
+    }
+    if (s1 > sup) {
+      if (sym_flag) k_gemm<<<(unsigned)(s1 - sup), 256, kGemmSmem, s>>>(gemm_tasks.p + sup, fronts.p, bbuf.p, sym_flag);
+      else k_gemm<<<(unsigned)(s1 - sup), 256, kGemmSmem, s>>>(gemm_tasks.p + sup, fronts.p, bbuf.p);
       CK_LAUNCH(ctx);
     }
   }

@@ -45,7 +45,8 @@ struct NodeDev {
 };
 
 // One 64x64 output tile of a batched complex GEMM on the fronts (k_gemm):
-//   mode 0: O = -X W     mode 1: O -= X W
+//   mode 0: O = -X W     mode 1: O -= X W     mode 2: as 1, and the transposed tile is written too
+//   when the factorisation is symmetric (Schur complement tiles below the diagonal)
 // X (M x K, ld ldx), W (K x N, ld ldw), O (M x N, ld ldo) as element offsets
 // into the front storage (wsel bit 0: W lives in the B_orig workspace).
 struct GemmTask {
@@ -110,7 +111,7 @@ struct FrontPlan {
   DevBuf<int2> copyb_tasks;
   DevBuf<GemmTask> gemm_tasks;
   DevBuf<double2> bbuf;
-  std::vector<int64_t> lev_copyb_off, lev_yz_off, lev_s_off;
+  std::vector<int64_t> lev_copyb_off, lev_yz_off, lev_s_off, lev_sup_off;
   // per level: start of the F_UP tiles inside the YZ range; transpose tiles
   // (symmetric fronts: packed F_UP = F_PU^T, k_transpose_up)
   std::vector<int64_t> lev_yzup_off, lev_tr_off;
@@ -119,6 +120,7 @@ struct FrontPlan {
   int32_t max_np = 0, max_m = 0, max_act = 0;
   int64_t front_total = 0, uvec_total = 0, w_max = 0;
   double factor_flops = 0, factor_entries = 0, schur_flops = 0;
+  double lu_flops = 0, exec_flops_full = 0, exec_flops_sym = 0;  // see FrontPlan::build
   // numeric storage
   DevBuf<double2> fronts, uvec, pbuf, wbuf;
   DevBuf<double> pivstat;  // per node: [min |pivot|, max |pivot|]

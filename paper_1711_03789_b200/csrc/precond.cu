@@ -1425,6 +1425,21 @@ int mdd_prec_symmetric(const mdd_prec* P, int* sym) {
   MDD_API_END
 }
 
+int mdd_prec_flop_counts(const mdd_prec* P, double* out3) {
+  MDD_API_BEGIN
+  const PrecCore& c = *P->core;
+  int f = 1;
+  if (c.sym_checked) {
+    c.symflag.download(&f, 1, c.ctx->stream);
+    CK(cudaStreamSynchronize(c.ctx->stream));
+  }
+  out3[0] = c.sub.factor_flops + c.coarse.factor_flops;
+  out3[1] = c.sub.lu_flops + c.coarse.lu_flops;
+  // the coarse block and ImpRAS local matrices are never taken as symmetric
+  out3[2] = (f == 0 ? c.sub.exec_flops_sym : c.sub.exec_flops_full) + c.coarse.exec_flops_full;
+  MDD_API_END
+}
+
 int mdd_prec_refactor(mdd_prec* P, const mdd_csr* A_prec, const mdd_coeffs* pc) {
   MDD_API_BEGIN
   CK(cudaSetDevice(P->core->ctx->device));

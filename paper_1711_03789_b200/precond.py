@@ -83,7 +83,11 @@ class _Factors:
         _lib.check(_lib.lib.mdd_prec_stats(self.handle, out))
         keys = ("n_fronts", "max_front", "factor_entries", "factor_flops", "factor_ms", "levels",
                 "sum_local_dofs", "coarse_n")
-        return dict(zip(keys, list(out)))
+        d = dict(zip(keys, list(out)))
+        fl = (C.c_double * 3)()
+        _lib.check(_lib.lib.mdd_prec_flop_counts(self.handle, fl))
+        d["lu_flops"], d["executed_flops"] = fl[1], fl[2]
+        return d
 
     def __del__(self):
         h = getattr(self, "handle", None)
