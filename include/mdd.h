@@ -117,6 +117,13 @@ typedef struct {
 int mdd_assemble(mdd_space* sp, const mdd_coeffs* co, int impedance,
                  int64_t nbf, const int64_t* bfaces,
                  mdd_csr** A, mdd_csr** S, mdd_csr** M, mdd_csr** Dk, mdd_csr** Mb);
+/* Sharded solves (no reference counterpart: the reference assembles the whole matrix in one
+ * process, fem.py:233-279): restrict the following mdd_assemble calls on this space to the
+ * cells that touch an unknown in [row_lo, row_hi) -- the rows one rank needs (its subdomains'
+ * unknowns and the columns of its owned rows, distributed.needed_rows).  Rows of the returned
+ * matrices inside the window are complete and bitwise equal to the unrestricted assembly; rows
+ * outside it are not.  row_lo < 0 (or the full range) removes the window. */
+int mdd_space_set_row_window(mdd_space* sp, int64_t row_lo, int64_t row_hi);
 /* fem.assemble_rhs (fem.py:373-390): fvals are the source values at the
  * 4-point rule's points, layout (4, nt, 3) complex; rhs is host (ndof). */
 int mdd_assemble_rhs(mdd_space* sp, const mdd_complex* fvals, mdd_complex* rhs);

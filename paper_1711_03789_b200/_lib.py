@@ -133,6 +133,7 @@ SIGNATURES = {
     ),
     "mdd_space_destroy": (None, [_P]),
     "mdd_space_nnz": (C.c_int, [_P, _pi64]),
+    "mdd_space_set_row_window": (C.c_int, [_P, _i64, _i64]),
     "mdd_assemble": (
         C.c_int,
         [_P, C.POINTER(mdd_coeffs), C.c_int, _i64, _pi64, _PP, _PP, _PP, _PP, _PP],

@@ -400,11 +400,15 @@ void assemble_system(mdd_space* sp, const mdd_coeffs* co, int impedance, int64_t
     if (co->mu) { dmu.upload(co->mu, sp->nt, s); cd.mu = dmu.p; }
     if (co->sigma) { dsig.upload(co->sigma, sp->nt, s); cd.sigma = dsig.p; }
   }
+  // a row window (sharded solve) assembles the cells that touch the rank's rows only
+  const bool win = sp->win_active;
+  const int64_t* coff = win ? sp->win_off : sp->color_off;
+  const int32_t* clist = win ? sp->win_cells.p : sp->cells_by_color.p;
   for (int c = 0; c < 8; ++c) {
-    const int64_t nc = sp->color_off[c + 1] - sp->color_off[c];
+    const int64_t nc = coff[c + 1] - coff[c];
     if (!nc) continue;
     k_assemble_cells<<<nblocks(nc * 32, 128), 128, 0, s>>>(
-        sp->cells_by_color.p + sp->color_off[c], nc, sp->verts.p, sp->tets.p, sp->tet_edges.p,
+        clist + coff[c], nc, sp->verts.p, sp->tets.p, sp->tet_edges.p,
         sp->signs.p, sp->e2d.p, sp->pat->rowptr.p, sp->pat->cols.p, cS->vals.p, cM->vals.p,
         het ? reinterpret_cast<double2*>(cA->vals.p) : nullptr, cd);
     CK_LAUNCH(ctx);
@@ -609,6 +613,47 @@ int mdd_assemble(mdd_space* sp, const mdd_coeffs* co, int impedance, int64_t nbf
   } else {
     assemble_system(sp, co, impedance, nbf, bfaces, A, S, M, Dk, Mb);
   }
+  MDD_API_END
+}
+
+int mdd_space_set_row_window(mdd_space* sp, int64_t row_lo, int64_t row_hi) {
+  MDD_API_BEGIN
+  if (row_lo < 0 || (row_lo == 0 && row_hi >= sp->ndof)) {  // reset: every cell
+    sp->win_active = false;
+    return MDD_OK;
+  }
+  if (sp->order != 1) fail(MDD_EINVAL, "row windows are implemented for lowest-order spaces");
+  if (row_hi <= row_lo || row_hi > sp->ndof) fail(MDD_EINVAL, "row window out of range");
+  if (sp->win_lo == row_lo && sp->win_hi == row_hi) {
+    sp->win_active = true;
+    return MDD_OK;
+  }
+  CK(cudaSetDevice(sp->ctx->device));
+  const int64_t ncell = sp->nt / 6;
+  // a cell is kept when one of its 36 (tet, edge) slots carries a kept unknown inside the window
+  std::vector<uint8_t> keep(ncell, 0);
+  for (int64_t c = 0; c < ncell; ++c) {
+    const int32_t* te = sp->h_tet_edges.data() + c * 36;
+    for (int q = 0; q < 36 && !keep[c]; ++q) {
+      const int32_t d = sp->h_e2d[te[q]];
+      keep[c] = d >= row_lo && d < row_hi;
+    }
+  }
+  std::vector<int32_t> h_cbc((size_t)sp->color_off[8]), list;
+  sp->cells_by_color.download(h_cbc.data(), h_cbc.size(), sp->ctx->stream);
+  CK(cudaStreamSynchronize(sp->ctx->stream));
+  list.reserve(h_cbc.size());
+  for (int col = 0; col < 8; ++col) {
+    sp->win_off[col] = (int64_t)list.size();
+    for (int64_t i = sp->color_off[col]; i < sp->color_off[col + 1]; ++i)
+      if (keep[h_cbc[i]]) list.push_back(h_cbc[i]);
+  }
+  sp->win_off[8] = (int64_t)list.size();
+  sp->win_cells.upload(list, sp->ctx->stream);
+  CK(cudaStreamSynchronize(sp->ctx->stream));
+  sp->win_lo = row_lo;
+  sp->win_hi = row_hi;
+  sp->win_active = true;
   MDD_API_END
 }
 

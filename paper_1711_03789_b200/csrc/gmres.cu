@@ -881,7 +881,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
 // iterations instead of once per iteration.  Partial blocks are summed over the CTAs in fixed
 // order by k_drift_finish.
 constexpr int kDriftP = 8;
-constexpr int kDriftR = 32;
+constexpr int kDriftR = 16;  // rows per tile, two tiles in shared memory
 constexpr int kDriftThreads = 256;  // >= maxit: one thread per older vector
 
 struct DriftArgs {
@@ -893,6 +893,7 @@ struct DriftArgs {
   double2* partial;     // gridDim.x x kDriftP x kDriftThreads
   double* drift;        // out: drift[k]
   int ncta;
+  int stage_elems;      // double2 per pipeline stage of k_drift_panel (two stages in shared memory)
 };
 
 __device__ __forceinline__ bool drift_range(const DriftArgs& a, int& k0, int& k1) {
@@ -908,6 +909,19 @@ __device__ __forceinline__ bool drift_range(const DriftArgs& a, int& k0, int& k1
   return k1 >= k0 && k1 >= 1;
 }
 
+__device__ __forceinline__ void drift_cp16(double2* dst, const double2* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// Row tiles go through a two-stage cp.async ring: the next tile's loads are in flight while
+// thread j accumulates its column of the current one.  The tile height adapts to the panel:
+// a stage holds R x (J + P) elements, so early panels (few older vectors) take hundreds of rows
+// per tile and late ones kDriftR.  (Round 2's single-buffered 32-row tiles paid a DRAM round
+// trip and two barriers per tile whatever J was: 2.1 ms for the first panel of cfg4, which reads
+// 0.5 GB, 105 ms per solve.)  Rows are accumulated in the same order as before: the drift values
+// are bitwise unchanged.
 __global__ void __launch_bounds__(kDriftThreads) k_drift_panel(DriftArgs a) {
   int k0, k1;
   if (!drift_range(a, k0, k1)) return;
@@ -916,32 +930,49 @@ __global__ void __launch_bounds__(kDriftThreads) k_drift_panel(DriftArgs a) {
   const int np = k1 - k0 + 1;       // new vectors V_{k0} .. V_{k1}
   const int Jp = J | 1;             // odd row stride: conflict-free transposed stores
   extern __shared__ double2 sm[];
-  double2* As = sm;                          // kDriftR x Jp
-  double2* Bs = sm + (size_t)kDriftR * Jp;   // kDriftR x kDriftP
+  const size_t stage_elems = (size_t)a.stage_elems;
+  const int R = max(kDriftR, min(512, (a.stage_elems / (Jp + kDriftP)) & ~15));  // rows per tile
   const int64_t slab = (a.n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = (int64_t)blockIdx.x * slab, hi = min(a.n, lo + slab);
   double2 acc[kDriftP];
 #pragma unroll
   for (int k = 0; k < kDriftP; ++k) acc[k] = make_double2(0.0, 0.0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kDriftThreads / 32;
-  for (int64_t r0 = lo; r0 < hi; r0 += kDriftR) {
-    const int nr = (int)min((int64_t)kDriftR, hi - r0);
-    __syncthreads();
-    // stage: warp w loads rows r0 .. r0+31 of vectors j = w, w+nw, ... (coalesced 512 B each)
-    for (int j = warp; j < J + np; j += nw) {
-      const double2 v = lane < nr ? __ldcg(a.V + (int64_t)(j < J ? j : k0 + (j - J)) * a.n + r0 + lane)
-                                  : make_double2(0.0, 0.0);
-      if (j < J) As[(size_t)lane * Jp + j] = v;
-      else Bs[lane * kDriftP + (j - J)] = v;
+  // stage: element e = (vector j, row r), r fastest (coalesced along the rows of one vector);
+  // rows beyond the slab are zero-filled
+  auto stage = [&](int st, int64_t r0) {
+    double2* As = sm + st * stage_elems;        // R x Jp
+    double2* Bs = As + (size_t)R * Jp;          // R x kDriftP
+    const int nr = (int)min((int64_t)R, hi - r0);
+    for (int e = threadIdx.x; e < (J + np) * R; e += kDriftThreads) {
+      const int j = e / R, r = e % R;
+      const bool ok = r < nr;
+      const double2* src = a.V + (int64_t)(j < J ? j : k0 + (j - J)) * a.n + r0 + (ok ? r : 0);
+      double2* dst = j < J ? As + (size_t)r * Jp + j : Bs + r * kDriftP + (j - J);
+      drift_cp16(dst, src, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (lo < hi) stage(0, lo);
+  int it = 0;
+  for (int64_t r0 = lo; r0 < hi; r0 += R, ++it) {
+    if (r0 + R < hi) {
+      stage((it + 1) & 1, r0 + R);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const double2* As = sm + (it & 1) * stage_elems;
+    const double2* Bs = As + (size_t)R * Jp;
     if ((int)threadIdx.x < J) {
-      for (int r = 0; r < kDriftR; ++r) {
+#pragma unroll 4
+      for (int r = 0; r < R; ++r) {
         const double2 x = As[(size_t)r * Jp + threadIdx.x];
 #pragma unroll
         for (int k = 0; k < kDriftP; ++k) acc[k] = cdotc_acc(acc[k], x, Bs[r * kDriftP + k]);
       }
     }
+    __syncthreads();  // the stage is refilled by the next iteration's loads
   }
   double2* out = a.partial + (size_t)blockIdx.x * kDriftP * kDriftThreads;
 #pragma unroll
@@ -1873,7 +1904,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   };
   const int drift_ctas = 2 * ctx->nsm;
   DevBuf<double2> drift_partial(panel_drift ? (size_t)drift_ctas * kDriftP * kDriftThreads : 1);
-  const size_t drift_smem = sizeof(double2) * ((size_t)kDriftR * (maxit | 1) + (size_t)kDriftR * kDriftP);
+  const size_t drift_smem = 2 * sizeof(double2) * ((size_t)kDriftR * (maxit | 1) + (size_t)kDriftR * kDriftP);
   if (panel_drift)
     CK(cudaFuncSetAttribute(k_drift_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)drift_smem));
   // in_loop: the kernels decide from the device iteration counter whether a panel is complete
@@ -1888,6 +1919,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     da.partial = drift_partial.p;
     da.drift = ddrift.p;
     da.ncta = drift_ctas;
+    da.stage_elems = (int)(drift_smem / (2 * sizeof(double2)));
     k_drift_panel<<<drift_ctas, kDriftThreads, drift_smem, s>>>(da);
     CK_LAUNCH(ctx);
     k_drift_finish<<<kDriftP, kDriftThreads, 0, s>>>(da);

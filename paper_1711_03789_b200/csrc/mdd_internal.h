@@ -170,6 +170,12 @@ struct mdd_space {
   // colour share an edge, so one thread per cell scatters without atomics
   mdd::DevBuf<int32_t> cells_by_color;
   int64_t color_off[9] = {0};
+  // row window of a sharded solve (mdd_space_set_row_window): the colour lists restricted to
+  // the cells that touch a row in [win_lo, win_hi); the lists stay cached while inactive
+  bool win_active = false;
+  int64_t win_lo = -1, win_hi = -1;
+  mdd::DevBuf<int32_t> win_cells;
+  int64_t win_off[9] = {0};
   // dof -> incident (tet*6 + local edge), ascending tet (rhs gather);
   // order 2: (tet*20 + local dof)
   mdd::DevBuf<int32_t> inc_ptr, inc;

@@ -511,20 +511,33 @@ def _bfaces(space: EdgeSpace) -> np.ndarray:
     return np.ascontiguousarray(space.mesh.boundary_faces, dtype=np.int64)
 
 
-def assemble(space: EdgeSpace, coeffs: Coefficients, source=None) -> SystemBundle:
-    """Device assembly of the system bundle (reference fem.py:233-279)."""
+def assemble(space: EdgeSpace, coeffs: Coefficients, source=None, rows=None) -> SystemBundle:
+    """Device assembly of the system bundle (reference fem.py:233-279).
+
+    ``rows=(lo, hi)`` (sharded solves, no reference counterpart) assembles only the cells that
+    touch an unknown in ``[lo, hi)``: those rows of the matrices are complete and bitwise equal
+    to the full assembly, the others are not to be read (``distributed.needed_rows`` gives the
+    range a rank needs).  Such an operator serves the sharded CGS2 loop, which multiplies a
+    rank's owned rows only; the MGS2 loop with a sharded preconditioner keeps whole vectors and
+    needs the whole matrix."""
     dev = space.device()
     cc, hold = coeffs.to_c(space.mesh.n_tets)
     imp = space.bc_kind == "impedance"
     bf = _bfaces(space) if imp else np.zeros((0, 3), dtype=np.int64)
     hA, hS, hM, hD, hMb = (C.c_void_p() for _ in range(5))
     try:
-        _lib.check(
-            _lib.lib.mdd_assemble(
-                dev.handle, C.byref(cc), 1 if imp else 0, len(bf), _lib.ptr(bf, C.c_int64),
-                C.byref(hA), C.byref(hS), C.byref(hM), C.byref(hD), C.byref(hMb),
+        if rows is not None:
+            _lib.check(_lib.lib.mdd_space_set_row_window(dev.handle, int(rows[0]), int(rows[1])))
+        try:
+            _lib.check(
+                _lib.lib.mdd_assemble(
+                    dev.handle, C.byref(cc), 1 if imp else 0, len(bf), _lib.ptr(bf, C.c_int64),
+                    C.byref(hA), C.byref(hS), C.byref(hM), C.byref(hD), C.byref(hMb),
+                )
             )
-        )
+        finally:
+            if rows is not None:
+                _lib.check(_lib.lib.mdd_space_set_row_window(dev.handle, -1, -1))
     except _lib.MddError as e:
         raise_for(e)
     ctx = dev.ctx

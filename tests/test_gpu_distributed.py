@@ -104,7 +104,7 @@ def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
     the one-GPU solve to the north_star tolerances."""
     import threading
 
-    from paper_1711_03789_b200 import KrylovConfig, _lib, gmres, precond
+    from paper_1711_03789_b200 import KrylovConfig, _lib, fem, gmres, precond
     from paper_1711_03789_b200.distributed import Communicator, LoopbackGroup, setup_sharded
 
     prob, d = case
@@ -128,7 +128,12 @@ def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
                 comm = Communicator(ctx, loopback=(group, r))
                 st = setup_sharded(pr, dr, spec, comm=comm)
                 applied = st.apply(v)
-                rep = gmres(pr.A, pr.rhs, precond=st, config=cfg)
+                # sharded assembly: in the sharded CGS2 loop a rank multiplies its owned rows of A
+                # only, so its operator holds the needed rows only (the MGS2 loop keeps replicated
+                # Krylov vectors and multiplies whole vectors: it needs the whole matrix)
+                assert st.assembly_rows is not None and st.assembly_rows == st.row_ranges["need"]
+                A_r = fem.assemble(pr.space, pr.coefficients, rows=st.assembly_rows).A if ortho == "cgs2" else pr.A
+                rep = gmres(A_r, pr.rhs, precond=st, config=cfg)
                 ctx.synchronize()
                 ghost = (st.row_ranges["need"][1] - st.row_ranges["need"][0]) - (st.row_ranges["own"][1] - st.row_ranges["own"][0])
                 out[r] = (len(st.shard.subdomains), applied, rep, ghost)
@@ -154,3 +159,30 @@ def test_loopback_ranks(gpu, case, nranks, ortho, fam, cor):
     assert first.converged == want.converged
     assert abs(first.iterations - want.iterations) <= 1
     assert rel(first.x, want.x) <= 1e-8
+
+
+@pytest.mark.parametrize("bc", ["pec", "impedance"])
+def test_row_window_assembly_is_bitwise_on_its_rows(gpu, bc):
+    """Sharded assembly (mdd_space_set_row_window): only the cells that touch the window are
+    assembled; the window's rows equal the full assembly bit for bit (same cells, same order),
+    rows far outside stay empty, and the window does not outlive the call."""
+    from paper_1711_03789_b200 import fem, mesh
+
+    s = fem.build_edge_space(mesh.build_cube_mesh(6), bc)
+    rng = np.random.default_rng(1)
+    co = fem.Coefficients(k=5.0, xi=2.0, eps=1 + rng.random(s.mesh.n_tets), sigma=rng.random(s.mesh.n_tets))
+    full = fem.assemble(s, co)
+    lo, hi = s.ndof // 3, s.ndof // 2
+    part = fem.assemble(s, co, rows=(lo, hi))
+    for name in ("A", "S", "M", "Dk"):
+        f, p = getattr(full, name).to_scipy().tocsr(), getattr(part, name).to_scipy().tocsr()
+        assert np.array_equal(f.indptr, p.indptr) and np.array_equal(f.indices, p.indices)
+        a, b = f.indptr[lo], f.indptr[hi]
+        assert np.array_equal(f.data[a:b], p.data[a:b]), name
+    # the first rows are more than a cell layer away from the window: nothing was assembled there
+    # (the impedance boundary term is added on every boundary face, window or not)
+    if bc == "pec":
+        Ap = part.A.to_scipy().tocsr()
+        assert not Ap.data[: Ap.indptr[10]].any()
+    again = fem.assemble(s, co)
+    assert np.array_equal(again.A.to_scipy().data, full.A.to_scipy().data)

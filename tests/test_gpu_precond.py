@@ -215,6 +215,12 @@ def test_symmetric_transpose_path_matches_gemm_path(gpu, monkeypatch):
         flags.append(f.value)
     assert flags == [1, 0]  # the assembled A_prec is bitwise symmetric; MDD_NO_SYM forces the GEMM
     assert rel(y_sym, y_gemm) <= 1e-12
+    # flop accounting (mdd_prec_flop_counts): the symmetric path skips the F_UP GEMM and the Schur
+    # tiles above the diagonal; the partial-LU count lies below the full-elimination count
+    fs, fg = st_sym.stats(), st_gemm.stats()
+    assert fs["factor_flops"] == fg["factor_flops"] and fs["lu_flops"] == fg["lu_flops"]
+    assert 0 < fs["executed_flops"] < fg["executed_flops"] <= fs["factor_flops"] * (1 + 1e-12)
+    assert 0 < fs["lu_flops"] < fs["factor_flops"]
     A = prob.A.to_scipy()
     R0 = d.coarse.R0
     ref = O.Schwarz(d.dofs, d.pou, O.minors(A, d.dofs), levels="two", R0=R0, A0=(R0 @ A @ R0.T).tocsc(),
