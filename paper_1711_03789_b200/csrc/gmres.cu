@@ -622,6 +622,35 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// Tensor memory as a scratchpad for the tail of w (E < 0).  The 256 KB of TMEM per SM are idle
+// in this kernel (no tcgen05.mma), and together with the shared-memory head they hold cfg4's
+// whole 381 KB w slice on the SM, which registers could not (the 512-thread register-tail
+// variant spilled).  Layout: a double2 is four 32-bit columns; with the 32x32b access shape
+// thread l of warp q reaches lane 32*(q%4)+l only, so the eight warps that share a lane
+// quarter take 64 columns each: 16 elements per thread, 16,384 per CTA.  Every thread only
+// ever reads back what it stored itself, so tcgen05.wait::st at the end of a sweep is the only
+// ordering needed.
+constexpr int kTmemElems = 16;  // double2 per thread
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+// the loaded registers pass through the wait, so no use of them can be scheduled above it
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])::"memory");
+}
+__device__ __forceinline__ double2 tmem_unpack(const uint32_t (&r)[4]) {
+  return make_double2(__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2]));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"((uint32_t)__double2loint(v.x)), "r"((uint32_t)__double2hiint(v.x)),
+               "r"((uint32_t)__double2loint(v.y)), "r"((uint32_t)__double2hiint(v.y))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // One sweep of the CTA's slice: w <- w - h A (axpy with X_t), acc = <B, w> (dot with X_{t+1}),
 // dacc = <B, D> (drift partner, first pass only).  Flags are compile-time so the loop body is a
 // handful of loads and DFMAs (the generic loop ran at ~150 instructions per element under the
@@ -630,13 +659,14 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 // Template parameters: T threads per CTA; E > 0: the tail of w (beyond shared memory) lives in
 // registers, E elements per thread (T x E must cover it: cfg4's 23.8k-element slices = 13.6k in
 // shared memory + 512 x 20 in registers), so w never touches the L2 and the L2 is left to the
-// basis; E = 0: the tail stays in L2 under an evict_last policy (any slice length).
+// basis; E = 0: the tail stays in L2 under an evict_last policy (any slice length); E < 0: the
+// tail lives in tensor memory (tm_ne trips of T elements, at most kTmemElems).
 template <int T, int E, bool HASB, bool HASD, bool DOWN>
 __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const double2* __restrict__ B,
                                            const double2* __restrict__ D, double2* __restrict__ WS,
                                            double2* __restrict__ wg, double2 (&W)[E > 0 ? E : 1], int ws, int len,
                                            double2 h, uint64_t pol_first, uint64_t pol_last, double2& acc,
-                                           double2& dacc) {
+                                           double2& dacc, uint32_t tm_addr, int tm_ne) {
   // piece 1: w in shared memory.  kWideU elements per thread are loaded before any is used: the
   // un-unrolled loop had one element's loads in flight per thread and ran at DRAM/L2 latency
   // per trip (ncu, profiles/r02_prof_wide_final_cfg4.ncu-rep: long scoreboard 36 warps per issue)
@@ -669,7 +699,40 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
   };
   // piece 2: the tail of w
   auto piece2 = [&]() {
-    if constexpr (E > 0) {
+    if constexpr (E < 0) {
+      // trip counts and the branches around tcgen05 instructions are CTA-uniform (.sync.aligned)
+      for (int k0 = 0; k0 < tm_ne; k0 += kWideU) {
+        double2 av[kWideU], bv[kWideU], dv[kWideU];
+        uint32_t r[kWideU][4];
+#pragma unroll
+        for (int u = 0; u < kWideU; ++u) {
+          const int k = min(k0 + u, tm_ne - 1);
+          const int e = DOWN ? tm_ne - 1 - k : k;
+          const int i = min(ws + e * T + (int)threadIdx.x, len - 1);
+          av[u] = ld_hint(A + i, pol_first);
+          if (HASB) bv[u] = __ldcg(B + i);
+          if (HASD) dv[u] = __ldcg(D + i);
+          tmem_ld4(tm_addr + 4 * e, r[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kWideU; ++u) tmem_wait_ld(r[u]);
+#pragma unroll
+        for (int u = 0; u < kWideU; ++u) {
+          if (k0 + u < tm_ne) {
+            const int e = DOWN ? tm_ne - 1 - (k0 + u) : k0 + u;
+            const int i = ws + e * T + (int)threadIdx.x;
+            const double2 wi = caxmy(tmem_unpack(r[u]), h, av[u]);
+            tmem_st4(tm_addr + 4 * e, wi);
+            if (i < len) {
+              const double2 x = HASB ? bv[u] : wi;
+              acc = cdotc_acc(acc, x, wi);
+              if (HASD) dacc = cdotc_acc(dacc, x, dv[u]);
+            }
+          }
+        }
+      }
+      tmem_wait_st();
+    } else if constexpr (E > 0) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = ws + (int)threadIdx.x + e * T;
@@ -741,6 +804,25 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
   const int ws = (int)min((int64_t)len, a.wcap);
   double2* wg = a.w + lo;
   double2 W[E > 0 ? E : 1];
+  // E < 0: the tail of w in tensor memory (all 512 columns; one CTA per SM, nobody else uses TMEM)
+  __shared__ uint32_t tm_base_s;
+  uint32_t tm_addr = 0;
+  int tm_ne = 0;
+  if constexpr (E < 0) {
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&tm_base_s)),
+                   "r"(512u)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t wq = threadIdx.x >> 5;
+    tm_addr = tm_base_s + (((wq & 3u) * 32u) << 16) + (wq >> 2) * (4u * kTmemElems);
+    tm_ne = len > ws ? (len - ws + T - 1) / T : 0;  // <= kTmemElems (checked by the host)
+  }
   const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();  // (evict_normal for the w tail: cfg4 Arnoldi 1265 -> 1290 ms)
   for (int j = threadIdx.x; j <= m; j += T) col[j] = make_double2(0.0, 0.0);
   const double2 zero = make_double2(0.0, 0.0);
@@ -764,7 +846,20 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
       acc = cdotc_acc(acc, x, wi);
       if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
     }
-    if constexpr (E > 0) {
+    if constexpr (E < 0) {
+      for (int e = 0; e < tm_ne; ++e) {
+        const int i = ws + (int)threadIdx.x + e * T;
+        double2 wi = zero;
+        if (i < len) {
+          wi = __ldcg(wg + i);
+          const double2 x = __ldcg(B + i);
+          acc = cdotc_acc(acc, x, wi);
+          if (do_drift) dacc = cdotc_acc(dacc, x, __ldcg(dvm1 + i));
+        }
+        tmem_st4(tm_addr + 4 * e, wi);
+      }
+      tmem_wait_st();
+    } else if constexpr (E > 0) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = ws + (int)threadIdx.x + e * T;
@@ -802,7 +897,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
     // chunks of X_{t+1} fetched last in pass t are then the first ones pass t+1 needs again
     const bool down = a.zigzag && (t & 1);
 #define MDD_SWEEP(HB, HD, DN) \
-  wide_sweep<T, E, HB, HD, DN>(A, B, dvm1, WS, wg, W, ws, len, h, pol_first, pol_last, acc, dacc)
+  wide_sweep<T, E, HB, HD, DN>(A, B, dvm1, WS, wg, W, ws, len, h, pol_first, pol_last, acc, dacc, tm_addr, tm_ne)
     if (!hasB) MDD_SWEEP(false, false, false);
     else if (hasD) {
       if (down) MDD_SWEEP(true, true, true);
@@ -845,7 +940,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
   if (!breakdown) {
     double2* vm = a.V + (int64_t)m * n + lo;
     double2* vin = a.vin + lo;
-    for (int i = threadIdx.x; i < (E > 0 ? ws : len); i += T) {
+    for (int i = threadIdx.x; i < (E != 0 ? ws : len); i += T) {
       // the tail's last read demotes its L2 lines (evict_first): left as evict_last they sit in
       // the L2 through the next preconditioner apply (measured: 65 ms per cfg4 solve)
       const double2 wi = i < ws ? WS[i] : ld_hint(wg + i, pol_first);
@@ -853,7 +948,20 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
       vm[i] = q;
       vin[i] = q;
     }
-    if constexpr (E > 0) {
+    if constexpr (E < 0) {
+      for (int e = 0; e < tm_ne; ++e) {
+        const int i = ws + (int)threadIdx.x + e * T;
+        uint32_t r[4];
+        tmem_ld4(tm_addr + 4 * e, r);
+        tmem_wait_ld(r);
+        if (i < len) {
+          const double2 wi = tmem_unpack(r);
+          const double2 q = make_double2(wi.x / hlast, wi.y / hlast);
+          vm[i] = q;
+          vin[i] = q;
+        }
+      }
+    } else if constexpr (E > 0) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int i = ws + (int)threadIdx.x + e * T;
@@ -864,6 +972,12 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
         }
       }
     }
+  }
+  if constexpr (E < 0) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_s), "r"(512u) : "memory");
   }
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   if (do_drift) a.drift[m - 1] = dmax;
@@ -1832,7 +1946,14 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   using ArnFn = void (*)(ArnoldiArgs);
   // (a 512-thread variant holding the tail of w in 20 registers per thread instead of L2 was
   // measured on cfg4: Arnoldi 1291 -> 1358 ms, spills and half the warps; not kept)
-  ArnFn kfn = mode == 1 ? k_arnoldi<1> : mode == 2 ? k_arnoldi_wide<kWideThreads, 0> : k_arnoldi<0>;
+  // the tail of w beyond shared memory goes to tensor memory when it fits its 16 elements per
+  // thread (cfg4: 10.2k of 16.4k), to L2 otherwise; MDD_ARN_TMEM=0 forces the L2 tail (tests, A/B)
+  const int64_t wtail = mode == 2 ? std::max<int64_t>(0, slice - wcap) : 0;
+  const bool tm_tail = wtail > 0 && wtail <= (int64_t)kTmemElems * kWideThreads &&
+                       !(getenv("MDD_ARN_TMEM") && atoi(getenv("MDD_ARN_TMEM")) == 0);
+  ArnFn kfn = mode == 1 ? k_arnoldi<1>
+              : mode == 2 ? (tm_tail ? k_arnoldi_wide<kWideThreads, -1> : k_arnoldi_wide<kWideThreads, 0>)
+                          : k_arnoldi<0>;
   const int arn_threads = mode == 2 ? kWideThreads : kArnThreads;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int per_sm = 0;

@@ -203,14 +203,18 @@ def test_arnoldi_paths_match_reference(gpu, gg, monkeypatch, mode, wcap):
     assert np.allclose(r.residual_history, base.residual_history, rtol=1e-10, atol=1e-15)
 
 
-@pytest.mark.parametrize("grid,wcap,regs", [("3", None, None), ("2", "896", "1"), ("2", "448", None), ("5", "0", "1"),
-                                            ("148", None, None)])
-def test_wide_arnoldi_matches_register_path(gpu, monkeypatch, grid, wcap, regs):
-    """k_arnoldi_wide (1024 threads per CTA, w in shared memory with an L2-resident tail,
+@pytest.mark.parametrize("grid,wcap,regs,tmem", [
+    ("3", None, None, None), ("2", "896", "1", None), ("2", "448", None, None), ("5", "0", "1", None),
+    ("1", "0", "1", None), ("2", "896", "1", "0"), ("2", "448", None, "0"), ("5", "0", "1", "0"),
+    ("148", None, None, None)])
+def test_wide_arnoldi_matches_register_path(gpu, monkeypatch, grid, wcap, regs, tmem):
+    """k_arnoldi_wide (1024 threads per CTA, w in shared memory, its tail in tensor memory --
+    tcgen05.ld/st, up to 16 elements per thread -- or, forced with MDD_ARN_TMEM=0, in L2;
     optional alternating sweep direction) on a mid-size problem with the grid capped so each
     CTA owns a long slice, against the register-path kernel on the same solve.  The cases put
-    w in shared memory only, shared + L2 tail (with and without the alternating sweep), L2 only,
-    and the production grid."""
+    w in shared memory only, shared + tail (with and without the alternating sweep), tail only
+    (one CTA: 11 of the 16 tensor-memory trips), each tail in both tiers, and the production
+    grid."""
     from paper_1711_03789_b200 import decomp, fem, mesh, precond
     from paper_1711_03789_b200.krylov import KrylovConfig, gmres
 
@@ -227,6 +231,8 @@ def test_wide_arnoldi_matches_register_path(gpu, monkeypatch, grid, wcap, regs):
         monkeypatch.setenv("MDD_ARNOLDI_WCAP", wcap)
     if regs is not None:
         monkeypatch.setenv("MDD_ARN_ZIGZAG", regs)
+    if tmem is not None:
+        monkeypatch.setenv("MDD_ARN_TMEM", tmem)
     r = gmres(prob.A, prob.rhs, precond=st, config=cfg)
     assert r.iterations == base.iterations and r.converged
     # another grid is another summation order: the histories agree to rounding amplified by

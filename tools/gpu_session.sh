@@ -43,5 +43,20 @@ sanitize)
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 3 python tools/sanitize_case.py > gpurun_out/san_$tool.log 2>&1
   echo "$tool rc=$?"; tail -n 12 gpurun_out/san_$tool.log | cut -c1-200
   ;;
+tmem)
+  # the w tail of the wide Arnoldi kernel in tensor memory vs in L2: forced-path tests, then A/B bench lines
+  timeout 900 python -m pytest tests/test_gpu_gmres.py -m gpu -q -x > gpurun_out/pytest_tmem.log 2>&1; echo "pytest rc=$?"; tail -n 3 gpurun_out/pytest_tmem.log
+  timeout 600 python bench.py --config $cfg --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_tmem_on.json 2> gpurun_out/bench_tmem_on.err; echo "tmem on rc=$?"
+  MDD_ARN_TMEM=0 timeout 600 python bench.py --config $cfg --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_tmem_off.json 2> gpurun_out/bench_tmem_off.err; echo "tmem off rc=$?"
+  python - <<'PY'
+import json
+for f in ("on", "off"):
+    try:
+        d = json.loads(open(f"gpurun_out/bench_tmem_{f}.json").read().strip().splitlines()[-1])
+        print(f, d["ms_per_step"], {k: round(v, 1) for k, v in d["phases_ms"].items() if k.startswith("gmres_")})
+    except Exception as e:
+        print(f, "failed", e)
+PY
+  ;;
 *) echo "unknown recipe $what"; exit 2;;
 esac
