@@ -74,6 +74,7 @@ struct ArnoldiArgs {
   int pf;        // REG path: L2 prefetch distance in MGS steps (kArnPf; MDD_ARN_PF)
   int zigzag;        // WIDE path: 1 = odd passes sweep the slice downwards
   int64_t pf_bytes;  // WIDE path: bytes of the next dot operand's slice prefetched into L2 during the exchange
+  int pf_trips;      // WIDE path: in-sweep L2 prefetch distance of the dot operand, in trips (0 = off)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -600,7 +601,9 @@ extern "C" int mdd_debug_arn_trace(unsigned long long* out, size_t count) {
 #define ARN_TRACE(step, which)
 #endif
 constexpr int kWideThreads = 1024;  // 32 warps x 64 registers
-constexpr int kWideU = 2;          // elements per thread with their loads in flight together
+constexpr int kWideU = 2;          // elements per thread with their loads in flight together (1024 threads)
+// loads in flight per thread: 1024 threads x 2 under the 64-register cap, 512 threads x 6 with 128
+constexpr int wide_unroll(int threads) { return threads >= 1024 ? kWideU : 6; }
 
 __device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t policy) {
   double2 v;
@@ -666,17 +669,36 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
                                            const double2* __restrict__ D, double2* __restrict__ WS,
                                            double2* __restrict__ wg, double2 (&W)[E > 0 ? E : 1], int ws, int len,
                                            double2 h, uint64_t pol_first, uint64_t pol_last, double2& acc,
-                                           double2& dacc, uint32_t tm_addr, int tm_ne) {
-  // piece 1: w in shared memory.  kWideU elements per thread are loaded before any is used: the
+                                           double2& dacc, uint32_t tm_addr, int tm_ne, int pft) {
+  constexpr int KU = wide_unroll(T);
+  // in-sweep L2 prefetch of the dot operand (its first touch: DRAM latency), pft trips ahead of
+  // the loads.  The sweep is a monotone walk over [0, len), upwards or downwards, in trips of
+  // KU*T elements; thread 0 issues one bulk prefetch per trip.
+  auto pf_at = [&](int x) {  // x: start (UP) or exclusive upper end (DOWN) of the current trip
+    if (!HASB || pft <= 0 || threadIdx.x != 0) return;
+    constexpr int c = KU * T;
+    if (DOWN) {
+      const int hi = x - pft * c;
+      if (hi > 0) {
+        const int lo = max(0, hi - c);
+        prefetch_l2(B + lo, (int64_t)(hi - lo) * 16);
+      }
+    } else {
+      const int lo = x + pft * c;
+      if (lo < len) prefetch_l2(B + lo, (int64_t)min(c, len - lo) * 16);
+    }
+  };
+  // piece 1: w in shared memory.  KU elements per thread are loaded before any is used: the
   // un-unrolled loop had one element's loads in flight per thread and ran at DRAM/L2 latency
   // per trip (ncu, profiles/r02_prof_wide_final_cfg4.ncu-rep: long scoreboard 36 warps per issue)
   auto piece1 = [&]() {
-    for (int i0 = threadIdx.x; i0 < ws; i0 += kWideU * T) {
-      double2 av[kWideU], bv[kWideU], dv[kWideU];
+    for (int i0 = threadIdx.x; i0 < ws; i0 += KU * T) {
+      pf_at(DOWN ? ws - (i0 - (int)threadIdx.x) : i0 - (int)threadIdx.x);
+      double2 av[KU], bv[KU], dv[KU];
 #pragma unroll
-      for (int u = 0; u < kWideU; ++u) {
+      for (int u = 0; u < KU; ++u) {
         // out-of-range lanes load a clamped (valid) element and are masked below: no branch
-        // around the loads, so all kWideU go out back to back
+        // around the loads, so all KU go out back to back
         const int iu = min(i0 + u * T, ws - 1);
         const int i = DOWN ? ws - 1 - iu : iu;
         av[u] = ld_hint(A + i, pol_first);
@@ -684,7 +706,7 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
         if (HASD) dv[u] = __ldcg(D + i);
       }
 #pragma unroll
-      for (int u = 0; u < kWideU; ++u) {
+      for (int u = 0; u < KU; ++u) {
         const int iu = i0 + u * T;
         if (iu < ws) {
           const int i = DOWN ? ws - 1 - iu : iu;
@@ -701,11 +723,12 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
   auto piece2 = [&]() {
     if constexpr (E < 0) {
       // trip counts and the branches around tcgen05 instructions are CTA-uniform (.sync.aligned)
-      for (int k0 = 0; k0 < tm_ne; k0 += kWideU) {
-        double2 av[kWideU], bv[kWideU], dv[kWideU];
-        uint32_t r[kWideU][4];
+      for (int k0 = 0; k0 < tm_ne; k0 += KU) {
+        pf_at(DOWN ? min(len, ws + (tm_ne - k0) * T) : ws + k0 * T);
+        double2 av[KU], bv[KU], dv[KU];
+        uint32_t r[KU][4];
 #pragma unroll
-        for (int u = 0; u < kWideU; ++u) {
+        for (int u = 0; u < KU; ++u) {
           const int k = min(k0 + u, tm_ne - 1);
           const int e = DOWN ? tm_ne - 1 - k : k;
           const int i = min(ws + e * T + (int)threadIdx.x, len - 1);
@@ -715,9 +738,9 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
           tmem_ld4(tm_addr + 4 * e, r[u]);
         }
 #pragma unroll
-        for (int u = 0; u < kWideU; ++u) tmem_wait_ld(r[u]);
+        for (int u = 0; u < KU; ++u) tmem_wait_ld(r[u]);
 #pragma unroll
-        for (int u = 0; u < kWideU; ++u) {
+        for (int u = 0; u < KU; ++u) {
           if (k0 + u < tm_ne) {
             const int e = DOWN ? tm_ne - 1 - (k0 + u) : k0 + u;
             const int i = ws + e * T + (int)threadIdx.x;
@@ -749,10 +772,10 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
         }
       }
     } else {
-      for (int i0 = ws + threadIdx.x; i0 < len; i0 += kWideU * T) {
-        double2 av[kWideU], bv[kWideU], dv[kWideU], wv[kWideU];
+      for (int i0 = ws + threadIdx.x; i0 < len; i0 += KU * T) {
+        double2 av[KU], bv[KU], dv[KU], wv[KU];
 #pragma unroll
-        for (int u = 0; u < kWideU; ++u) {
+        for (int u = 0; u < KU; ++u) {
           const int iu = min(i0 + u * T, len - 1);
           const int i = DOWN ? len - 1 - (iu - ws) : iu;
           av[u] = ld_hint(A + i, pol_first);
@@ -761,7 +784,7 @@ __device__ __forceinline__ void wide_sweep(const double2* __restrict__ A, const 
           if (HASD) dv[u] = __ldcg(D + i);
         }
 #pragma unroll
-        for (int u = 0; u < kWideU; ++u) {
+        for (int u = 0; u < KU; ++u) {
           const int iu = i0 + u * T;
           if (iu < len) {
             const int i = DOWN ? len - 1 - (iu - ws) : iu;
@@ -820,7 +843,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t wq = threadIdx.x >> 5;
-    tm_addr = tm_base_s + (((wq & 3u) * 32u) << 16) + (wq >> 2) * (4u * kTmemElems);
+    tm_addr = tm_base_s + (((wq & 3u) * 32u) << 16) + (wq >> 2) * (4u * kTmemElems * (1024 / T));
     tm_ne = len > ws ? (len - ws + T - 1) / T : 0;  // <= kTmemElems (checked by the host)
   }
   const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();  // (evict_normal for the w tail: cfg4 Arnoldi 1265 -> 1290 ms)
@@ -897,7 +920,7 @@ __global__ void __launch_bounds__(T, 1) k_arnoldi_wide(ArnoldiArgs a) {
     // chunks of X_{t+1} fetched last in pass t are then the first ones pass t+1 needs again
     const bool down = a.zigzag && (t & 1);
 #define MDD_SWEEP(HB, HD, DN) \
-  wide_sweep<T, E, HB, HD, DN>(A, B, dvm1, WS, wg, W, ws, len, h, pol_first, pol_last, acc, dacc, tm_addr, tm_ne)
+  wide_sweep<T, E, HB, HD, DN>(A, B, dvm1, WS, wg, W, ws, len, h, pol_first, pol_last, acc, dacc, tm_addr, tm_ne, a.pf_trips)
     if (!hasB) MDD_SWEEP(false, false, false);
     else if (hasD) {
       if (down) MDD_SWEEP(true, true, true);
@@ -1951,6 +1974,7 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   const int64_t wtail = mode == 2 ? std::max<int64_t>(0, slice - wcap) : 0;
   const bool tm_tail = wtail > 0 && wtail <= (int64_t)kTmemElems * kWideThreads &&
                        !(getenv("MDD_ARN_TMEM") && atoi(getenv("MDD_ARN_TMEM")) == 0);
+  // (512 threads x 6 loads in flight with the tensor-memory tail: cfg4 Arnoldi 901 -> 967 ms; not kept)
   ArnFn kfn = mode == 1 ? k_arnoldi<1>
               : mode == 2 ? (tm_tail ? k_arnoldi_wide<kWideThreads, -1> : k_arnoldi_wide<kWideThreads, 0>)
                           : k_arnoldi<0>;
@@ -2002,6 +2026,10 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
   {
     // what DRAM delivers during one exchange (~4 us at ~6 TB/s), spread over the CTAs
     aa.pf_bytes = (int64_t)(24e6 / G) & ~(int64_t)127;
+    // (measured on cfg4 with the tensor-memory tail, Arnoldi ms per solve: no head prefetch 979,
+    // 162 KB per CTA 901, the whole 381 KB slice 952)
+    // in-sweep prefetch distance: off 901, 2 trips 921, 4 trips 876; MDD_ARN_PF_TRIPS overrides
+    aa.pf_trips = getenv("MDD_ARN_PF_TRIPS") ? atoi(getenv("MDD_ARN_PF_TRIPS")) : (tm_tail ? 4 : 0);
     // vectors that the L2 cannot keep whole between their two uses are swept in alternating
     // directions (cfg4: 56 MB; measured 1508 -> 1350 ms per solve; cfg3's 24 MB vectors lose 10%)
     aa.zigzag = (n * 16 > 40000000ll || getenv("MDD_ARN_ZIGZAG")) ? 1 : 0;  // env: test hook

@@ -58,5 +58,32 @@ for f in ("on", "off"):
         print(f, "failed", e)
 PY
   ;;
+quick)
+  # parity tests of the solve path and the config goldens, then one short bench line (no CPU leg)
+  timeout 1200 python -m pytest tests/test_gpu_precond.py tests/test_gpu_config_goldens.py tests/test_gpu_configs.py -m gpu -q -x > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"; tail -n 3 gpurun_out/pytest_quick.log
+  timeout 600 python bench.py --config $cfg --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err; echo "bench rc=$?"
+  python - <<'PY'
+import json
+d = json.loads(open("gpurun_out/bench_quick.json").read().strip().splitlines()[-1])
+print(d["ms_per_step"], {k: round(v, 1) for k, v in d["phases_ms"].items()})
+print({k: (round(v["frac"], 3), round(v["ms_per_launch"], 3)) for k, v in d["roofline_all"].items()})
+PY
+  ;;
+arnsweep)
+  # experiment knobs of the wide Arnoldi kernel, one short bench line each ("VAR=val" strings in $3..)
+  shift 2
+  for v in "" "$@"; do
+    tag=$(echo "${v:-base}" | tr ' =' '__')
+    env $v timeout 600 python bench.py --config $cfg --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_arn_$tag.json 2> gpurun_out/bench_arn_$tag.err
+    python - "$tag" <<'PY'
+import json, sys
+try:
+    d = json.loads(open(f"gpurun_out/bench_arn_{sys.argv[1]}.json").read().strip().splitlines()[-1])
+    print(sys.argv[1], round(d["ms_per_step"], 1), "arnoldi", round(d["phases_ms"]["gmres_arnoldi"], 1), "precond", round(d["phases_ms"]["gmres_precond"], 1), "final", d.get("final_rel_residual"))
+except Exception as e:
+    print(sys.argv[1], "failed", e)
+PY
+  done
+  ;;
 *) echo "unknown recipe $what"; exit 2;;
 esac
