@@ -2032,7 +2032,8 @@ extern "C" int mdd_gmres(mdd_ctx* ctx, const mdd_gmres_ops* ops, int64_t n, cons
     aa.pf_trips = getenv("MDD_ARN_PF_TRIPS") ? atoi(getenv("MDD_ARN_PF_TRIPS")) : (tm_tail ? 4 : 0);
     // vectors that the L2 cannot keep whole between their two uses are swept in alternating
     // directions (cfg4: 56 MB; measured 1508 -> 1350 ms per solve; cfg3's 24 MB vectors lose 10%)
-    aa.zigzag = (n * 16 > 40000000ll || getenv("MDD_ARN_ZIGZAG")) ? 1 : 0;  // env: test hook
+    aa.zigzag = n * 16 > 40000000ll ? 1 : 0;
+    if (const char* e = getenv("MDD_ARN_ZIGZAG")) aa.zigzag = atoi(e) != 0;  // test hook / A-B runs
   }
 
   auto launch_arnoldi = [&](const ArnoldiArgs& args) {
