@@ -32,6 +32,15 @@ arnoldi)
       -o gpurun_out/prof_arnoldi_cfg$cfg -f python tools/prof_arnoldi.py $cfg 120 > gpurun_out/arn_ncu.log 2>&1
   echo "ncu rc=$?"; tail -n 2 gpurun_out/arn_plain.log gpurun_out/arn_ncu.log
   ;;
+applyncu)
+  # ncu --set full of the preconditioner-apply kernels (k_solve_tma levels, k_level_gather, k_scatter_owner) of one apply at cfgN
+  # (cfg1 by default: at cfg4 ncu cannot save/restore the 46 GB of factors per pass)
+  CFG=$cfg APPLIES=2 timeout 600 python tools/profile_apply.py > gpurun_out/apply_plain.log 2>&1 || { echo "plain run failed"; tail -n 5 gpurun_out/apply_plain.log; exit 1; }
+  CFG=$cfg APPLIES=2 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'k_solve_tma|k_level_gather|k_scatter_owner' -c ${3:-60} \
+      -o gpurun_out/prof_apply_cfg$cfg -f python tools/profile_apply.py > gpurun_out/apply_ncu.log 2>&1
+  echo "ncu rc=$?"; tail -n 2 gpurun_out/apply_plain.log gpurun_out/apply_ncu.log | cut -c1-300
+  ncu -i gpurun_out/prof_apply_cfg$cfg.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,smsp__average_warp_latency_issue_stalled_long_scoreboard.pct,smsp__average_warp_latency_issue_stalled_barrier.pct > gpurun_out/prof_apply_cfg${cfg}_raw.csv 2>&1
+  ;;
 emulate)
   timeout 1500 python tools/rank_emulation.py --config $cfg --ranks 1,2,4,8 --sample-ranks 2 --steps 1 > gpurun_out/rank_emulation_cfg$cfg.log 2>&1
   echo "rc=$?"; tail -n 12 gpurun_out/rank_emulation_cfg$cfg.log | cut -c1-300
